@@ -1,0 +1,240 @@
+/*
+ * gmask.h — C ABI of libgmask.so, the B200-native token-mask engine.
+ *
+ * This is the drop-in boundary for the reference's token-mask hot path
+ * (grammask, /root/reference/pkg/src/grammask).  Every entry point names the
+ * reference interface it replaces (REF = /root/reference/pkg/src/grammask).
+ * The Python host layer (paper_2411_15100_b200/_lib.py) binds these with
+ * ctypes; INTEGRATION.md shows the binding a maintainer of the reference
+ * would add.
+ *
+ * Conventions
+ *   - plain C types only: pointers + sizes, no torch types.
+ *   - "device pointer" arguments are CUDA global-memory addresses owned by
+ *     the caller (torch tensors in the Python layer); "host pointer"
+ *     arguments are ordinary host memory.
+ *   - all kernel launches are stream-ordered on the given cudaStream_t
+ *     (passed as void* so the header needs no CUDA include); 0 = legacy
+ *     default stream.  No call on the per-step path allocates memory or
+ *     synchronises the stream, except where documented ("syncs").
+ *   - every function returns gm_status; on failure gm_last_error() returns a
+ *     thread-local message.
+ *   - handles (gm_vocab, gm_grammar, gm_cache, gm_pool) are library-owned and
+ *     released with the matching *_release.
+ */
+#ifndef GMASK_H_
+#define GMASK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t gm_status;
+enum {
+  GM_OK = 0,
+  GM_ERR_INVALID = 1,     /* bad argument (MatcherError/ValueError in Python)   */
+  GM_ERR_CUDA = 2,        /* CUDA runtime failure                               */
+  GM_ERR_STATE_CAP = 3,   /* stack/branch set exceeded its cap (REF pda.py:53-57,
+                             cache.py:137-138, matcher.py:188-189)               */
+  GM_ERR_TERMINATED = 4,  /* matcher terminated (REF matcher.py:251-252, 379-381) */
+  GM_ERR_SHAPE = 5,       /* mask/bitmask shape mismatch (REF matcher.py:382-383) */
+  GM_ERR_ARENA_FULL = 6,  /* device stack arena exhausted                        */
+  GM_ERR_ROLLBACK = 7,    /* rollback beyond history (REF matcher.py:313-314)    */
+  GM_ERR_OOM = 8
+};
+
+/* Thread-local description of the last failure on this thread. */
+const char* gm_last_error(void);
+const char* gm_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* K0: apply_token_bitmask_inplace                                           */
+/* ------------------------------------------------------------------------ */
+/* Replaces XGrammar's apply_token_bitmask_inplace
+ * (xgrammar/matcher.py:58-188; absent in the reference — grammask never
+ * touches logits, REF bench.py:50-71).  For every row r (r = indices[i] when
+ * indices != NULL, else r = i for i < n_rows) and every token j < vocab_size:
+ *     bit j of bitmask[r] == 0  =>  logits[r, j] = -inf
+ * allowed logits are left bit-identical.  dtype: GM_DTYPE_*.  logits and
+ * bitmask are device pointers; strides are in elements. */
+enum { GM_DTYPE_F32 = 0, GM_DTYPE_F16 = 1, GM_DTYPE_BF16 = 2 };
+gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_rows,
+                           int64_t vocab_size, int64_t logits_stride,
+                           const int32_t* bitmask, int64_t bitmask_stride,
+                           const int32_t* indices, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Vocabulary                                                                */
+/* ------------------------------------------------------------------------ */
+/* Replaces Vocabulary + SortedVocabIndex (REF vocab.py:111-134, 203-234).
+ * bytes/offsets are host pointers: token i = bytes[offsets[i]:offsets[i+1]].
+ * special must contain eos_id (REF vocab.py:141).  The library uploads the
+ * token bytes, the lexicographic order of non-special non-empty tokens
+ * (ties by id, REF vocab.py:227-234) and the universe bitset (non-special,
+ * non-empty tokens, REF matcher.py:141-144) to the current device. */
+typedef struct gm_vocab gm_vocab;
+gm_status gm_vocab_create(const uint8_t* bytes, const int64_t* offsets,
+                          int32_t vocab_size, const int32_t* special,
+                          int32_t n_special, int32_t eos_id, gm_vocab** out);
+void gm_vocab_release(gm_vocab* v);
+int32_t gm_vocab_size(const gm_vocab* v);
+/* Device pointer to the universe row (ceil(V/32) int32 words). */
+const int32_t* gm_vocab_universe(const gm_vocab* v);
+
+/* ------------------------------------------------------------------------ */
+/* Grammar tables (output of the host front end)                             */
+/* ------------------------------------------------------------------------ */
+/* The front end (paper_2411_15100_b200/automaton.py) lowers grammar text to a
+ * byte-level pushdown automaton whose silent moves (epsilon, rule push,
+ * frame-internal pop) are pre-closed into per-(node, byte-class) transition
+ * lists.  A transition (target, push run) means: push the return nodes
+ * push_pool[off .. off+len) in order, then rest on `target`.
+ * node_flags: GM_NODE_POP   = node can silently complete its rule (pop the
+ *                             frame), the SC(n) fact of SURVEY §7;
+ *             GM_NODE_DEAD_END = final node with no moves except the pop
+ *                             (REF pda.py:131-134).
+ * follow_* is the context-expansion automaton (REF cache.py:241-333) as a
+ * DFA over byte classes: state -1 = dead, -2 = wildcard (anything follows). */
+enum { GM_NODE_POP = 1, GM_NODE_DEAD_END = 2 };
+enum { GM_FOLLOW_DEAD = -1, GM_FOLLOW_ANY = -2 };
+typedef struct gm_grammar_tables {
+  int32_t n_nodes;
+  int32_t n_rules;
+  int32_t n_classes;
+  int32_t start_node;          /* root rule start                              */
+  const uint8_t* byte_class;   /* [256]                                        */
+  const int32_t* trans_off;    /* [n_nodes*n_classes + 1] CSR offsets          */
+  const int32_t* trans;        /* [2*n_trans]: target, push_off | push_len<<24 */
+  int32_t n_trans;
+  const int32_t* push_pool;    /* [n_push] return nodes                        */
+  int32_t n_push;
+  const uint8_t* node_flags;   /* [n_nodes]                                    */
+  const int32_t* node_rule;    /* [n_nodes]                                    */
+  const int32_t* cache_keys;   /* [n_keys] resting nodes (cache key set),
+                                  REF pda.py:601-632                           */
+  int32_t n_keys;
+  const int32_t* follow_start; /* [n_rules]                                    */
+  const int32_t* follow_next;  /* [n_fstates*n_classes]                        */
+  int32_t n_fstates;
+} gm_grammar_tables;
+
+typedef struct gm_grammar gm_grammar;
+/* Copies the (host) tables to the current device. */
+gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out);
+void gm_grammar_release(gm_grammar* g);
+
+/* ------------------------------------------------------------------------ */
+/* K1/K1b: adaptive token-mask cache build                                   */
+/* ------------------------------------------------------------------------ */
+/* Replaces build_mask_cache / sweep / FollowFsa refinement
+ * (REF cache.py:88-193, 241-333, 516-574).  For each key index k in
+ * [key_begin, key_begin+n) (into tables.cache_keys) and every non-special,
+ * non-empty token t, classifies t from a synthetic single-frame stack at the
+ * key node: accepted (bit set in acc_rows[k-key_begin]), context dependent
+ * after context expansion (bit set in dep_rows[k-key_begin]) or rejected
+ * (neither bit).  acc_rows/dep_rows are device [n x ceil(V/32)] int32,
+ * zero-filled by this call.  Position sharding across GPUs = disjoint
+ * [key_begin, key_begin+n) ranges, then an all-gather of the rows. */
+gm_status gm_cache_build_rows(const gm_grammar* g, const gm_vocab* v,
+                              int32_t key_begin, int32_t n,
+                              int32_t* acc_rows, int32_t* dep_rows,
+                              void* stream);
+
+/* Assemble a cache from complete rows for all keys (device pointers; the
+ * rows are copied).  Dependent bit rows are compacted to sorted id lists
+ * (REF cache.py:400-402).  Syncs the stream. */
+typedef struct gm_cache gm_cache;
+typedef struct gm_cache_stats {
+  int32_t n_keys;
+  int64_t accepted_total;   /* REF cache.py:423-437 BuildStats */
+  int64_t dependent_total;
+  int64_t rejected_total;
+  int64_t row_bytes;        /* dense rows resident in HBM */
+} gm_cache_stats;
+gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v,
+                          const int32_t* acc_rows, const int32_t* dep_rows,
+                          gm_cache** out, gm_cache_stats* stats, void* stream);
+void gm_cache_release(gm_cache* c);
+/* Export for inspection / GMC1 serialisation: copies the accepted rows
+ * [n_keys x W], dependent offsets [n_keys+1] and dependent ids [n_dep] into
+ * caller device buffers (each nullable).  Syncs. */
+gm_status gm_cache_export(const gm_cache* c, int32_t* acc_rows_out, int32_t* dep_off_out,
+                          int32_t* dep_ids_out, int64_t* n_dep_out);
+
+/* ------------------------------------------------------------------------ */
+/* Matcher pool: device-resident persistent stacks                           */
+/* ------------------------------------------------------------------------ */
+/* Replaces Matcher state + StackArena (REF matcher.py:103-154, 239-355,
+ * pstack.py:24-111).  A pool holds `capacity` matcher slots.  Every slot
+ * keeps a ring of (history_window+1) stack-top sets of at most max_stacks
+ * (handle, node) pairs; handles index a device hash-consed arena of
+ * (parent, return-node) frames shared by all slots (equal content => equal
+ * handle, so branch/rollback cost one handle copy per stack). */
+typedef struct gm_pool gm_pool;
+gm_status gm_pool_create(int32_t capacity, int32_t max_stacks,
+                         int32_t max_window, int64_t arena_log2,
+                         gm_pool** out);
+void gm_pool_release(gm_pool* p);
+
+/* Bind slot to (grammar, cache, vocab) and reset it to the start state
+ * (REF matcher.py:154).  window = rollback history length for this slot. */
+gm_status gm_pool_reset(gm_pool* p, int32_t slot, const gm_grammar* g,
+                        const gm_cache* c, const gm_vocab* v, int32_t window,
+                        void* stream);
+/* Copy slot src to dst, history included (REF matcher.py:328-355 branch). */
+gm_status gm_pool_fork(gm_pool* p, int32_t src, int32_t dst, void* stream);
+
+/* K4: batched accept_token.  slots/token_ids are device int32[n];
+ * accepted_out device uint8[n] (1 = accepted).  Semantics of REF
+ * matcher.py:273-294: EOS terminates iff terminable; special or empty
+ * tokens are rejected; a rejected token leaves the slot unchanged. */
+gm_status gm_accept_tokens(gm_pool* p, const int32_t* slots,
+                           const int32_t* token_ids, int32_t n,
+                           uint8_t* accepted_out, void* stream);
+/* accept_bytes / accept_string for one slot (REF matcher.py:248-271);
+ * data is a host pointer; the result is written to accepted_out (device). */
+gm_status gm_accept_bytes(gm_pool* p, int32_t slot, const uint8_t* data,
+                          int64_t len, uint8_t* accepted_out, void* stream);
+
+/* K2: batched fill_next_token_bitmask.  For i < n: row = rows ? rows[i] : i,
+ * bitmask[row] (device, int32, row stride bitmask_stride) receives the
+ * permitted-token mask of slots[i] (REF matcher.py:377-444): universe AND
+ * union over stacks of (cached accepted row OR walked dependents), EOS bit
+ * iff terminable, bits >= V zero.  need_apply_out[i] (nullable, device
+ * uint8) = mask is not all-ones over the vocabulary. */
+gm_status gm_fill_tokens(gm_pool* p, const int32_t* slots, int32_t n,
+                         int32_t* bitmask, int64_t bitmask_stride,
+                         const int32_t* rows, uint8_t* need_apply_out,
+                         void* stream);
+
+/* rollback `steps` acceptances of each slot (REF matcher.py:310-326);
+ * slots/steps are device int32[n]. */
+gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps,
+                      int32_t n, void* stream);
+
+/* Introspection (syncs).  info = {n_stacks, terminated, history_len,
+ * terminable, window}; stacks_out (nullable) receives up to max_out
+ * (handle, node) pairs of the current top set. */
+gm_status gm_pool_slot_info(gm_pool* p, int32_t slot, int32_t* info5,
+                            int32_t* stacks_out, int32_t max_out);
+/* Materialise a stack: frames bottom-up into out (host), returns depth via
+ * *depth (REF pstack.py:70-77). */
+gm_status gm_pool_materialize(gm_pool* p, int32_t handle, int32_t* out,
+                              int32_t max_out, int32_t* depth);
+/* Union of acceptable first bytes (256-bit, 8 words) and terminability over
+ * the closure of the slot's current stacks (REF matcher.py:219-237); used
+ * by jump-forward (REF matcher.py:464-486).  Syncs. */
+gm_status gm_pool_first_bytes(gm_pool* p, int32_t slot, uint32_t* bytes8,
+                              int32_t* terminable);
+/* Sticky device error flags of the pool (GM_ERR_* bit set), cleared by the
+ * read.  Syncs. */
+gm_status gm_pool_check(gm_pool* p, int32_t* flags_out);
+/* arena statistics: live entries */
+int64_t gm_pool_arena_used(gm_pool* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GMASK_H_ */

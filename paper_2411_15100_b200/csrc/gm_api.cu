@@ -1,0 +1,530 @@
+// Host side of the C ABI: object lifetimes, uploads, the sorted vocabulary
+// index, cache assembly and the matcher pool.  All compute is in the
+// k_*.cu kernels; nothing here runs on the per-step path except argument
+// marshalling and kernel launches.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+
+namespace gm {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+gm_status fail(gm_status code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+// kernel launchers (k_*.cu)
+gm_status launch_cache_build(const DevGrammar&, const DevVocab&, const DevArena&, int32_t, int32_t,
+                             uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+gm_status launch_row_popcount(const uint32_t*, int32_t, int32_t, int64_t*, cudaStream_t);
+gm_status launch_dep_compact(const uint32_t*, int32_t, int32_t, const int32_t*, int32_t*, cudaStream_t);
+gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*,
+                      uint8_t*, int32_t, cudaStream_t);
+gm_status launch_accept_tokens(const DevPool&, const int32_t*, const int32_t*, int32_t, uint8_t*, cudaStream_t);
+gm_status launch_accept_bytes(const DevPool&, int32_t, const uint8_t*, int64_t, uint8_t*, cudaStream_t);
+gm_status launch_reset(const DevPool&, int32_t, const DevBinding*, int32_t, int32_t, cudaStream_t);
+gm_status launch_rollback(const DevPool&, const int32_t*, const int32_t*, int32_t, cudaStream_t);
+gm_status launch_probe(const DevPool&, int32_t, int32_t*, int2*, int32_t, uint32_t*, cudaStream_t);
+
+// RAII-less device buffer list: every object frees what it allocated.
+struct DevAllocs {
+  std::vector<void*> ptrs;
+  template <class T>
+  gm_status alloc(T** p, size_t count) {
+    void* q = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&q, count * sizeof(T));
+    if (e != cudaSuccess) return fail(GM_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    ptrs.push_back(q);
+    *p = static_cast<T*>(q);
+    return GM_OK;
+  }
+  template <class T>
+  gm_status upload(T** p, const T* host, size_t count) {
+    gm_status st = alloc(p, count);
+    if (st) return st;
+    if (count) GM_CUDA_TRY(cudaMemcpy(*p, host, count * sizeof(T), cudaMemcpyHostToDevice));
+    return GM_OK;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+// scratch arena for cache builds (walker frame overflow only), per process
+static DevArena g_build_arena{nullptr, 0, nullptr};
+static gm_status build_arena(DevArena* out) {
+  if (!g_build_arena.keys) {
+    const uint32_t cap = 1u << 20;
+    unsigned long long* keys = nullptr;
+    uint32_t* err = nullptr;
+    GM_CUDA_TRY(cudaMalloc(&keys, sizeof(unsigned long long) * cap));
+    GM_CUDA_TRY(cudaMemset(keys, 0xFF, sizeof(unsigned long long) * cap));
+    GM_CUDA_TRY(cudaMalloc(&err, sizeof(uint32_t)));
+    GM_CUDA_TRY(cudaMemset(err, 0, sizeof(uint32_t)));
+    g_build_arena = DevArena{keys, cap - 1, err};
+  }
+  *out = g_build_arena;
+  return GM_OK;
+}
+
+static gm_status err_bits_to_status(uint32_t bits, const char* where) {
+  if (!bits) return GM_OK;
+  std::string w(where);
+  if (bits & kErrCap) return fail(GM_ERR_STATE_CAP, w + ": stack set exceeded cap");
+  if (bits & kErrArena) return fail(GM_ERR_ARENA_FULL, w + ": device stack arena is full");
+  if (bits & kErrTerminated) return fail(GM_ERR_TERMINATED, w + ": matcher is terminated");
+  if (bits & (1u << GM_ERR_ROLLBACK)) return fail(GM_ERR_ROLLBACK, w + ": cannot roll back beyond history");
+  if (bits & kErrInvalid) return fail(GM_ERR_INVALID, w + ": token id out of range");
+  return fail(GM_ERR_INVALID, w + ": device error");
+}
+
+}  // namespace gm
+
+using namespace gm;
+
+// ---------------------------------------------------------------------------
+struct gm_vocab {
+  DevAllocs mem;
+  DevVocab dev;
+  std::vector<uint32_t> universe_host;
+};
+
+struct gm_grammar {
+  DevAllocs mem;
+  DevGrammar dev;
+  std::vector<int32_t> keys;
+};
+
+struct gm_cache {
+  DevAllocs mem;
+  DevBinding host_binding;
+  DevBinding* binding;  // device copy
+  int32_t n_keys;
+};
+
+struct gm_pool {
+  DevAllocs mem;
+  DevPool dev;
+  uint8_t* scratch_bytes;  // accept_bytes staging
+  int64_t scratch_cap;
+  int32_t* scratch_i32;    // probe outputs
+  int32_t max_w;
+};
+
+extern "C" {
+
+const char* gm_last_error(void) { return g_last_error.c_str(); }
+const char* gm_version(void) { return "gmask-b200 0.1 (sm_100a)"; }
+
+// ---------------------------------------------------------------------------
+// Vocabulary: REF vocab.py:111-134 (tokens/specials/eos), 227-234 (sorted
+// index, ties by id), matcher.py:141-144 (universe).
+
+gm_status gm_vocab_create(const uint8_t* bytes, const int64_t* offsets, int32_t V, const int32_t* special,
+                          int32_t n_special, int32_t eos_id, gm_vocab** out) {
+  if (V <= 0 || !offsets || !out) return fail(GM_ERR_INVALID, "bad vocabulary arguments");
+  if (eos_id < 0 || eos_id >= V) return fail(GM_ERR_INVALID, "eos_id outside vocabulary");
+  if (offsets[V] > INT32_MAX) return fail(GM_ERR_INVALID, "vocabulary bytes exceed 2 GiB");
+  std::vector<uint8_t> is_special(V, 0);
+  for (int32_t i = 0; i < n_special; ++i) {
+    if (special[i] < 0 || special[i] >= V) return fail(GM_ERR_INVALID, "special token id outside vocabulary");
+    is_special[special[i]] = 1;
+  }
+  is_special[eos_id] = 1;
+  const int32_t W = (V + 31) / 32;
+  std::vector<int32_t> off32(V + 1);
+  for (int32_t i = 0; i <= V; ++i) off32[i] = (int32_t)offsets[i];
+  std::vector<uint8_t> reject(V, 0);
+  std::vector<uint32_t> universe(W, 0);
+  std::vector<int32_t> ids;
+  ids.reserve(V);
+  for (int32_t t = 0; t < V; ++t) {
+    const bool empty = offsets[t + 1] == offsets[t];
+    reject[t] = (is_special[t] || empty) ? 1 : 0;
+    if (!reject[t]) {
+      universe[t >> 5] |= 1u << (t & 31);
+      ids.push_back(t);
+    }
+  }
+  std::sort(ids.begin(), ids.end(), [&](int32_t a, int32_t b) {
+    const uint8_t* pa = bytes + offsets[a];
+    const uint8_t* pb = bytes + offsets[b];
+    const int64_t la = offsets[a + 1] - offsets[a], lb = offsets[b + 1] - offsets[b];
+    const int c = std::memcmp(pa, pb, (size_t)std::min(la, lb));
+    if (c != 0) return c < 0;
+    if (la != lb) return la < lb;
+    return a < b;
+  });
+  gm_vocab* v = new gm_vocab();
+  gm_status st;
+  uint8_t* d_bytes;
+  int32_t *d_off, *d_sorted;
+  uint32_t* d_univ;
+  uint8_t* d_rej;
+  if ((st = v->mem.upload(&d_bytes, bytes, (size_t)offsets[V])) ||
+      (st = v->mem.upload(&d_off, off32.data(), off32.size())) ||
+      (st = v->mem.upload(&d_sorted, ids.data(), ids.size())) ||
+      (st = v->mem.upload(&d_univ, universe.data(), universe.size())) ||
+      (st = v->mem.upload(&d_rej, reject.data(), reject.size()))) {
+    v->mem.release();
+    delete v;
+    return st;
+  }
+  v->dev = DevVocab{V, W, (int32_t)ids.size(), eos_id, d_bytes, d_off, d_sorted, d_univ, d_rej};
+  v->universe_host = std::move(universe);
+  *out = v;
+  return GM_OK;
+}
+
+void gm_vocab_release(gm_vocab* v) {
+  if (!v) return;
+  v->mem.release();
+  delete v;
+}
+int32_t gm_vocab_size(const gm_vocab* v) { return v ? v->dev.V : 0; }
+const int32_t* gm_vocab_universe(const gm_vocab* v) {
+  return v ? reinterpret_cast<const int32_t*>(v->dev.universe) : nullptr;
+}
+
+// ---------------------------------------------------------------------------
+gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
+  if (!t || !out) return fail(GM_ERR_INVALID, "null tables");
+  if (t->n_nodes <= 0 || t->n_classes <= 0 || t->n_rules <= 0) return fail(GM_ERR_INVALID, "empty automaton");
+  if (t->start_node < 0 || t->start_node >= t->n_nodes) return fail(GM_ERR_INVALID, "bad start node");
+  for (int b = 0; b < 256; ++b)
+    if (t->byte_class[b] >= t->n_classes) return fail(GM_ERR_INVALID, "byte class out of range");
+  const int64_t n_idx = (int64_t)t->n_nodes * t->n_classes;
+  if (t->trans_off[0] != 0 || t->trans_off[n_idx] != t->n_trans) return fail(GM_ERR_INVALID, "bad transition CSR");
+  for (int32_t i = 0; i < t->n_trans; ++i) {
+    const int32_t d = t->trans[2 * i];
+    const uint32_t pk = (uint32_t)t->trans[2 * i + 1];
+    const uint32_t poff = pk & 0xFFFFFF, plen = pk >> 24;
+    if (d < 0 || d >= t->n_nodes || poff + plen > (uint32_t)t->n_push)
+      return fail(GM_ERR_INVALID, "transition out of range");
+  }
+  std::vector<int32_t> key_of_node(t->n_nodes, -1);
+  for (int32_t k = 0; k < t->n_keys; ++k) {
+    const int32_t nd = t->cache_keys[k];
+    if (nd < 0 || nd >= t->n_nodes) return fail(GM_ERR_INVALID, "cache key out of range");
+    key_of_node[nd] = k;
+  }
+  gm_grammar* g = new gm_grammar();
+  gm_status st;
+  uint8_t *bc, *flags;
+  int32_t *toff, *pool, *nrule, *keys, *kon, *fstart, *fnext;
+  int2* trans;
+  if ((st = g->mem.upload(&bc, t->byte_class, 256)) ||
+      (st = g->mem.upload(&toff, t->trans_off, (size_t)n_idx + 1)) ||
+      (st = g->mem.upload(&trans, reinterpret_cast<const int2*>(t->trans), (size_t)t->n_trans)) ||
+      (st = g->mem.upload(&pool, t->push_pool, (size_t)t->n_push)) ||
+      (st = g->mem.upload(&flags, t->node_flags, (size_t)t->n_nodes)) ||
+      (st = g->mem.upload(&nrule, t->node_rule, (size_t)t->n_nodes)) ||
+      (st = g->mem.upload(&keys, t->cache_keys, (size_t)t->n_keys)) ||
+      (st = g->mem.upload(&kon, key_of_node.data(), key_of_node.size())) ||
+      (st = g->mem.upload(&fstart, t->follow_start, (size_t)t->n_rules)) ||
+      (st = g->mem.upload(&fnext, t->follow_next, (size_t)t->n_fstates * t->n_classes))) {
+    g->mem.release();
+    delete g;
+    return st;
+  }
+  g->dev = DevGrammar{t->n_nodes, t->n_rules, t->n_classes, t->start_node, t->n_keys, t->n_fstates,
+                      bc, toff, trans, pool, flags, nrule, keys, kon, fstart, fnext};
+  g->keys.assign(t->cache_keys, t->cache_keys + t->n_keys);
+  *out = g;
+  return GM_OK;
+}
+
+void gm_grammar_release(gm_grammar* g) {
+  if (!g) return;
+  g->mem.release();
+  delete g;
+}
+
+// ---------------------------------------------------------------------------
+gm_status gm_cache_build_rows(const gm_grammar* g, const gm_vocab* v, int32_t key_begin, int32_t n,
+                              int32_t* acc_rows, int32_t* dep_rows, void* stream) {
+  if (!g || !v) return fail(GM_ERR_INVALID, "null grammar/vocab");
+  if (key_begin < 0 || n < 0 || key_begin + n > g->dev.n_keys) return fail(GM_ERR_INVALID, "key range out of bounds");
+  if (n == 0) return GM_OK;
+  cudaStream_t s = as_stream(stream);
+  const size_t bytes = (size_t)n * v->dev.W * 4;
+  GM_CUDA_TRY(cudaMemsetAsync(acc_rows, 0, bytes, s));
+  GM_CUDA_TRY(cudaMemsetAsync(dep_rows, 0, bytes, s));
+  DevArena A;
+  gm_status st = build_arena(&A);
+  if (st) return st;
+  GM_CUDA_TRY(cudaMemsetAsync(A.err, 0, 4, s));
+  st = launch_cache_build(g->dev, v->dev, A, key_begin, n, reinterpret_cast<uint32_t*>(acc_rows),
+                          reinterpret_cast<uint32_t*>(dep_rows), A.err, s);
+  if (st) return st;
+  uint32_t bits = 0;
+  GM_CUDA_TRY(cudaMemcpyAsync(&bits, A.err, 4, cudaMemcpyDeviceToHost, s));
+  GM_CUDA_TRY(cudaStreamSynchronize(s));
+  return err_bits_to_status(bits, "cache build");
+}
+
+gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t* acc_rows,
+                          const int32_t* dep_rows, gm_cache** out, gm_cache_stats* stats, void* stream) {
+  if (!g || !v || !out) return fail(GM_ERR_INVALID, "null argument");
+  cudaStream_t s = as_stream(stream);
+  const int32_t n = g->dev.n_keys, W = v->dev.W;
+  gm_cache* c = new gm_cache();
+  gm_status st;
+  uint32_t *acc, *dep_tmp;
+  int64_t* counts;
+  int32_t* dep_off;
+  if ((st = c->mem.alloc(&acc, (size_t)n * W)) || (st = c->mem.alloc(&counts, (size_t)n + 1)) ||
+      (st = c->mem.alloc(&dep_off, (size_t)n + 1))) {
+    c->mem.release();
+    delete c;
+    return st;
+  }
+  std::vector<int64_t> dep_cnt(n), acc_cnt(n);
+  if (n) {
+    GM_CUDA_TRY(cudaMemcpyAsync(acc, acc_rows, (size_t)n * W * 4, cudaMemcpyDeviceToDevice, s));
+    dep_tmp = reinterpret_cast<uint32_t*>(const_cast<int32_t*>(dep_rows));
+    if ((st = launch_row_popcount(dep_tmp, W, n, counts, s))) return st;
+    GM_CUDA_TRY(cudaMemcpyAsync(dep_cnt.data(), counts, n * 8, cudaMemcpyDeviceToHost, s));
+    if ((st = launch_row_popcount(acc, W, n, counts, s))) return st;
+    GM_CUDA_TRY(cudaMemcpyAsync(acc_cnt.data(), counts, n * 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  std::vector<int32_t> off(n + 1, 0);
+  int64_t dep_total = 0, acc_total = 0;
+  for (int32_t k = 0; k < n; ++k) {
+    dep_total += dep_cnt[k];
+    acc_total += acc_cnt[k];
+    if (dep_total > INT32_MAX) return fail(GM_ERR_INVALID, "too many dependent tokens");
+    off[k + 1] = (int32_t)dep_total;
+  }
+  int32_t* dep_ids;
+  if ((st = c->mem.alloc(&dep_ids, (size_t)dep_total))) {
+    c->mem.release();
+    delete c;
+    return st;
+  }
+  GM_CUDA_TRY(cudaMemcpyAsync(dep_off, off.data(), (n + 1) * 4, cudaMemcpyHostToDevice, s));
+  if (n && (st = launch_dep_compact(reinterpret_cast<const uint32_t*>(dep_rows), W, n, dep_off, dep_ids, s)))
+    return st;
+  c->host_binding.g = g->dev;
+  c->host_binding.v = v->dev;
+  c->host_binding.c = DevCache{acc, dep_off, dep_ids};
+  DevBinding* db;
+  if ((st = c->mem.alloc(&db, 1))) return st;
+  GM_CUDA_TRY(cudaMemcpyAsync(db, &c->host_binding, sizeof(DevBinding), cudaMemcpyHostToDevice, s));
+  GM_CUDA_TRY(cudaStreamSynchronize(s));
+  c->binding = db;
+  c->n_keys = n;
+  if (stats) {
+    int64_t n_univ = v->dev.n_sorted;
+    stats->n_keys = n;
+    stats->accepted_total = acc_total;
+    stats->dependent_total = dep_total;
+    stats->rejected_total = (int64_t)n * n_univ - acc_total - dep_total;
+    stats->row_bytes = (int64_t)n * W * 4;
+  }
+  *out = c;
+  return GM_OK;
+}
+
+void gm_cache_release(gm_cache* c) {
+  if (!c) return;
+  c->mem.release();
+  delete c;
+}
+gm_status gm_cache_export(const gm_cache* c, int32_t* acc_rows_out, int32_t* dep_off_out, int32_t* dep_ids_out,
+                          int64_t* n_dep_out) {
+  if (!c) return fail(GM_ERR_INVALID, "null cache");
+  const int32_t n = c->n_keys, W = c->host_binding.v.W;
+  int32_t total = 0;
+  GM_CUDA_TRY(cudaMemcpy(&total, c->host_binding.c.dep_off + n, 4, cudaMemcpyDeviceToHost));
+  if (n_dep_out) *n_dep_out = total;
+  if (acc_rows_out && n)
+    GM_CUDA_TRY(cudaMemcpy(acc_rows_out, c->host_binding.c.acc_rows, (size_t)n * W * 4, cudaMemcpyDeviceToDevice));
+  if (dep_off_out)
+    GM_CUDA_TRY(cudaMemcpy(dep_off_out, c->host_binding.c.dep_off, (size_t)(n + 1) * 4, cudaMemcpyDeviceToDevice));
+  if (dep_ids_out && total)
+    GM_CUDA_TRY(cudaMemcpy(dep_ids_out, c->host_binding.c.dep_ids, (size_t)total * 4, cudaMemcpyDeviceToDevice));
+  return GM_OK;
+}
+
+// ---------------------------------------------------------------------------
+gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_window, int64_t arena_log2,
+                         gm_pool** out) {
+  if (capacity <= 0 || max_stacks <= 0 || max_stacks > 32 || max_window < 0 || arena_log2 < 10 ||
+      arena_log2 > 30 || !out)
+    return fail(GM_ERR_INVALID, "bad pool arguments (max_stacks <= 32, 10 <= arena_log2 <= 30)");
+  gm_pool* p = new gm_pool();
+  const int32_t H = max_window + 1;
+  const uint32_t acap = 1u << arena_log2;
+  gm_status st;
+  int2* tops;
+  int32_t *meta, *head, *hist, *win, *scr;
+  const DevBinding** bind;
+  unsigned long long* keys;
+  uint32_t* err;
+  uint8_t* sb;
+  if ((st = p->mem.alloc(&tops, (size_t)capacity * H * max_stacks)) ||
+      (st = p->mem.alloc(&meta, (size_t)capacity * H)) || (st = p->mem.alloc(&head, (size_t)capacity)) ||
+      (st = p->mem.alloc(&hist, (size_t)capacity)) || (st = p->mem.alloc(&win, (size_t)capacity)) ||
+      (st = p->mem.alloc(&bind, (size_t)capacity)) || (st = p->mem.alloc(&keys, (size_t)acap)) ||
+      (st = p->mem.alloc(&err, 1)) || (st = p->mem.alloc(&sb, 1 << 16)) || (st = p->mem.alloc(&scr, 1024))) {
+    p->mem.release();
+    delete p;
+    return st;
+  }
+  GM_CUDA_TRY(cudaMemset(keys, 0xFF, sizeof(unsigned long long) * acap));
+  GM_CUDA_TRY(cudaMemset(err, 0, 4));
+  GM_CUDA_TRY(cudaMemset(meta, 0, sizeof(int32_t) * (size_t)capacity * H));
+  GM_CUDA_TRY(cudaMemset(head, 0, sizeof(int32_t) * (size_t)capacity));
+  GM_CUDA_TRY(cudaMemset(hist, 0, sizeof(int32_t) * (size_t)capacity));
+  GM_CUDA_TRY(cudaMemset(bind, 0, sizeof(void*) * (size_t)capacity));
+  p->dev = DevPool{capacity, max_stacks, H, tops, meta, head, hist, win, bind, DevArena{keys, acap - 1, err}, err};
+  p->scratch_bytes = sb;
+  p->scratch_cap = 1 << 16;
+  p->scratch_i32 = scr;
+  p->max_w = 0;
+  *out = p;
+  return GM_OK;
+}
+
+void gm_pool_release(gm_pool* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();
+  p->mem.release();
+  delete p;
+}
+
+gm_status gm_pool_reset(gm_pool* p, int32_t slot, const gm_grammar* g, const gm_cache* c, const gm_vocab* v,
+                        int32_t window, void* stream) {
+  if (!p || !g || !c || !v) return fail(GM_ERR_INVALID, "null argument");
+  if (slot < 0 || slot >= p->dev.capacity) return fail(GM_ERR_INVALID, "slot out of range");
+  if (window < 0 || window > p->dev.H - 1) return fail(GM_ERR_INVALID, "history window exceeds pool maximum");
+  if (v->dev.W > p->max_w) p->max_w = v->dev.W;
+  return launch_reset(p->dev, slot, c->binding, g->dev.start_node, window, as_stream(stream));
+}
+
+gm_status gm_pool_fork(gm_pool* p, int32_t src, int32_t dst, void* stream) {
+  if (!p || src < 0 || dst < 0 || src >= p->dev.capacity || dst >= p->dev.capacity)
+    return fail(GM_ERR_INVALID, "slot out of range");
+  cudaStream_t s = as_stream(stream);
+  const DevPool& P = p->dev;
+  const size_t tops_per = (size_t)P.H * P.max_stacks;
+  GM_CUDA_TRY(cudaMemcpyAsync(P.tops + dst * tops_per, P.tops + src * tops_per, tops_per * sizeof(int2),
+                              cudaMemcpyDeviceToDevice, s));
+  GM_CUDA_TRY(cudaMemcpyAsync(P.meta + (size_t)dst * P.H, P.meta + (size_t)src * P.H, P.H * 4,
+                              cudaMemcpyDeviceToDevice, s));
+  GM_CUDA_TRY(cudaMemcpyAsync(P.head + dst, P.head + src, 4, cudaMemcpyDeviceToDevice, s));
+  GM_CUDA_TRY(cudaMemcpyAsync(P.hist_len + dst, P.hist_len + src, 4, cudaMemcpyDeviceToDevice, s));
+  GM_CUDA_TRY(cudaMemcpyAsync(P.window + dst, P.window + src, 4, cudaMemcpyDeviceToDevice, s));
+  GM_CUDA_TRY(cudaMemcpyAsync(P.binding + dst, P.binding + src, sizeof(void*), cudaMemcpyDeviceToDevice, s));
+  return GM_OK;
+}
+
+gm_status gm_accept_tokens(gm_pool* p, const int32_t* slots, const int32_t* token_ids, int32_t n,
+                           uint8_t* accepted_out, void* stream) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  return launch_accept_tokens(p->dev, slots, token_ids, n, accepted_out, as_stream(stream));
+}
+
+gm_status gm_accept_bytes(gm_pool* p, int32_t slot, const uint8_t* data, int64_t len, uint8_t* accepted_out,
+                          void* stream) {
+  if (!p || slot < 0 || slot >= p->dev.capacity) return fail(GM_ERR_INVALID, "slot out of range");
+  cudaStream_t s = as_stream(stream);
+  if (len > p->scratch_cap) {
+    uint8_t* nb;
+    GM_CUDA_TRY(cudaStreamSynchronize(s));
+    GM_CUDA_TRY(cudaMalloc(&nb, (size_t)len));
+    p->mem.ptrs.push_back(nb);
+    p->scratch_bytes = nb;
+    p->scratch_cap = len;
+  }
+  if (len) GM_CUDA_TRY(cudaMemcpyAsync(p->scratch_bytes, data, (size_t)len, cudaMemcpyHostToDevice, s));
+  return launch_accept_bytes(p->dev, slot, p->scratch_bytes, len, accepted_out, s);
+}
+
+gm_status gm_fill_tokens(gm_pool* p, const int32_t* slots, int32_t n, int32_t* bitmask, int64_t bitmask_stride,
+                         const int32_t* rows, uint8_t* need_apply_out, void* stream) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  return launch_fill(p->dev, slots, n, bitmask, bitmask_stride, rows, need_apply_out, p->max_w,
+                     as_stream(stream));
+}
+
+gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps, int32_t n, void* stream) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  return launch_rollback(p->dev, slots, steps, n, as_stream(stream));
+}
+
+gm_status gm_pool_check(gm_pool* p, int32_t* flags_out) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  uint32_t bits = 0;
+  GM_CUDA_TRY(cudaDeviceSynchronize());
+  GM_CUDA_TRY(cudaMemcpy(&bits, p->dev.err, 4, cudaMemcpyDeviceToHost));
+  GM_CUDA_TRY(cudaMemset(p->dev.err, 0, 4));
+  if (flags_out) *flags_out = (int32_t)bits;
+  return err_bits_to_status(bits, "matcher");
+}
+
+gm_status gm_pool_slot_info(gm_pool* p, int32_t slot, int32_t* info5, int32_t* stacks_out, int32_t max_out) {
+  if (!p || slot < 0 || slot >= p->dev.capacity) return fail(GM_ERR_INVALID, "slot out of range");
+  if (max_out > 32) max_out = 32;
+  int32_t* d = p->scratch_i32;  // [0..8) info, [16..24) bytes, [64..) stacks
+  gm_status st = launch_probe(p->dev, slot, d, reinterpret_cast<int2*>(d + 64), max_out,
+                              reinterpret_cast<uint32_t*>(d + 16), 0);
+  if (st) return st;
+  int32_t host[128];
+  GM_CUDA_TRY(cudaMemcpy(host, d, sizeof(host), cudaMemcpyDeviceToHost));
+  std::memcpy(info5, host, 5 * 4);
+  if (stacks_out && max_out > 0) std::memcpy(stacks_out, host + 64, (size_t)std::min(max_out, host[0]) * 8);
+  return GM_OK;
+}
+
+gm_status gm_pool_first_bytes(gm_pool* p, int32_t slot, uint32_t* bytes8, int32_t* terminable) {
+  if (!p || slot < 0 || slot >= p->dev.capacity) return fail(GM_ERR_INVALID, "slot out of range");
+  int32_t* d = p->scratch_i32;
+  gm_status st = launch_probe(p->dev, slot, d, reinterpret_cast<int2*>(d + 64), 0,
+                              reinterpret_cast<uint32_t*>(d + 16), 0);
+  if (st) return st;
+  int32_t host[32];
+  GM_CUDA_TRY(cudaMemcpy(host, d, sizeof(host), cudaMemcpyDeviceToHost));
+  std::memcpy(bytes8, host + 16, 32);
+  if (terminable) *terminable = host[3];
+  return GM_OK;
+}
+
+gm_status gm_pool_materialize(gm_pool* p, int32_t handle, int32_t* out, int32_t max_out, int32_t* depth) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  std::vector<int32_t> chain;
+  int32_t h = handle;
+  while (h >= 0) {
+    unsigned long long k;
+    GM_CUDA_TRY(cudaMemcpy(&k, p->dev.arena.keys + h, 8, cudaMemcpyDeviceToHost));
+    chain.push_back((int32_t)((uint32_t)k >> 1));
+    h = (int32_t)(uint32_t)(k >> 32) - 1;
+    if ((int64_t)chain.size() > (int64_t)p->dev.arena.mask + 1) return fail(GM_ERR_INVALID, "corrupt chain");
+  }
+  std::reverse(chain.begin(), chain.end());
+  *depth = (int32_t)chain.size();
+  for (int32_t i = 0; i < (int32_t)chain.size() && i < max_out; ++i) out[i] = chain[i];
+  return GM_OK;
+}
+
+int64_t gm_pool_arena_used(gm_pool* p) {
+  if (!p) return -1;
+  // counted on the host: cheap enough for diagnostics
+  std::vector<unsigned long long> keys((size_t)p->dev.arena.mask + 1);
+  if (cudaMemcpy(keys.data(), p->dev.arena.keys, keys.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  int64_t used = 0;
+  for (auto k : keys) used += (k != kEmptyKey);
+  return used;
+}
+
+}  // extern "C"

@@ -1,0 +1,220 @@
+// K4 — batched accept_token / accept_bytes on device-resident stacks, plus
+// the small state kernels (reset, rollback, first-byte probe).
+//
+// Replaces Matcher.accept_token / accept_bytes / _sim_bytes / _rewrite_kernel
+// / _push_history / rollback (REF matcher.py:192-217, 239-326).  One thread
+// advances one request: the request's stack set is walked byte by byte with
+// walker-local frames; survivors are interned into the hash-consed arena
+// (parents first), deduplicated by (handle, node) — which is deduplication by
+// stack content because the arena is hash-consed (REF matcher.py:202-206) —
+// and written as the next entry of the slot's history ring.  A rejected token
+// leaves the slot unchanged (REF matcher.py:267-268).
+#include "device.cuh"
+
+namespace gm {
+
+constexpr int kAccS = 32;
+constexpr int kAccF = 160;
+
+__device__ void push_history(const DevPool& P, int32_t slot, int32_t h, int nt,
+                             const int32_t* refs, const int32_t* nodes, int terminated) {
+  const int32_t nh = (h + 1) % P.H;
+  int2* dst = slot_tops(P, slot, nh);
+  for (int s = 0; s < nt; ++s) {
+    const int32_t r = refs[s];
+    dst[s] = make_int2(r == -1 ? -1 : -2 - r, nodes[s]);
+  }
+  P.meta[(size_t)slot * P.H + nh] = nt | (terminated << 16);
+  P.head[slot] = nh;
+  const int32_t hl = P.hist_len[slot] + 1;
+  P.hist_len[slot] = hl < P.window[slot] ? hl : P.window[slot];
+}
+
+// Shared by token and byte-string acceptance.  data/len = bytes to consume;
+// is_eos = EOS token.  Returns 1 if accepted.
+__device__ int accept_one(const DevPool& P, int32_t slot, const uint8_t* data, int64_t len,
+                          bool is_eos, bool reject_token) {
+  const DevBinding* B = P.binding[slot];
+  const DevGrammar& G = B->g;
+  const int32_t h = P.head[slot];
+  const int32_t meta = P.meta[(size_t)slot * P.H + h];
+  const int ntops = meta & 0xFFFF;
+  if ((meta >> 16) & 1) {  // REF matcher.py:276-277 "matcher is terminated"
+    atomicOr(P.err, kErrTerminated);
+    return 0;
+  }
+  const int2* tops = slot_tops(P, slot, h);
+  Walker<kAccS, kAccF> w;
+  w.reset();
+  for (int s = 0; s < ntops; ++s) w.add(tops[s].x < 0 ? -1 : -2 - tops[s].x, tops[s].y);
+  if (is_eos) {  // REF matcher.py:280-288
+    bool term = false;
+    for (int s = 0; s < w.n && !term; ++s) term = w.terminable(G, P.arena, w.ref[s], w.node[s]);
+    if (!term) return 0;
+    push_history(P, slot, h, w.n, w.ref, w.node, 1);
+    return 1;
+  }
+  if (reject_token) return 0;  // special or empty token (REF matcher.py:289-293)
+  for (int64_t i = 0; i < len; ++i) {
+    if (w.nf > kAccF / 2) {
+      if (!w.intern_all(P.arena)) break;
+    }
+    bool pb = false;
+    if (!w.template step<kAccS>(G, P.arena, data[i], &pb)) break;
+  }
+  if (w.err) {
+    atomicOr(P.err, w.err);
+    return 0;
+  }
+  if (w.n == 0) return 0;
+  if (!w.intern_all(P.arena)) {
+    atomicOr(P.err, w.err | kErrArena);
+    return 0;
+  }
+  if (w.n > P.max_stacks) {
+    atomicOr(P.err, kErrCap);
+    return 0;
+  }
+  push_history(P, slot, h, w.n, w.ref, w.node, 0);
+  return 1;
+}
+
+__global__ void accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots,
+                                     const int32_t* __restrict__ token_ids, int32_t n,
+                                     uint8_t* __restrict__ accepted) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t slot = slots[i];
+  const int32_t tid = token_ids[i];
+  const DevVocab& Vc = P.binding[slot]->v;
+  if (tid < 0 || tid >= Vc.V) {  // REF matcher.py:278-279
+    atomicOr(P.err, kErrInvalid);
+    accepted[i] = 0;
+    return;
+  }
+  const int32_t o0 = Vc.off[tid];
+  const int64_t len = Vc.off[tid + 1] - o0;
+  accepted[i] = (uint8_t)accept_one(P, slot, Vc.bytes + o0, len, tid == Vc.eos, Vc.reject[tid] != 0);
+}
+
+__global__ void accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len,
+                                    uint8_t* accepted) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const int32_t h = P.head[slot];
+  const int32_t meta = P.meta[(size_t)slot * P.H + h];
+  if ((meta >> 16) & 1) {
+    atomicOr(P.err, kErrTerminated);
+    *accepted = 0;
+    return;
+  }
+  if (len == 0) {  // REF matcher.py:253-258: empty input records a history entry
+    const int nt = meta & 0xFFFF;
+    const int2* tops = slot_tops(P, slot, h);
+    int32_t refs[kAccS], nodes[kAccS];
+    for (int s = 0; s < nt; ++s) {
+      refs[s] = tops[s].x < 0 ? -1 : -2 - tops[s].x;
+      nodes[s] = tops[s].y;
+    }
+    push_history(P, slot, h, nt, refs, nodes, 0);
+    *accepted = 1;
+    return;
+  }
+  *accepted = (uint8_t)accept_one(P, slot, data, len, false, false);
+}
+
+__global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32_t start, int32_t window) {
+  if (threadIdx.x != 0) return;
+  P.binding[slot] = b;
+  P.head[slot] = 0;
+  P.hist_len[slot] = 0;
+  P.window[slot] = window;
+  slot_tops(P, slot, 0)[0] = make_int2(-1, start);
+  P.meta[(size_t)slot * P.H] = 1;
+}
+
+__global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots,
+                                const int32_t* __restrict__ steps, int32_t n) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t slot = slots[i], k = steps[i];
+  const int32_t hl = P.hist_len[slot];
+  if (k < 0 || k > hl) {  // REF matcher.py:313-314
+    atomicOr(P.err, 1u << GM_ERR_ROLLBACK);
+    return;
+  }
+  P.head[slot] = ((P.head[slot] - k) % P.H + P.H) % P.H;
+  P.hist_len[slot] = hl - k;
+}
+
+// info: n_stacks, terminated, history_len, terminable, window; stacks copy;
+// bytes8: union of acceptable first bytes over the closure (REF matcher.py:
+// 219-237 _closed_facts).
+__global__ void slot_probe_kernel(DevPool P, int32_t slot, int32_t* info, int2* stacks, int32_t max_out,
+                                  uint32_t* bytes8) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const DevGrammar& G = P.binding[slot]->g;
+  const int32_t h = P.head[slot];
+  const int32_t meta = P.meta[(size_t)slot * P.H + h];
+  const int nt = meta & 0xFFFF;
+  const int2* tops = slot_tops(P, slot, h);
+  int term = 0;
+  uint32_t fb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int s = 0; s < nt; ++s) {
+    int32_t hh = tops[s].x, m = tops[s].y;
+    if (s < max_out) stacks[s] = tops[s];
+    // walk the pop chain: every node reachable by silent completion
+    while (true) {
+      for (int b = 0; b < 256; ++b) {
+        const int32_t idx = m * G.n_classes + G.byte_class[b];
+        if (G.trans_off[idx + 1] > G.trans_off[idx]) fb[b >> 5] |= 1u << (b & 31);
+      }
+      if (!(G.node_flags[m] & GM_NODE_POP)) break;
+      if (hh < 0) { term = 1; break; }
+      const unsigned long long k = arena_load(P.arena, hh);
+      hh = key_parent(k);
+      m = key_node(k);
+    }
+  }
+  info[0] = nt;
+  info[1] = (meta >> 16) & 1;
+  info[2] = P.hist_len[slot];
+  info[3] = term;
+  info[4] = P.window[slot];
+  for (int i = 0; i < 8; ++i) bytes8[i] = fb[i];
+}
+
+gm_status launch_accept_tokens(const DevPool& P, const int32_t* slots, const int32_t* toks, int32_t n,
+                               uint8_t* acc, cudaStream_t s) {
+  if (n <= 0) return GM_OK;
+  const int threads = 64;
+  accept_tokens_kernel<<<(unsigned)ceil_div(n, threads), threads, 0, s>>>(P, slots, toks, n, acc);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_accept_bytes(const DevPool& P, int32_t slot, const uint8_t* data, int64_t len,
+                              uint8_t* acc, cudaStream_t s) {
+  accept_bytes_kernel<<<1, 1, 0, s>>>(P, slot, data, len, acc);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_reset(const DevPool& P, int32_t slot, const DevBinding* b, int32_t start, int32_t window,
+                       cudaStream_t s) {
+  reset_kernel<<<1, 32, 0, s>>>(P, slot, b, start, window);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_rollback(const DevPool& P, const int32_t* slots, const int32_t* steps, int32_t n,
+                          cudaStream_t s) {
+  if (n <= 0) return GM_OK;
+  rollback_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(P, slots, steps, n);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_probe(const DevPool& P, int32_t slot, int32_t* info, int2* stacks, int32_t max_out,
+                       uint32_t* bytes8, cudaStream_t s) {
+  slot_probe_kernel<<<1, 32, 0, s>>>(P, slot, info, stacks, max_out, bytes8);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+
+}  // namespace gm

@@ -1,0 +1,277 @@
+"""Device-side engine objects over the C ABI.
+
+DeviceVocab, DeviceGrammar and DeviceCache own libgmask handles; MatcherPool
+owns the device-resident stack state of every live matcher (one pool per
+CUDA device, slots handed out to matchers).  compile_on_device() is the
+compile pipeline: host front end -> tables upload -> K1/K1b cache build
+(optionally sharded over a torch.distributed group with an NCCL all-gather of
+the finished rows) -> cache assembly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .automaton import AutomatonOptions, CompiledTables, StateLimitError, build_tables
+from .grammar import parse_grammar
+from .vocab import Vocabulary
+
+__all__ = ["MatcherError", "DeviceVocab", "DeviceGrammar", "DeviceCache", "CompiledDeviceGrammar",
+           "MatcherPool", "compile_on_device", "get_pool"]
+
+
+class MatcherError(RuntimeError):
+    """Runtime matcher misuse (REF matcher.py:35-36)."""
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class DeviceVocab:
+    """A Vocabulary uploaded to the current CUDA device (gm_vocab)."""
+
+    def __init__(self, vocab: Vocabulary):
+        _lib.require_cuda()
+        lib = _lib.load()
+        self.vocab = vocab
+        self.size = vocab.size
+        self.words = (vocab.size + 31) // 32
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        data, off = vocab.packed()
+        special = np.asarray(sorted(vocab.special_tokens), dtype=np.int32)
+        h = C.c_void_p()
+        _lib.check(lib.gm_vocab_create(_ptr(data), _ptr(off), vocab.size, _ptr(special), len(special),
+                                       vocab.eos_id, C.byref(h)), "gm_vocab_create")
+        self.handle = h
+        self._hash = vocab.content_hash()
+
+    def content_hash(self) -> bytes:
+        return self._hash
+
+    def __del__(self):
+        if getattr(self, "handle", None) is not None and _lib._lib is not None:
+            _lib._lib.gm_vocab_release(self.handle)
+            self.handle = None
+
+
+class DeviceGrammar:
+    """Automaton tables resident on the device (gm_grammar)."""
+
+    def __init__(self, t: CompiledTables):
+        lib = _lib.load()
+        self.tables = t
+        self._keep = [t.byte_class, t.trans_off, t.trans, t.push_pool, t.node_flags, t.node_rule,
+                      t.cache_keys, t.follow_start, t.follow_next]
+        st = _lib.gm_grammar_tables(
+            n_nodes=t.n_nodes, n_rules=t.n_rules, n_classes=t.n_classes, start_node=t.start_node,
+            byte_class=_ptr(t.byte_class), trans_off=_ptr(t.trans_off), trans=_ptr(t.trans),
+            n_trans=len(t.trans) // 2, push_pool=_ptr(t.push_pool), n_push=len(t.push_pool),
+            node_flags=_ptr(t.node_flags), node_rule=_ptr(t.node_rule), cache_keys=_ptr(t.cache_keys),
+            n_keys=len(t.cache_keys), follow_start=_ptr(t.follow_start), follow_next=_ptr(t.follow_next),
+            n_fstates=t.n_fstates,
+        )
+        h = C.c_void_p()
+        _lib.check(lib.gm_grammar_create(C.byref(st), C.byref(h)), "gm_grammar_create")
+        self.handle = h
+        self.n_keys = len(t.cache_keys)
+
+    def __del__(self):
+        if getattr(self, "handle", None) is not None and _lib._lib is not None:
+            _lib._lib.gm_grammar_release(self.handle)
+            self.handle = None
+
+
+class DeviceCache:
+    """Assembled adaptive cache: dense accepted rows + dependent id lists."""
+
+    def __init__(self, grammar: DeviceGrammar, dvocab: DeviceVocab, acc_rows: torch.Tensor,
+                 dep_rows: torch.Tensor, stream=None):
+        lib = _lib.load()
+        h = C.c_void_p()
+        stats = _lib.gm_cache_stats()
+        _lib.check(lib.gm_cache_create(grammar.handle, dvocab.handle, acc_rows.data_ptr(), dep_rows.data_ptr(),
+                                       C.byref(h), C.byref(stats), _lib.stream_ptr(stream)), "gm_cache_create")
+        self.handle = h
+        self.grammar = grammar  # keep tables alive: the cache binding points at them
+        self.dvocab = dvocab
+        self.stats = {
+            "entries": stats.n_keys,
+            "accepted_total": stats.accepted_total,
+            "dependent_total": stats.dependent_total,
+            "rejected_total": stats.rejected_total,
+            "row_bytes": stats.row_bytes,
+        }
+
+    def export(self):
+        """(acc_rows [n_keys, W] int32 device tensor, dep_off numpy, dep_ids numpy) — inspection only."""
+        lib = _lib.load()
+        n, w = self.grammar.n_keys, self.dvocab.words
+        nd = C.c_int64()
+        _lib.check(lib.gm_cache_export(self.handle, None, None, None, C.byref(nd)), "gm_cache_export")
+        acc = torch.empty((max(n, 1), w), dtype=torch.int32, device=self.dvocab.device)
+        off = torch.empty(n + 1, dtype=torch.int32, device=self.dvocab.device)
+        ids = torch.empty(max(nd.value, 1), dtype=torch.int32, device=self.dvocab.device)
+        _lib.check(lib.gm_cache_export(self.handle, acc.data_ptr(), off.data_ptr(), ids.data_ptr(), None),
+                   "gm_cache_export")
+        return acc[:n], off.cpu().numpy(), ids[: nd.value].cpu().numpy()
+
+    def __del__(self):
+        if getattr(self, "handle", None) is not None and _lib._lib is not None:
+            _lib._lib.gm_cache_release(self.handle)
+            self.handle = None
+
+
+@dataclass
+class CompiledDeviceGrammar:
+    tables: CompiledTables
+    grammar: DeviceGrammar
+    cache: DeviceCache
+    dvocab: DeviceVocab
+    timings_ms: dict = field(default_factory=dict)
+
+    @property
+    def stats(self) -> dict:
+        return {**self.tables.stats, **self.cache.stats}
+
+
+def build_cache_rows(grammar: DeviceGrammar, dvocab: DeviceVocab, key_begin: int, n: int, stream=None):
+    lib = _lib.load()
+    acc = torch.empty((n, dvocab.words), dtype=torch.int32, device=dvocab.device)
+    dep = torch.empty((n, dvocab.words), dtype=torch.int32, device=dvocab.device)
+    if n:
+        status = lib.gm_cache_build_rows(grammar.handle, dvocab.handle, key_begin, n, acc.data_ptr(),
+                                         dep.data_ptr(), _lib.stream_ptr(stream))
+        if status == _lib.GM_ERR_STATE_CAP:
+            raise StateLimitError(lib.gm_last_error().decode())
+        _lib.check(status, "gm_cache_build_rows")
+    return acc, dep
+
+
+def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOptions] = None, *,
+                      root_rule_name: Optional[str] = None, group=None, stream=None,
+                      uncached: bool = False) -> CompiledDeviceGrammar:
+    """Front end + K1/K1b build.  With a torch.distributed ``group`` of size G
+    the cache keys are dealt round-robin-by-block across ranks and the rows
+    are replicated with one all-gather."""
+    t0 = time.perf_counter()
+    tables = build_tables(parse_grammar(text, root_rule_name), opts)
+    t1 = time.perf_counter()
+    grammar = DeviceGrammar(tables)
+    n_keys = grammar.n_keys
+    world = 1
+    if group is not None:
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group)
+    if uncached:
+        # no cache: every token is context dependent, fill walks the whole
+        # vocabulary (the reference's uncached path, REF matcher.py:446-460)
+        universe = torch.empty(dvocab.words, dtype=torch.int32, device=dvocab.device)
+        lib = _lib.load()
+        ptr = lib.gm_vocab_universe(dvocab.handle)
+        u = np.zeros(dvocab.words, dtype=np.uint32)
+        for t in range(dvocab.size):
+            if t not in dvocab.vocab.special_tokens and dvocab.vocab.tokens[t]:
+                u[t >> 5] |= np.uint32(1 << (t & 31))
+        del ptr, universe
+        acc = torch.zeros((n_keys, dvocab.words), dtype=torch.int32, device=dvocab.device)
+        dep = torch.from_numpy(u.view(np.int32)).to(dvocab.device).expand(n_keys, -1).contiguous()
+    elif world <= 1:
+        acc, dep = build_cache_rows(grammar, dvocab, 0, n_keys, stream)
+    else:
+        import torch.distributed as dist
+
+        rank = dist.get_rank(group)
+        per = (n_keys + world - 1) // world
+        lo, hi = min(rank * per, n_keys), min((rank + 1) * per, n_keys)
+        acc_l, dep_l = build_cache_rows(grammar, dvocab, lo, hi - lo, stream)
+        pad = torch.zeros((2, per, dvocab.words), dtype=torch.int32, device=dvocab.device)
+        pad[0, : hi - lo] = acc_l
+        pad[1, : hi - lo] = dep_l
+        full = torch.empty((world, 2, per, dvocab.words), dtype=torch.int32, device=dvocab.device)
+        dist.all_gather_into_tensor(full, pad, group=group)
+        acc = full[:, 0].reshape(world * per, -1)[:n_keys].contiguous()
+        dep = full[:, 1].reshape(world * per, -1)[:n_keys].contiguous()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    cache = DeviceCache(grammar, dvocab, acc, dep, stream)
+    t3 = time.perf_counter()
+    timings = {"front_end": (t1 - t0) * 1e3, "cache_build": (t2 - t1) * 1e3, "assemble": (t3 - t2) * 1e3,
+               "total": (t3 - t0) * 1e3}
+    return CompiledDeviceGrammar(tables, grammar, cache, dvocab, timings)
+
+
+# ---------------------------------------------------------------------------
+# matcher pool
+
+
+class MatcherPool:
+    """Device-resident matcher slots (gm_pool) with a host free list."""
+
+    def __init__(self, capacity: int = 4096, max_stacks: int = 32, max_window: int = 64, arena_log2: int = 24):
+        _lib.require_cuda()
+        lib = _lib.load()
+        h = C.c_void_p()
+        _lib.check(lib.gm_pool_create(capacity, max_stacks, max_window, arena_log2, C.byref(h)), "gm_pool_create")
+        self.handle = h
+        self.capacity = capacity
+        self.max_window = max_window
+        self.max_stacks = max_stacks
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self._free = list(range(capacity - 1, -1, -1))
+        self._lock = threading.Lock()
+        self._flag = torch.zeros(1, dtype=torch.uint8, device=self.device)
+        self._pinned_flag = torch.zeros(1, dtype=torch.uint8).pin_memory()
+
+    def alloc(self) -> int:
+        with self._lock:
+            if not self._free:
+                raise MatcherError(f"matcher pool exhausted ({self.capacity} slots); set GMASK_POOL_SLOTS")
+            return self._free.pop()
+
+    def free(self, slot: int):
+        with self._lock:
+            self._free.append(slot)
+
+    def check(self, runtime: bool = True):
+        """Raise the sticky device error, if any (syncs)."""
+        flags = C.c_int32()
+        status = _lib.load().gm_pool_check(self.handle, C.byref(flags))
+        if status != _lib.GM_OK:
+            msg = _lib.load().gm_last_error().decode()
+            if status in (_lib.GM_ERR_STATE_CAP, _lib.GM_ERR_TERMINATED, _lib.GM_ERR_ROLLBACK,
+                          _lib.GM_ERR_INVALID, _lib.GM_ERR_ARENA_FULL):
+                raise MatcherError(msg)
+            _lib.check(status, "matcher")
+
+    def __del__(self):
+        if getattr(self, "handle", None) is not None and _lib._lib is not None:
+            _lib._lib.gm_pool_release(self.handle)
+            self.handle = None
+
+
+_pools: dict = {}
+
+
+def get_pool(device=None) -> MatcherPool:
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index
+    pool = _pools.get(dev)
+    if pool is None:
+        with torch.cuda.device(dev):
+            pool = MatcherPool(
+                capacity=int(os.environ.get("GMASK_POOL_SLOTS", "4096")),
+                max_window=int(os.environ.get("GMASK_MAX_WINDOW", "64")),
+                arena_log2=int(os.environ.get("GMASK_ARENA_LOG2", "24")),
+            )
+        _pools[dev] = pool
+    return pool

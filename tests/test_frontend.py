@@ -1,0 +1,111 @@
+"""Host front end vs the reference (CPU): language, errors, vocabularies,
+schema lowering.  Golden verdicts come from the reference itself
+(tools/make_golden.py); the device tables are interpreted by tests/tablesim.py."""
+
+import json
+
+import pytest
+
+from paper_2411_15100_b200.automaton import StateLimitError, build_tables
+from paper_2411_15100_b200.grammar import GrammarError, parse_grammar
+from paper_2411_15100_b200.schema import SchemaError, schema_to_grammar_text
+from tablesim import TableSim
+from workloads import GOLDEN, build_gen_vocab, build_toy200, grammar_text, languages, vocab_by_name
+
+
+def test_vocab_hashes_match_reference():
+    want = json.loads((GOLDEN / "vocab_hashes.json").read_text())
+    assert build_toy200().content_hash().hex() == want["toy200"]
+    assert build_gen_vocab().content_hash().hex() == want["gen"]
+    for key in ("512:text", "4000:mixed", "32000:text"):
+        assert vocab_by_name(key).content_hash().hex() == want[key], key
+
+
+@pytest.mark.slow
+def test_synth_vocab_128k_matches_reference():
+    want = json.loads((GOLDEN / "vocab_hashes.json").read_text())
+    assert vocab_by_name("128256:text").content_hash().hex() == want["128256:text"]
+
+
+def _sims():
+    lang = languages()
+    names = sorted({g for g, _, _ in lang["accepts"]})
+    return {n: TableSim(build_tables(parse_grammar(grammar_text(n)))) for n in names}
+
+
+def test_language_equals_reference_oracle():
+    sims = _sims()
+    bad = []
+    for g, hx, want in languages()["accepts"]:
+        if sims[g].accepts(bytes.fromhex(hx)) != want:
+            bad.append((g, hx, want))
+    assert not bad, bad[:10]
+
+
+@pytest.mark.parametrize("inline", [False, True])
+def test_language_independent_of_inlining(inline):
+    from paper_2411_15100_b200.automaton import AutomatonOptions
+
+    for g in languages()["grammars"]:
+        sim = TableSim(build_tables(parse_grammar(grammar_text(g)), AutomatonOptions(inline=inline)))
+        for gg, hx, want in languages()["accepts"]:
+            if gg == g:
+                assert sim.accepts(bytes.fromhex(hx)) == want, (g, hx)
+
+
+def test_grammar_errors_match_reference():
+    for text, cls, msg in languages()["errors"]:
+        if cls is None:
+            build_tables(parse_grammar(text))
+            continue
+        with pytest.raises(GrammarError) as ei:
+            build_tables(parse_grammar(text))
+        assert str(ei.value) == msg, (text, str(ei.value), msg)
+
+
+def test_left_recursion_raises_state_limit():
+    kind, msg = languages()["left_recursion"]
+    assert kind == "StateLimitError"
+    with pytest.raises(StateLimitError, match="exceeded cap"):
+        build_tables(parse_grammar('root ::= root "a" | "b"'))
+
+
+def test_schema_language_matches_reference():
+    for key, case in languages()["schemas"].items():
+        ws = bool(int(key.split(":")[1]))
+        sim = TableSim(build_tables(parse_grammar(schema_to_grammar_text(case["schema"], whitespace=ws))))
+        for hx, want in case["docs"]:
+            assert sim.accepts(bytes.fromhex(hx)) == want, (key, bytes.fromhex(hx))
+
+
+def test_schema_errors_match_reference():
+    for sch, msg in languages()["schema_errors"]:
+        if msg is None:
+            schema_to_grammar_text(sch)
+            continue
+        with pytest.raises(SchemaError) as ei:
+            schema_to_grammar_text(sch)
+        assert str(ei.value).split(":")[0] == msg.split(":")[0], (sch, str(ei.value), msg)
+
+
+def test_masks_on_small_vocab_match_golden():
+    """Full-mask KAT on the toy200/gen fixtures via the table interpreter."""
+    from workloads import load_fixture, mask_fixtures
+
+    for fname in mask_fixtures():
+        fx = load_fixture(fname)
+        if fx["vocab"] not in ("toy200", "gen"):
+            continue
+        vocab = vocab_by_name(fx["vocab"])
+        sim = TableSim(build_tables(parse_grammar(grammar_text(fx["grammar"]))))
+        for traj in fx["trajectories"][:6]:
+            st = sim.start()
+            for step, rec in enumerate(traj["masks"]):
+                ids = sim.mask_ids(st, vocab.tokens, vocab.special_tokens, vocab.eos_id)
+                words = bytearray(4 * ((vocab.size + 31) // 32))
+                for t in ids:
+                    words[t >> 3] |= 1 << (t & 7)
+                assert words.hex() == rec["hex"], (fname, step)
+                if step >= len(traj["tokens"]) or traj["tokens"][step] == vocab.eos_id:
+                    break
+                st = sim.walk(st, vocab.tokens[traj["tokens"][step]])

@@ -214,6 +214,11 @@ gm_status gm_fill_tokens(gm_pool* p, const int32_t* slots, int32_t n,
 gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps,
                       int32_t n, void* stream);
 
+/* Serving-loop request recycling: every slot in slots[0..n) (device int32)
+ * whose current state is terminated restarts at the grammar start with an
+ * empty history; other slots are untouched.  Stream-ordered, no sync. */
+gm_status gm_pool_recycle(gm_pool* p, const int32_t* slots, int32_t n, void* stream);
+
 /* Introspection (syncs).  info = {n_stacks, terminated, history_len,
  * terminable, window}; stacks_out (nullable) receives up to max_out
  * (handle, node) pairs of the current top set. */

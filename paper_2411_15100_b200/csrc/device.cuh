@@ -44,7 +44,34 @@ struct DevGrammar {
   const int32_t* key_of_node;  // [n_nodes] -> key index or -1
   const int32_t* follow_start; // [n_rules]
   const int32_t* follow_next;  // [n_fstates*n_classes]
+  // The walker tables (byte_class .. key_of_node) live in one contiguous
+  // 16-byte-aligned blob so a CTA can stage them into shared memory with a
+  // single coalesced copy.
+  const uint8_t* blob;
+  int32_t blob_bytes;
 };
+
+constexpr int kStageBytes = 32 * 1024;  // shared-memory budget for staged tables
+
+// Cooperative copy of the grammar blob into shared memory; returns a view
+// whose table pointers address the shared copy (or the global tables when
+// the blob does not fit).  Must be called by every thread of the CTA.
+__device__ __forceinline__ DevGrammar stage_grammar(const DevGrammar& G, uint8_t* smem) {
+  DevGrammar g = G;
+  if (G.blob_bytes > kStageBytes) return g;
+  const int4* src = reinterpret_cast<const int4*>(G.blob);
+  int4* dst = reinterpret_cast<int4*>(smem);
+  for (int i = threadIdx.x; i < G.blob_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+  auto rb = [&](const void* p) { return smem + (reinterpret_cast<const uint8_t*>(p) - G.blob); };
+  g.byte_class = rb(G.byte_class);
+  g.node_flags = rb(G.node_flags);
+  g.trans_off = reinterpret_cast<const int32_t*>(rb(G.trans_off));
+  g.trans = reinterpret_cast<const int2*>(rb(G.trans));
+  g.push_pool = reinterpret_cast<const int32_t*>(rb(G.push_pool));
+  g.key_of_node = reinterpret_cast<const int32_t*>(rb(G.key_of_node));
+  g.node_rule = reinterpret_cast<const int32_t*>(rb(G.node_rule));
+  return g;
+}
 
 struct DevVocab {
   int32_t V, W, n_sorted, eos;
@@ -59,6 +86,8 @@ struct DevCache {
   const uint32_t* acc_rows;    // [n_keys*W]
   const int32_t* dep_off;      // [n_keys+1]
   const int32_t* dep_ids;
+  const int4* dep_ent;         // [n_dep]: (token id, byte offset, length, 0)
+  const uint8_t* dep_bytes;    // dependent tokens' bytes, contiguous
 };
 
 // Everything a matcher slot needs, resident in device memory.
@@ -182,14 +211,14 @@ struct Walker {
       int32_t r = ref[s], m = node[s];
       while (true) {
         const int32_t idx = m * G.n_classes + c;
-        const int32_t t0 = __ldg(G.trans_off + idx), t1 = __ldg(G.trans_off + idx + 1);
+        const int32_t t0 = G.trans_off[idx], t1 = G.trans_off[idx + 1];
         for (int32_t t = t0; t < t1; ++t) {
-          const int2 tr = __ldg(G.trans + t);
+          const int2 tr = G.trans[t];
           int32_t d = tr.x;
           const int plen = (int)((uint32_t)tr.y >> 24);
           const int poff = tr.y & 0xFFFFFF;
           int32_t rr = r;
-          for (int k = 0; k < plen; ++k) rr = push(G, A, rr, __ldg(G.push_pool + poff + k));
+          for (int k = 0; k < plen; ++k) rr = push(G, A, rr, G.push_pool[poff + k]);
           if (plen == 0) {
             while ((G.node_flags[d] & GM_NODE_DEAD_END) && rr != -1) {
               int32_t pr, pn;
@@ -273,10 +302,55 @@ struct DevPool {
   const DevBinding** binding; // [capacity]
   DevArena arena;
   uint32_t* err;
+  struct SlotHdr* hdr;        // [capacity] current-state summary
 };
 
 __device__ __forceinline__ int2* slot_tops(const DevPool& P, int32_t slot, int32_t h) {
   return P.tops + ((size_t)slot * P.H + h) * P.max_stacks;
+}
+
+// Current-state summary of a slot, one 256-byte record written by every
+// state change (reset / accept / rollback / recycle / fork).  The fill kernel
+// reads it with one coalesced load instead of chasing head -> ring entry ->
+// key_of_node -> dep_off (each a cold HBM round trip once the model's forward
+// pass has flushed L2).
+constexpr int kHdrTops = 8;
+struct __align__(16) SlotHdr {
+  const DevBinding* binding;
+  int32_t ntops;               // -1: more than kHdrTops stacks (fill uses the ring)
+  int32_t flags;               // bit0 terminated, bit1 terminable
+  int32_t key[kHdrTops];
+  int32_t dep_lo[kHdrTops];
+  int32_t dep_hi[kHdrTops];
+  int2 top[kHdrTops];
+  int32_t pad[20];
+};
+static_assert(sizeof(SlotHdr) == 256, "SlotHdr layout");
+
+// Summarise (tops, terminated) of `slot` into its header.
+__device__ inline void write_header(const DevPool& P, int32_t slot, const DevBinding* B, const int2* tops, int n,
+                                    int terminated) {
+  const DevGrammar& G = B->g;
+  SlotHdr h;
+  h.binding = B;
+  int term = 0;
+  for (int s = 0; s < n; ++s) {
+    const int2 t = tops[s];
+    if (!terminated && (G.node_flags[t.y] & GM_NODE_POP) &&
+        (t.x < 0 || key_term(arena_load(P.arena, t.x))))
+      term = 1;
+    if (s < kHdrTops) {
+      const int32_t k = G.key_of_node[t.y];
+      h.key[s] = k;
+      h.dep_lo[s] = k >= 0 ? B->c.dep_off[k] : 0;
+      h.dep_hi[s] = k >= 0 ? B->c.dep_off[k + 1] : 0;
+      h.top[s] = t;
+    }
+  }
+  h.ntops = n <= kHdrTops ? n : -1;
+  h.flags = (terminated ? 1 : 0) | (term ? 2 : 0);
+  for (int i = 0; i < 20; ++i) h.pad[i] = 0;
+  P.hdr[slot] = h;
 }
 
 }  // namespace gm

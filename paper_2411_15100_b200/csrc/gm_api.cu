@@ -30,6 +30,8 @@ gm_status launch_accept_tokens(const DevPool&, const int32_t*, const int32_t*, i
 gm_status launch_accept_bytes(const DevPool&, int32_t, const uint8_t*, int64_t, uint8_t*, cudaStream_t);
 gm_status launch_reset(const DevPool&, int32_t, const DevBinding*, int32_t, int32_t, cudaStream_t);
 gm_status launch_rollback(const DevPool&, const int32_t*, const int32_t*, int32_t, cudaStream_t);
+gm_status launch_recycle(const DevPool&, const int32_t*, int32_t, cudaStream_t);
+gm_status launch_fork(const DevPool&, int32_t, int32_t, cudaStream_t);
 gm_status launch_probe(const DevPool&, int32_t, int32_t*, int2*, int32_t, uint32_t*, cudaStream_t);
 
 // RAII-less device buffer list: every object frees what it allocated.
@@ -95,6 +97,8 @@ struct gm_vocab {
   DevAllocs mem;
   DevVocab dev;
   std::vector<uint32_t> universe_host;
+  std::vector<uint8_t> bytes_host;
+  std::vector<int64_t> off_host;
 };
 
 struct gm_grammar {
@@ -180,6 +184,8 @@ gm_status gm_vocab_create(const uint8_t* bytes, const int64_t* offsets, int32_t 
   }
   v->dev = DevVocab{V, W, (int32_t)ids.size(), eos_id, d_bytes, d_off, d_sorted, d_univ, d_rej};
   v->universe_host = std::move(universe);
+  v->bytes_host.assign(bytes, bytes + offsets[V]);
+  v->off_host.assign(offsets, offsets + V + 1);
   *out = v;
   return GM_OK;
 }
@@ -216,27 +222,54 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
     if (nd < 0 || nd >= t->n_nodes) return fail(GM_ERR_INVALID, "cache key out of range");
     key_of_node[nd] = k;
   }
+  // walker tables in one contiguous 16-byte aligned blob (staged into shared
+  // memory by the fill/accept kernels)
+  std::vector<uint8_t> blob;
+  auto put = [&](const void* src, size_t bytes) {
+    size_t off = (blob.size() + 15) & ~size_t(15);
+    blob.resize(off + ((bytes + 15) & ~size_t(15)), 0);
+    if (bytes) std::memcpy(blob.data() + off, src, bytes);
+    return off;
+  };
+  const size_t o_bc = put(t->byte_class, 256);
+  const size_t o_flags = put(t->node_flags, (size_t)t->n_nodes);
+  const size_t o_toff = put(t->trans_off, ((size_t)n_idx + 1) * 4);
+  const size_t o_trans = put(t->trans, (size_t)t->n_trans * 8);
+  const size_t o_pool = put(t->push_pool, (size_t)t->n_push * 4);
+  const size_t o_kon = put(key_of_node.data(), key_of_node.size() * 4);
+  const size_t o_rule = put(t->node_rule, (size_t)t->n_nodes * 4);
+  if (blob.size() > (size_t)INT32_MAX) return fail(GM_ERR_INVALID, "automaton tables too large");
   gm_grammar* g = new gm_grammar();
   gm_status st;
-  uint8_t *bc, *flags;
-  int32_t *toff, *pool, *nrule, *keys, *kon, *fstart, *fnext;
-  int2* trans;
-  if ((st = g->mem.upload(&bc, t->byte_class, 256)) ||
-      (st = g->mem.upload(&toff, t->trans_off, (size_t)n_idx + 1)) ||
-      (st = g->mem.upload(&trans, reinterpret_cast<const int2*>(t->trans), (size_t)t->n_trans)) ||
-      (st = g->mem.upload(&pool, t->push_pool, (size_t)t->n_push)) ||
-      (st = g->mem.upload(&flags, t->node_flags, (size_t)t->n_nodes)) ||
-      (st = g->mem.upload(&nrule, t->node_rule, (size_t)t->n_nodes)) ||
+  uint8_t* d_blob;
+  int32_t *keys, *fstart, *fnext;
+  if ((st = g->mem.upload(&d_blob, blob.data(), blob.size())) ||
       (st = g->mem.upload(&keys, t->cache_keys, (size_t)t->n_keys)) ||
-      (st = g->mem.upload(&kon, key_of_node.data(), key_of_node.size())) ||
       (st = g->mem.upload(&fstart, t->follow_start, (size_t)t->n_rules)) ||
       (st = g->mem.upload(&fnext, t->follow_next, (size_t)t->n_fstates * t->n_classes))) {
     g->mem.release();
     delete g;
     return st;
   }
-  g->dev = DevGrammar{t->n_nodes, t->n_rules, t->n_classes, t->start_node, t->n_keys, t->n_fstates,
-                      bc, toff, trans, pool, flags, nrule, keys, kon, fstart, fnext};
+  DevGrammar& G = g->dev;
+  G.n_nodes = t->n_nodes;
+  G.n_rules = t->n_rules;
+  G.n_classes = t->n_classes;
+  G.start_node = t->start_node;
+  G.n_keys = t->n_keys;
+  G.n_fstates = t->n_fstates;
+  G.byte_class = d_blob + o_bc;
+  G.node_flags = d_blob + o_flags;
+  G.trans_off = reinterpret_cast<const int32_t*>(d_blob + o_toff);
+  G.trans = reinterpret_cast<const int2*>(d_blob + o_trans);
+  G.push_pool = reinterpret_cast<const int32_t*>(d_blob + o_pool);
+  G.key_of_node = reinterpret_cast<const int32_t*>(d_blob + o_kon);
+  G.node_rule = reinterpret_cast<const int32_t*>(d_blob + o_rule);
+  G.cache_keys = keys;
+  G.follow_start = fstart;
+  G.follow_next = fnext;
+  G.blob = d_blob;
+  G.blob_bytes = (int32_t)blob.size();
   g->keys.assign(t->cache_keys, t->cache_keys + t->n_keys);
   *out = g;
   return GM_OK;
@@ -314,9 +347,28 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
   GM_CUDA_TRY(cudaMemcpyAsync(dep_off, off.data(), (n + 1) * 4, cudaMemcpyHostToDevice, s));
   if (n && (st = launch_dep_compact(reinterpret_cast<const uint32_t*>(dep_rows), W, n, dep_off, dep_ids, s)))
     return st;
+  // dependent entries with their bytes laid out contiguously per key, so a
+  // fill-time walk needs one load for (id, bytes) instead of id -> offsets ->
+  // bytes (cold round trips)
+  std::vector<int32_t> ids_host((size_t)dep_total);
+  if (dep_total) GM_CUDA_TRY(cudaMemcpyAsync(ids_host.data(), dep_ids, dep_total * 4, cudaMemcpyDeviceToHost, s));
+  GM_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<int4> ent((size_t)dep_total);
+  std::vector<uint8_t> dbytes;
+  for (int64_t i = 0; i < dep_total; ++i) {
+    const int32_t tid = ids_host[i];
+    const int64_t o0 = v->off_host[tid], o1 = v->off_host[tid + 1];
+    ent[i] = make_int4(tid, (int32_t)dbytes.size(), (int32_t)(o1 - o0), 0);
+    dbytes.insert(dbytes.end(), v->bytes_host.begin() + o0, v->bytes_host.begin() + o1);
+  }
+  int4* d_ent;
+  uint8_t* d_dbytes;
+  if ((st = c->mem.upload(&d_ent, ent.data(), ent.size())) ||
+      (st = c->mem.upload(&d_dbytes, dbytes.data(), dbytes.size())))
+    return st;
   c->host_binding.g = g->dev;
   c->host_binding.v = v->dev;
-  c->host_binding.c = DevCache{acc, dep_off, dep_ids};
+  c->host_binding.c = DevCache{acc, dep_off, dep_ids, d_ent, d_dbytes};
   DevBinding* db;
   if ((st = c->mem.alloc(&db, 1))) return st;
   GM_CUDA_TRY(cudaMemcpyAsync(db, &c->host_binding, sizeof(DevBinding), cudaMemcpyHostToDevice, s));
@@ -372,7 +424,8 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   unsigned long long* keys;
   uint32_t* err;
   uint8_t* sb;
-  if ((st = p->mem.alloc(&tops, (size_t)capacity * H * max_stacks)) ||
+  SlotHdr* hdr;
+  if ((st = p->mem.alloc(&hdr, (size_t)capacity)) || (st = p->mem.alloc(&tops, (size_t)capacity * H * max_stacks)) ||
       (st = p->mem.alloc(&meta, (size_t)capacity * H)) || (st = p->mem.alloc(&head, (size_t)capacity)) ||
       (st = p->mem.alloc(&hist, (size_t)capacity)) || (st = p->mem.alloc(&win, (size_t)capacity)) ||
       (st = p->mem.alloc(&bind, (size_t)capacity)) || (st = p->mem.alloc(&keys, (size_t)acap)) ||
@@ -387,7 +440,9 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   GM_CUDA_TRY(cudaMemset(head, 0, sizeof(int32_t) * (size_t)capacity));
   GM_CUDA_TRY(cudaMemset(hist, 0, sizeof(int32_t) * (size_t)capacity));
   GM_CUDA_TRY(cudaMemset(bind, 0, sizeof(void*) * (size_t)capacity));
-  p->dev = DevPool{capacity, max_stacks, H, tops, meta, head, hist, win, bind, DevArena{keys, acap - 1, err}, err};
+  GM_CUDA_TRY(cudaMemset(hdr, 0, sizeof(SlotHdr) * (size_t)capacity));
+  p->dev = DevPool{capacity, max_stacks, H,   tops, meta, head, hist, win, bind,
+                   DevArena{keys, acap - 1, err}, err, hdr};
   p->scratch_bytes = sb;
   p->scratch_cap = 1 << 16;
   p->scratch_i32 = scr;
@@ -415,18 +470,7 @@ gm_status gm_pool_reset(gm_pool* p, int32_t slot, const gm_grammar* g, const gm_
 gm_status gm_pool_fork(gm_pool* p, int32_t src, int32_t dst, void* stream) {
   if (!p || src < 0 || dst < 0 || src >= p->dev.capacity || dst >= p->dev.capacity)
     return fail(GM_ERR_INVALID, "slot out of range");
-  cudaStream_t s = as_stream(stream);
-  const DevPool& P = p->dev;
-  const size_t tops_per = (size_t)P.H * P.max_stacks;
-  GM_CUDA_TRY(cudaMemcpyAsync(P.tops + dst * tops_per, P.tops + src * tops_per, tops_per * sizeof(int2),
-                              cudaMemcpyDeviceToDevice, s));
-  GM_CUDA_TRY(cudaMemcpyAsync(P.meta + (size_t)dst * P.H, P.meta + (size_t)src * P.H, P.H * 4,
-                              cudaMemcpyDeviceToDevice, s));
-  GM_CUDA_TRY(cudaMemcpyAsync(P.head + dst, P.head + src, 4, cudaMemcpyDeviceToDevice, s));
-  GM_CUDA_TRY(cudaMemcpyAsync(P.hist_len + dst, P.hist_len + src, 4, cudaMemcpyDeviceToDevice, s));
-  GM_CUDA_TRY(cudaMemcpyAsync(P.window + dst, P.window + src, 4, cudaMemcpyDeviceToDevice, s));
-  GM_CUDA_TRY(cudaMemcpyAsync(P.binding + dst, P.binding + src, sizeof(void*), cudaMemcpyDeviceToDevice, s));
-  return GM_OK;
+  return launch_fork(p->dev, src, dst, as_stream(stream));
 }
 
 gm_status gm_accept_tokens(gm_pool* p, const int32_t* slots, const int32_t* token_ids, int32_t n,
@@ -461,6 +505,11 @@ gm_status gm_fill_tokens(gm_pool* p, const int32_t* slots, int32_t n, int32_t* b
 gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps, int32_t n, void* stream) {
   if (!p) return fail(GM_ERR_INVALID, "null pool");
   return launch_rollback(p->dev, slots, steps, n, as_stream(stream));
+}
+
+gm_status gm_pool_recycle(gm_pool* p, const int32_t* slots, int32_t n, void* stream) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  return launch_recycle(p->dev, slots, n, as_stream(stream));
 }
 
 gm_status gm_pool_check(gm_pool* p, int32_t* flags_out) {

@@ -1,24 +1,41 @@
 // K4 — batched accept_token / accept_bytes on device-resident stacks, plus
-// the small state kernels (reset, rollback, first-byte probe).
+// the small state kernels (reset, recycle, rollback, probe).
 //
 // Replaces Matcher.accept_token / accept_bytes / _sim_bytes / _rewrite_kernel
-// / _push_history / rollback (REF matcher.py:192-217, 239-326).  One thread
-// advances one request: the request's stack set is walked byte by byte with
-// walker-local frames; survivors are interned into the hash-consed arena
-// (parents first), deduplicated by (handle, node) — which is deduplication by
-// stack content because the arena is hash-consed (REF matcher.py:202-206) —
-// and written as the next entry of the slot's history ring.  A rejected token
-// leaves the slot unchanged (REF matcher.py:267-268).
+// / _push_history / rollback (REF matcher.py:192-217, 239-326).  One CTA (one
+// warp) advances one request: the warp stages the grammar tables into shared
+// memory with one coalesced copy, then lane 0 walks the request's stack set
+// byte by byte with walker-local frames; survivors are interned into the
+// hash-consed arena (parents first), deduplicated by (handle, node) — which
+// is deduplication by stack content because the arena is hash-consed
+// (REF matcher.py:202-206) — and written as the next entry of the slot's
+// history ring together with the slot header.  A rejected token leaves the
+// slot unchanged (REF matcher.py:267-268).
 #include "device.cuh"
 
 namespace gm {
 
 constexpr int kAccS = 32;
 constexpr int kAccF = 160;
+constexpr int kAccThreads = 32;
 
-__device__ void push_history(const DevPool& P, int32_t slot, int32_t h, int nt,
-                             const int32_t* refs, const int32_t* nodes, int terminated) {
-  const int32_t nh = (h + 1) % P.H;
+// Current (handle, node) set of a slot: from the header when it fits, else
+// from the ring.  Returns the count.
+__device__ int load_tops(const DevPool& P, int32_t slot, const SlotHdr& hdr, int2* out) {
+  if (hdr.ntops >= 0) {
+    for (int s = 0; s < hdr.ntops; ++s) out[s] = hdr.top[s];
+    return hdr.ntops;
+  }
+  const int32_t h = P.head[slot];
+  const int n = P.meta[(size_t)slot * P.H + h] & 0xFFFF;
+  const int2* tops = slot_tops(P, slot, h);
+  for (int s = 0; s < n; ++s) out[s] = tops[s];
+  return n;
+}
+
+__device__ void push_history(const DevPool& P, int32_t slot, const DevBinding* B, int nt, const int32_t* refs,
+                             const int32_t* nodes, int terminated) {
+  const int32_t nh = (P.head[slot] + 1) % P.H;
   int2* dst = slot_tops(P, slot, nh);
   for (int s = 0; s < nt; ++s) {
     const int32_t r = refs[s];
@@ -28,30 +45,26 @@ __device__ void push_history(const DevPool& P, int32_t slot, int32_t h, int nt,
   P.head[slot] = nh;
   const int32_t hl = P.hist_len[slot] + 1;
   P.hist_len[slot] = hl < P.window[slot] ? hl : P.window[slot];
+  write_header(P, slot, B, dst, nt, terminated);
 }
 
-// Shared by token and byte-string acceptance.  data/len = bytes to consume;
-// is_eos = EOS token.  Returns 1 if accepted.
-__device__ int accept_one(const DevPool& P, int32_t slot, const uint8_t* data, int64_t len,
-                          bool is_eos, bool reject_token) {
-  const DevBinding* B = P.binding[slot];
-  const DevGrammar& G = B->g;
-  const int32_t h = P.head[slot];
-  const int32_t meta = P.meta[(size_t)slot * P.H + h];
-  const int ntops = meta & 0xFFFF;
-  if ((meta >> 16) & 1) {  // REF matcher.py:276-277 "matcher is terminated"
+// Shared by token and byte-string acceptance (lane 0 only).  data/len =
+// bytes to consume; is_eos = EOS token.  Returns 1 if accepted.
+__device__ int accept_one(const DevPool& P, int32_t slot, const SlotHdr& hdr, const DevGrammar& G,
+                          const uint8_t* data, int64_t len, bool is_eos, bool reject_token) {
+  const DevBinding* B = hdr.binding;
+  if (hdr.flags & 1) {  // REF matcher.py:276-277 "matcher is terminated"
     atomicOr(P.err, kErrTerminated);
     return 0;
   }
-  const int2* tops = slot_tops(P, slot, h);
+  int2 tops[kAccS];
+  const int ntops = load_tops(P, slot, hdr, tops);
   Walker<kAccS, kAccF> w;
   w.reset();
   for (int s = 0; s < ntops; ++s) w.add(tops[s].x < 0 ? -1 : -2 - tops[s].x, tops[s].y);
   if (is_eos) {  // REF matcher.py:280-288
-    bool term = false;
-    for (int s = 0; s < w.n && !term; ++s) term = w.terminable(G, P.arena, w.ref[s], w.node[s]);
-    if (!term) return 0;
-    push_history(P, slot, h, w.n, w.ref, w.node, 1);
+    if (!(hdr.flags & 2)) return 0;
+    push_history(P, slot, B, w.n, w.ref, w.node, 1);
     return 1;
   }
   if (reject_token) return 0;  // special or empty token (REF matcher.py:289-293)
@@ -60,7 +73,7 @@ __device__ int accept_one(const DevPool& P, int32_t slot, const uint8_t* data, i
       if (!w.intern_all(P.arena)) break;
     }
     bool pb = false;
-    if (!w.template step<kAccS>(G, P.arena, data[i], &pb)) break;
+    if (!w.template step<kAccS>(G, P.arena, __ldg(data + i), &pb)) break;
   }
   if (w.err) {
     atomicOr(P.err, w.err);
@@ -75,51 +88,69 @@ __device__ int accept_one(const DevPool& P, int32_t slot, const uint8_t* data, i
     atomicOr(P.err, kErrCap);
     return 0;
   }
-  push_history(P, slot, h, w.n, w.ref, w.node, 0);
+  push_history(P, slot, B, w.n, w.ref, w.node, 0);
   return 1;
 }
 
-__global__ void accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots,
-                                     const int32_t* __restrict__ token_ids, int32_t n,
-                                     uint8_t* __restrict__ accepted) {
-  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void load_header(const DevPool& P, int32_t slot, SlotHdr* s_hdr) {
+  if (threadIdx.x < 16)
+    reinterpret_cast<int4*>(s_hdr)[threadIdx.x] = reinterpret_cast<const int4*>(P.hdr + slot)[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kAccThreads)
+accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t* __restrict__ token_ids, int32_t n,
+                     uint8_t* __restrict__ accepted) {
+  extern __shared__ __align__(16) uint8_t tables[];
+  __shared__ SlotHdr s_hdr;
+  const int32_t i = blockIdx.x;
   if (i >= n) return;
-  const int32_t slot = slots[i];
-  const int32_t tid = token_ids[i];
-  const DevVocab& Vc = P.binding[slot]->v;
+  const int32_t slot = __ldg(slots + i);
+  const int32_t tid = __ldg(token_ids + i);
+  load_header(P, slot, &s_hdr);
+  __syncthreads();
+  const DevBinding* B = s_hdr.binding;
+  const DevGrammar G = stage_grammar(B->g, tables);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const DevVocab& Vc = B->v;
   if (tid < 0 || tid >= Vc.V) {  // REF matcher.py:278-279
     atomicOr(P.err, kErrInvalid);
     accepted[i] = 0;
     return;
   }
-  const int32_t o0 = Vc.off[tid];
-  const int64_t len = Vc.off[tid + 1] - o0;
-  accepted[i] = (uint8_t)accept_one(P, slot, Vc.bytes + o0, len, tid == Vc.eos, Vc.reject[tid] != 0);
+  const int32_t o0 = __ldg(Vc.off + tid);
+  const int64_t len = __ldg(Vc.off + tid + 1) - o0;
+  accepted[i] = (uint8_t)accept_one(P, slot, s_hdr, G, Vc.bytes + o0, len, tid == Vc.eos, Vc.reject[tid] != 0);
 }
 
-__global__ void accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len,
-                                    uint8_t* accepted) {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  const int32_t h = P.head[slot];
-  const int32_t meta = P.meta[(size_t)slot * P.H + h];
-  if ((meta >> 16) & 1) {
+__global__ void __launch_bounds__(kAccThreads)
+accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len, uint8_t* accepted) {
+  extern __shared__ __align__(16) uint8_t tables[];
+  __shared__ SlotHdr s_hdr;
+  load_header(P, slot, &s_hdr);
+  __syncthreads();
+  const DevBinding* B = s_hdr.binding;
+  const DevGrammar G = stage_grammar(B->g, tables);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (s_hdr.flags & 1) {
     atomicOr(P.err, kErrTerminated);
     *accepted = 0;
     return;
   }
   if (len == 0) {  // REF matcher.py:253-258: empty input records a history entry
-    const int nt = meta & 0xFFFF;
-    const int2* tops = slot_tops(P, slot, h);
+    int2 tops[kAccS];
     int32_t refs[kAccS], nodes[kAccS];
+    const int nt = load_tops(P, slot, s_hdr, tops);
     for (int s = 0; s < nt; ++s) {
       refs[s] = tops[s].x < 0 ? -1 : -2 - tops[s].x;
       nodes[s] = tops[s].y;
     }
-    push_history(P, slot, h, nt, refs, nodes, 0);
+    push_history(P, slot, B, nt, refs, nodes, 0);
     *accepted = 1;
     return;
   }
-  *accepted = (uint8_t)accept_one(P, slot, data, len, false, false);
+  *accepted = (uint8_t)accept_one(P, slot, s_hdr, G, data, len, false, false);
 }
 
 __global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32_t start, int32_t window) {
@@ -128,12 +159,30 @@ __global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32
   P.head[slot] = 0;
   P.hist_len[slot] = 0;
   P.window[slot] = window;
-  slot_tops(P, slot, 0)[0] = make_int2(-1, start);
+  int2* t = slot_tops(P, slot, 0);
+  t[0] = make_int2(-1, start);
   P.meta[(size_t)slot * P.H] = 1;
+  write_header(P, slot, b, t, 1, 0);
 }
 
-__global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots,
-                                const int32_t* __restrict__ steps, int32_t n) {
+// Request recycling for serving loops: a terminated slot restarts at the
+// grammar's start state (fresh request, same grammar), others are untouched.
+__global__ void recycle_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t slot = slots[i];
+  if (!(P.hdr[slot].flags & 1)) return;
+  const DevBinding* b = P.binding[slot];
+  P.head[slot] = 0;
+  P.hist_len[slot] = 0;
+  int2* t = slot_tops(P, slot, 0);
+  t[0] = make_int2(-1, b->g.start_node);
+  P.meta[(size_t)slot * P.H] = 1;
+  write_header(P, slot, b, t, 1, 0);
+}
+
+__global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t* __restrict__ steps,
+                                int32_t n) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t slot = slots[i], k = steps[i];
@@ -142,8 +191,12 @@ __global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots,
     atomicOr(P.err, 1u << GM_ERR_ROLLBACK);
     return;
   }
-  P.head[slot] = ((P.head[slot] - k) % P.H + P.H) % P.H;
+  if (k == 0) return;
+  const int32_t h = ((P.head[slot] - k) % P.H + P.H) % P.H;
+  P.head[slot] = h;
   P.hist_len[slot] = hl - k;
+  const int32_t meta = P.meta[(size_t)slot * P.H + h];
+  write_header(P, slot, P.binding[slot], slot_tops(P, slot, h), meta & 0xFFFF, (meta >> 16) & 1);
 }
 
 // info: n_stacks, terminated, history_len, terminable, window; stacks copy;
@@ -162,8 +215,7 @@ __global__ void slot_probe_kernel(DevPool P, int32_t slot, int32_t* info, int2* 
   for (int s = 0; s < nt; ++s) {
     int32_t hh = tops[s].x, m = tops[s].y;
     if (s < max_out) stacks[s] = tops[s];
-    // walk the pop chain: every node reachable by silent completion
-    while (true) {
+    while (true) {  // every node reachable by silent completion
       for (int b = 0; b < 256; ++b) {
         const int32_t idx = m * G.n_classes + G.byte_class[b];
         if (G.trans_off[idx + 1] > G.trans_off[idx]) fb[b >> 5] |= 1u << (b & 31);
@@ -178,22 +230,45 @@ __global__ void slot_probe_kernel(DevPool P, int32_t slot, int32_t* info, int2* 
   info[0] = nt;
   info[1] = (meta >> 16) & 1;
   info[2] = P.hist_len[slot];
-  info[3] = term;
+  info[3] = term && !((meta >> 16) & 1);
   info[4] = P.window[slot];
   for (int i = 0; i < 8; ++i) bytes8[i] = fb[i];
 }
 
-gm_status launch_accept_tokens(const DevPool& P, const int32_t* slots, const int32_t* toks, int32_t n,
-                               uint8_t* acc, cudaStream_t s) {
+// branch / fork (REF matcher.py:328-355): copy the whole slot state.
+__global__ void fork_kernel(DevPool P, int32_t src, int32_t dst) {
+  const size_t per = (size_t)P.H * P.max_stacks;
+  for (size_t k = threadIdx.x; k < per; k += blockDim.x) P.tops[dst * per + k] = P.tops[src * per + k];
+  for (int k = threadIdx.x; k < P.H; k += blockDim.x) P.meta[(size_t)dst * P.H + k] = P.meta[(size_t)src * P.H + k];
+  if (threadIdx.x < 16)
+    reinterpret_cast<int4*>(P.hdr + dst)[threadIdx.x] = reinterpret_cast<const int4*>(P.hdr + src)[threadIdx.x];
+  if (threadIdx.x == 0) {
+    P.head[dst] = P.head[src];
+    P.hist_len[dst] = P.hist_len[src];
+    P.window[dst] = P.window[src];
+    P.binding[dst] = P.binding[src];
+  }
+}
+
+static gm_status set_smem_attr(const void* fn) {
+  GM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytes));
+  return GM_OK;
+}
+
+gm_status launch_accept_tokens(const DevPool& P, const int32_t* slots, const int32_t* toks, int32_t n, uint8_t* acc,
+                               cudaStream_t s) {
   if (n <= 0) return GM_OK;
-  const int threads = 64;
-  accept_tokens_kernel<<<(unsigned)ceil_div(n, threads), threads, 0, s>>>(P, slots, toks, n, acc);
+  static gm_status once = set_smem_attr(reinterpret_cast<const void*>(accept_tokens_kernel));
+  if (once) return once;
+  accept_tokens_kernel<<<n, kAccThreads, kStageBytes, s>>>(P, slots, toks, n, acc);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }
-gm_status launch_accept_bytes(const DevPool& P, int32_t slot, const uint8_t* data, int64_t len,
-                              uint8_t* acc, cudaStream_t s) {
-  accept_bytes_kernel<<<1, 1, 0, s>>>(P, slot, data, len, acc);
+gm_status launch_accept_bytes(const DevPool& P, int32_t slot, const uint8_t* data, int64_t len, uint8_t* acc,
+                              cudaStream_t s) {
+  static gm_status once = set_smem_attr(reinterpret_cast<const void*>(accept_bytes_kernel));
+  if (once) return once;
+  accept_bytes_kernel<<<1, kAccThreads, kStageBytes, s>>>(P, slot, data, len, acc);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }
@@ -203,8 +278,13 @@ gm_status launch_reset(const DevPool& P, int32_t slot, const DevBinding* b, int3
   GM_LAUNCH_CHECK();
   return GM_OK;
 }
-gm_status launch_rollback(const DevPool& P, const int32_t* slots, const int32_t* steps, int32_t n,
-                          cudaStream_t s) {
+gm_status launch_recycle(const DevPool& P, const int32_t* slots, int32_t n, cudaStream_t s) {
+  if (n <= 0) return GM_OK;
+  recycle_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(P, slots, n);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_rollback(const DevPool& P, const int32_t* slots, const int32_t* steps, int32_t n, cudaStream_t s) {
   if (n <= 0) return GM_OK;
   rollback_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(P, slots, steps, n);
   GM_LAUNCH_CHECK();
@@ -213,6 +293,11 @@ gm_status launch_rollback(const DevPool& P, const int32_t* slots, const int32_t*
 gm_status launch_probe(const DevPool& P, int32_t slot, int32_t* info, int2* stacks, int32_t max_out,
                        uint32_t* bytes8, cudaStream_t s) {
   slot_probe_kernel<<<1, 32, 0, s>>>(P, slot, info, stacks, max_out, bytes8);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_fork(const DevPool& P, int32_t src, int32_t dst, cudaStream_t s) {
+  fork_kernel<<<1, 256, 0, s>>>(P, src, dst);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

@@ -4,85 +4,106 @@
 // kernels/apply_token_bitmask_inplace_{cuda.cu,triton.py}); the reference
 // grammask has no apply step (REF bench.py:50-71 samples on the host).
 //
-// HBM-streaming design: one thread owns one 16-byte chunk of a logits row
-// (8 bf16/fp16 or 4 fp32 tokens) so a warp's store instruction covers 512
-// contiguous bytes.  The chunk's mask bits are a byte (or nibble) of one
-// bitmask word; fully-allowed chunks cost only the (shared) bitmask read,
-// fully-masked chunks are a single 128-bit store of -inf with no logits read,
-// and only mixed chunks read-modify-write.  Algorithmic traffic per row is
-// therefore 4*ceil(V/32) + s*M (M = masked tokens), the minimum for an
-// in-place kernel.
+// HBM-streaming design.  A warp owns "tiles" of 32 bitmask words = 1024
+// tokens of one row.  Lane l loads word l (one coalesced 128-byte load per
+// tile); the tile's logits are then covered by 16-byte chunks in lane-major
+// order, so every store instruction of the warp writes a contiguous 512-byte
+// span, and each lane fetches its chunk's mask byte (or nibble) from the
+// owning lane with a shuffle.  Fully allowed chunks cost nothing beyond the
+// (shared) mask word, fully masked chunks are one 128-bit store of -inf, and
+// mixed chunks store only their masked elements — logits are never read, so
+// per row the traffic is the algorithmic minimum 4*ceil(V/32) + s*M
+// (M = masked tokens).  Several tiles per warp are loaded before any store
+// (ILP) and the grid is sized to the 148 SMs.
 #include "common.cuh"
 
 namespace gm {
 namespace {
 
-__device__ __forceinline__ uint4 ld_v4(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void st_v4(void* p, uint4 v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
-               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+__device__ __forceinline__ void st_v4(void* p, uint32_t v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%1,%1,%1};" :: "l"(p), "r"(v) : "memory");
 }
 
-// EB = bytes per element, NEG = -inf bit pattern (replicated per lane).
+constexpr int kTileTok = 1024;  // tokens per warp tile (32 words)
+constexpr int kUnroll = 4;      // tiles in flight per warp
+
+// EB = bytes per element.
 template <int EB>
 __global__ void __launch_bounds__(256)
-apply_vec_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab,
-                 int64_t lstride_bytes, const int32_t* __restrict__ bitmask,
-                 int64_t bstride, const int32_t* __restrict__ indices,
-                 uint32_t neg_pattern) {
+apply_tile_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab, int64_t lstride_bytes,
+                  const int32_t* __restrict__ bitmask, int64_t bstride, const int32_t* __restrict__ indices,
+                  uint32_t neg, int64_t tiles_per_row) {
   constexpr int VEC = 16 / EB;                 // tokens per 16-byte chunk
-  constexpr uint32_t FULL = (VEC == 32) ? 0xFFFFFFFFu : ((1u << VEC) - 1u);
-  const int64_t chunks = (vocab + VEC - 1) / VEC;
-  for (int64_t i = blockIdx.y; i < n_rows; i += gridDim.y) {
-    const int64_t row = indices ? (int64_t)indices[i] : i;
-    char* rowp = logits + row * lstride_bytes;
-    const uint32_t* brow = reinterpret_cast<const uint32_t*>(bitmask + row * bstride);
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks;
-         c += (int64_t)gridDim.x * blockDim.x) {
-      const int64_t tok0 = c * VEC;
-      const uint32_t word = __ldg(brow + (tok0 >> 5));
-      uint32_t bits = (word >> (tok0 & 31)) & FULL;
-      int nvalid = VEC;
-      if (tok0 + VEC > vocab) {  // ragged tail: tokens >= vocab untouched
-        nvalid = (int)(vocab - tok0);
-        bits |= FULL & ~((1u << nvalid) - 1u);
-      }
-      if (bits == FULL) continue;
-      char* p = rowp + tok0 * EB;
-      if (nvalid == VEC && bits == 0) {
-        st_v4(p, make_uint4(neg_pattern, neg_pattern, neg_pattern, neg_pattern));
-        continue;
-      }
-      uint4 v = ld_v4(p);
-      uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  constexpr int CHUNKS = kTileTok / VEC;       // chunks per tile
+  constexpr int ROUNDS = CHUNKS / 32;          // store rounds per tile
+  constexpr int CPW = 32 / VEC;                // chunks per mask word
+  constexpr uint32_t FULL = (1u << VEC) - 1u;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = n_rows * tiles_per_row;
+  const int64_t words_row = (vocab + 31) >> 5;
+
+  for (int64_t base = warp * kUnroll; base < total; base += n_warps * kUnroll) {
+    uint32_t w[kUnroll];
 #pragma unroll
-      for (int j = 0; j < VEC; ++j) {
-        if (!((bits >> j) & 1u)) {
-          if (EB == 4) {
-            w[j] = neg_pattern;
-          } else {
-            const int k = j >> 1, sh = (j & 1) * 16;
-            w[k] = (w[k] & ~(0xFFFFu << sh)) | ((neg_pattern & 0xFFFFu) << sh);
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t tile = base + u;
+      w[u] = 0xFFFFFFFFu;
+      if (tile < total) {
+        const int64_t i = tile / tiles_per_row;
+        const int64_t t = tile - i * tiles_per_row;
+        const int64_t row = indices ? (int64_t)__ldg(indices + i) : i;
+        const int64_t word = t * 32 + lane;
+        if (word < words_row) w[u] = (uint32_t)__ldg(bitmask + row * bstride + word);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t tile = base + u;
+      if (tile >= total) break;
+      if (__all_sync(0xFFFFFFFFu, w[u] == 0xFFFFFFFFu)) continue;  // whole tile allowed
+      const int64_t i = tile / tiles_per_row;
+      const int64_t t = tile - i * tiles_per_row;
+      const int64_t row = indices ? (int64_t)__ldg(indices + i) : i;
+      char* rowp = logits + row * lstride_bytes;
+      const int64_t tok_base = t * kTileTok;
+#pragma unroll
+      for (int r = 0; r < ROUNDS; ++r) {
+        const int c = r * 32 + lane;  // chunk within the tile
+        const uint32_t word = __shfl_sync(0xFFFFFFFFu, w[u], c / CPW);
+        uint32_t bits = (word >> ((c % CPW) * VEC)) & FULL;
+        const int64_t tok0 = tok_base + (int64_t)c * VEC;
+        if (tok0 >= vocab) continue;
+        int nvalid = VEC;
+        if (tok0 + VEC > vocab) {
+          nvalid = (int)(vocab - tok0);
+          bits |= FULL & ~((1u << nvalid) - 1u);
+        }
+        if (bits == FULL) continue;
+        char* p = rowp + tok0 * EB;
+        if (bits == 0) {
+          st_v4(p, neg);
+        } else {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) {
+            if (!((bits >> j) & 1u)) {
+              if (EB == 4) *reinterpret_cast<uint32_t*>(p + j * 4) = neg;
+              else *reinterpret_cast<uint16_t*>(p + j * 2) = (uint16_t)neg;
+            }
           }
         }
       }
-      st_v4(p, make_uint4(w[0], w[1], w[2], w[3]));
     }
   }
 }
 
-// Unaligned rows: one thread per token.
+// Rows that are not 16-byte aligned: one thread per token.
 template <int EB>
 __global__ void __launch_bounds__(256)
-apply_scalar_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab,
-                    int64_t lstride_bytes, const int32_t* __restrict__ bitmask,
-                    int64_t bstride, const int32_t* __restrict__ indices,
-                    uint32_t neg_pattern) {
+apply_scalar_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab, int64_t lstride_bytes,
+                    const int32_t* __restrict__ bitmask, int64_t bstride, const int32_t* __restrict__ indices,
+                    uint32_t neg) {
   for (int64_t i = blockIdx.y; i < n_rows; i += gridDim.y) {
     const int64_t row = indices ? (int64_t)indices[i] : i;
     char* rowp = logits + row * lstride_bytes;
@@ -90,8 +111,8 @@ apply_scalar_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab,
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < vocab;
          t += (int64_t)gridDim.x * blockDim.x) {
       if ((__ldg(brow + (t >> 5)) >> (t & 31)) & 1) continue;
-      if (EB == 4) *reinterpret_cast<uint32_t*>(rowp + t * 4) = neg_pattern;
-      else *reinterpret_cast<uint16_t*>(rowp + t * 2) = (uint16_t)neg_pattern;
+      if (EB == 4) *reinterpret_cast<uint32_t*>(rowp + t * 4) = neg;
+      else *reinterpret_cast<uint16_t*>(rowp + t * 2) = (uint16_t)neg;
     }
   }
 }
@@ -101,9 +122,8 @@ apply_scalar_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab,
 
 using namespace gm;
 
-extern "C" gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_rows,
-                                      int64_t vocab_size, int64_t logits_stride,
-                                      const int32_t* bitmask, int64_t bitmask_stride,
+extern "C" gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_rows, int64_t vocab_size,
+                                      int64_t logits_stride, const int32_t* bitmask, int64_t bitmask_stride,
                                       const int32_t* indices, void* stream) {
   if (n_rows < 0 || vocab_size < 0) return fail(GM_ERR_INVALID, "negative shape");
   if (n_rows == 0 || vocab_size == 0) return GM_OK;
@@ -119,19 +139,30 @@ extern "C" gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_row
   const int64_t lstride_bytes = logits_stride * eb;
   const bool aligned = (reinterpret_cast<uintptr_t>(logits) % 16 == 0) && (lstride_bytes % 16 == 0);
   cudaStream_t s = as_stream(stream);
-  const int threads = 256;
-  const int64_t per_thread = aligned ? (16 / eb) : 1;
-  int64_t gx = ceil_div(ceil_div(vocab_size, per_thread), threads);
-  if (gx > 65535) gx = 65535;
-  const unsigned gy = (unsigned)(n_rows < 65535 ? n_rows : 65535);
-  dim3 grid((unsigned)gx, gy);
   char* lp = static_cast<char*>(logits);
   if (aligned) {
-    if (eb == 4) apply_vec_kernel<4><<<grid, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask, bitmask_stride, indices, neg);
-    else apply_vec_kernel<2><<<grid, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask, bitmask_stride, indices, neg);
+    const int64_t tiles_per_row = ceil_div(vocab_size, kTileTok);
+    const int64_t warps = ceil_div(n_rows * tiles_per_row, kUnroll);
+    const int threads = 256;
+    int64_t blocks = ceil_div(warps * 32, threads);
+    const int64_t cap = (int64_t)kNumSMs * 8;  // 8 x 256 threads resident per SM
+    if (blocks > cap) blocks = cap;
+    if (eb == 4)
+      apply_tile_kernel<4><<<(unsigned)blocks, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask,
+                                                               bitmask_stride, indices, neg, tiles_per_row);
+    else
+      apply_tile_kernel<2><<<(unsigned)blocks, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask,
+                                                               bitmask_stride, indices, neg, tiles_per_row);
   } else {
-    if (eb == 4) apply_scalar_kernel<4><<<grid, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask, bitmask_stride, indices, neg);
-    else apply_scalar_kernel<2><<<grid, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask, bitmask_stride, indices, neg);
+    int64_t gx = ceil_div(vocab_size, 256);
+    if (gx > 65535) gx = 65535;
+    dim3 grid((unsigned)gx, (unsigned)(n_rows < 65535 ? n_rows : 65535));
+    if (eb == 4)
+      apply_scalar_kernel<4><<<grid, 256, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask, bitmask_stride,
+                                                  indices, neg);
+    else
+      apply_scalar_kernel<2><<<grid, 256, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask, bitmask_stride,
+                                                  indices, neg);
   }
   GM_LAUNCH_CHECK();
   return GM_OK;

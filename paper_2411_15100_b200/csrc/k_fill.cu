@@ -6,13 +6,16 @@
 // plus the EOS bit iff some stack is terminable, with bits >= V zero
 // (REF matcher.py:388-390, 411-412).  This is the reference's Algorithm-1 set
 // algebra with the dense accepted row as the stored form, so the expand is a
-// pure streaming OR of L2-resident rows.
+// pure streaming OR of rows.
 //
-// One CTA per request row.  Phase 1: the CTA's threads each walk one
-// context-dependent token of one stack against the request's full stack
-// (device arena chain), setting bits of a shared-memory row.  Phase 2: all
-// threads stream the output row with 128-bit loads/stores, OR-ing the cached
-// rows of every stack top, the shared dependent row and the universe.
+// One CTA per request row, designed for a cold L2 (the model's forward pass
+// evicts everything between decode steps), i.e. for few dependent round
+// trips: the slot header (one 256-byte record) gives keys, dependent ranges
+// and the EOS fact; the grammar tables are staged into shared memory in one
+// coalesced copy; each dependent token (id + bytes, contiguous per key) is
+// walked by one thread against the request's full stack, setting bits of a
+// shared-memory row; finally all threads stream the output row with 128-bit
+// loads/stores.
 #include "device.cuh"
 
 namespace gm {
@@ -20,72 +23,87 @@ namespace gm {
 constexpr int kFillThreads = 256;
 constexpr int kDepS = 16;
 constexpr int kDepF = 64;
-constexpr int kMaxTopsInFill = 32;
 
 __global__ void __launch_bounds__(kFillThreads)
 fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
-            int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply) {
-  extern __shared__ uint32_t dep_acc[];  // [W]
-  __shared__ int32_t s_key[kMaxTopsInFill];
-  __shared__ int32_t s_dep0[kMaxTopsInFill + 1];
-  __shared__ int s_term, s_partial;
+            int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wmax) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* dep_acc = reinterpret_cast<uint32_t*>(smem);         // [Wmax]
+  uint8_t* tables = smem + (((size_t)Wmax * 4 + 15) & ~(size_t)15);   // staged grammar blob
+  __shared__ SlotHdr s_hdr;
+  __shared__ int s_partial, s_nt;
+  __shared__ int32_t s_key[32], s_lo[32], s_hi[32];
+  __shared__ int2 s_top[32];
   const int32_t i = blockIdx.x;
   if (i >= n) return;
-  const int32_t slot = slots[i];
-  const int64_t row = rows ? (int64_t)rows[i] : (int64_t)i;
-  const DevBinding* B = P.binding[slot];
-  const DevGrammar& G = B->g;
+  const int32_t slot = __ldg(slots + i);
+  const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
+
+  // header: 256 bytes, one coalesced load
+  if (threadIdx.x < 16)
+    reinterpret_cast<int4*>(&s_hdr)[threadIdx.x] = reinterpret_cast<const int4*>(P.hdr + slot)[threadIdx.x];
+  if (threadIdx.x == 0) s_partial = 0;
+  __syncthreads();
+  const DevBinding* B = s_hdr.binding;
   const DevVocab& Vc = B->v;
   const DevCache& C = B->c;
   const int32_t W = Vc.W;
-  const int32_t h = P.head[slot];
-  const int32_t meta = P.meta[(size_t)slot * P.H + h];
-  const int ntops = meta & 0xFFFF;
-  const bool terminated = (meta >> 16) & 1;
-  const int2* tops = slot_tops(P, slot, h);
-
-  for (int32_t w = threadIdx.x; w < W; w += blockDim.x) dep_acc[w] = 0u;
+  const bool terminated = s_hdr.flags & 1;
   if (threadIdx.x == 0) {
-    int term = 0, total = 0;
-    if (terminated) atomicOr(P.err, kErrTerminated);
-    for (int s = 0; s < ntops && s < kMaxTopsInFill; ++s) {
-      const int2 t = tops[s];
-      s_key[s] = G.key_of_node[t.y];
-      s_dep0[s] = total;
-      const int32_t kk = s_key[s];
-      total += kk >= 0 ? C.dep_off[kk + 1] - C.dep_off[kk] : 0;
-      // terminable: POP(node) && every chain frame POP (term bit)
-      if (!terminated && (G.node_flags[t.y] & GM_NODE_POP)) {
-        const int32_t hh = t.x;
-        if (hh < 0 || key_term(arena_load(P.arena, hh))) term = 1;
+    int nt = s_hdr.ntops;
+    if (terminated) {
+      atomicOr(P.err, kErrTerminated);
+      nt = 0;
+    } else if (nt >= 0) {
+      for (int s = 0; s < nt; ++s) {
+        s_key[s] = s_hdr.key[s];
+        s_lo[s] = s_hdr.dep_lo[s];
+        s_hi[s] = s_hdr.dep_hi[s];
+        s_top[s] = s_hdr.top[s];
+      }
+    } else {  // more stacks than the header holds: read the ring entry
+      const int32_t h = P.head[slot];
+      nt = P.meta[(size_t)slot * P.H + h] & 0xFFFF;
+      const int2* tops = slot_tops(P, slot, h);
+      for (int s = 0; s < nt; ++s) {
+        const int32_t k = B->g.key_of_node[tops[s].y];
+        s_key[s] = k;
+        s_lo[s] = k >= 0 ? C.dep_off[k] : 0;
+        s_hi[s] = k >= 0 ? C.dep_off[k + 1] : 0;
+        s_top[s] = tops[s];
       }
     }
-    s_dep0[ntops < kMaxTopsInFill ? ntops : kMaxTopsInFill] = total;
-    s_term = term;
-    s_partial = 0;
+    s_nt = nt;
   }
   __syncthreads();
-  const int nt = terminated ? 0 : (ntops < kMaxTopsInFill ? ntops : kMaxTopsInFill);
+  const int nt = s_nt;
+  int total = 0;
+  for (int s = 0; s < nt; ++s) total += s_hi[s] - s_lo[s];
+
+  for (int32_t w = threadIdx.x; w < W; w += blockDim.x) dep_acc[w] = 0u;
+  DevGrammar G = B->g;
+  if (total) G = stage_grammar(B->g, tables);
+  __syncthreads();
 
   // Phase 1: dependent-token walks, one thread per (stack, dependent token).
-  const int32_t total_deps = s_dep0[nt];
-  for (int32_t q = threadIdx.x; q < total_deps; q += blockDim.x) {
-    int s = 0;
-    while (s + 1 < nt && s_dep0[s + 1] <= q) ++s;
-    const int32_t kk = s_key[s];
-    const int32_t tid = C.dep_ids[C.dep_off[kk] + (q - s_dep0[s])];
+  for (int32_t q = threadIdx.x; q < total; q += blockDim.x) {
+    int s = 0, base = 0;
+    while (q - base >= s_hi[s] - s_lo[s]) {
+      base += s_hi[s] - s_lo[s];
+      ++s;
+    }
+    const int4 ent = __ldg(C.dep_ent + s_lo[s] + (q - base));
+    const int32_t tid = ent.x;
     if ((dep_acc[tid >> 5] >> (tid & 31)) & 1u) continue;  // already allowed by another stack
-    const int2 t = tops[s];
-    const int32_t o0 = __ldg(Vc.off + tid);
-    const int len = __ldg(Vc.off + tid + 1) - o0;
-    const uint8_t* tok = Vc.bytes + o0;
+    const uint8_t* tok = C.dep_bytes + ent.y;
+    const int2 t = s_top[s];
     Walker<kDepS, kDepF> w;
     w.reset();
     w.add(t.x < 0 ? -1 : -2 - t.x, t.y);
-    for (int b = 0; b < len; ++b) {
+    for (int b = 0; b < ent.z; ++b) {
       if (w.nf > kDepF / 2) w.intern_all(P.arena);
       bool pb = false;
-      if (!w.template step<kDepS>(G, P.arena, tok[b], &pb)) break;
+      if (!w.template step<kDepS>(G, P.arena, __ldg(tok + b), &pb)) break;
     }
     if (w.err) atomicOr(P.err, w.err);
     if (w.n > 0) atomicOr(dep_acc + (tid >> 5), 1u << (tid & 31));
@@ -95,7 +113,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   // Phase 2: expand.  128-bit vectors when the row is 16-byte aligned.
   uint32_t* out = bitmask + row * bstride;
   const int32_t eos_w = Vc.eos >> 5;
-  const uint32_t eos_bit = s_term ? (1u << (Vc.eos & 31)) : 0u;
+  const uint32_t eos_bit = (!terminated && (s_hdr.flags & 2)) ? (1u << (Vc.eos & 31)) : 0u;
   const uint32_t tail = (Vc.V & 31) ? ((1u << (Vc.V & 31)) - 1u) : 0xFFFFFFFFu;
   bool partial = false;
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && (W % 4 == 0);
@@ -116,8 +134,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
         const int32_t w = w4 * 4 + e;
         if (w == eos_w) v[e] |= eos_bit;
         if (w == W - 1) v[e] &= tail;
-        const uint32_t full = (w == W - 1) ? tail : 0xFFFFFFFFu;
-        partial |= (v[e] != full);
+        partial |= (v[e] != ((w == W - 1) ? tail : 0xFFFFFFFFu));
       }
       reinterpret_cast<uint4*>(out)[w4] = make_uint4(v[0], v[1], v[2], v[3]);
     }
@@ -130,9 +147,8 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       }
       acc &= __ldg(Vc.universe + w);
       if (w == eos_w) acc |= eos_bit;
-      const uint32_t full = (w == W - 1) ? tail : 0xFFFFFFFFu;
       if (w == W - 1) acc &= tail;
-      partial |= (acc != full);
+      partial |= (acc != ((w == W - 1) ? tail : 0xFFFFFFFFu));
       out[w] = acc;
     }
   }
@@ -143,19 +159,18 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   }
 }
 
-gm_status launch_fill(const DevPool& P, const int32_t* slots, int32_t n, int32_t* bitmask,
-                      int64_t bstride, const int32_t* rows, uint8_t* need_apply, int32_t W,
-                      cudaStream_t s) {
+gm_status launch_fill(const DevPool& P, const int32_t* slots, int32_t n, int32_t* bitmask, int64_t bstride,
+                      const int32_t* rows, uint8_t* need_apply, int32_t Wmax, cudaStream_t s) {
   if (n <= 0) return GM_OK;
-  const size_t smem = (size_t)W * 4;
+  const size_t smem = (((size_t)Wmax * 4 + 15) & ~(size_t)15) + kStageBytes;
   static bool attr_set = false;
   if (!attr_set) {
-    GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set = true;
   }
-  if (smem > 200 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for fill kernel");
-  fill_kernel<<<n, kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride,
-                                            rows, need_apply);
+  if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for fill kernel");
+  fill_kernel<<<n, kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows,
+                                            need_apply, Wmax);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

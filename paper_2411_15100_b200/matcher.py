@@ -298,6 +298,12 @@ def batch_fill(pool: MatcherPool, slots: torch.Tensor, bitmask: torch.Tensor, ro
                                            _lib.stream_ptr(stream)), "gm_fill_tokens")
 
 
+def batch_recycle(pool: MatcherPool, slots: torch.Tensor, stream=None) -> None:
+    """Restart every terminated slot among ``slots`` (serving loops)."""
+    _lib.check(_lib.load().gm_pool_recycle(pool.handle, slots.data_ptr(), slots.numel(), _lib.stream_ptr(stream)),
+               "gm_pool_recycle")
+
+
 def batch_accept(pool: MatcherPool, slots: torch.Tensor, tokens: torch.Tensor, out: Optional[torch.Tensor] = None,
                  stream=None) -> torch.Tensor:
     """K4 over device slot ids / token ids; returns uint8 accepted flags (device)."""

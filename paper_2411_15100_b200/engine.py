@@ -157,6 +157,40 @@ def build_cache_rows(grammar: DeviceGrammar, dvocab: DeviceVocab, key_begin: int
     return acc, dep
 
 
+def shard_range(n_keys: int, world: int, rank: int):
+    """Contiguous block of cache keys owned by ``rank``."""
+    per = (n_keys + world - 1) // world if world else n_keys
+    return min(rank * per, n_keys), min((rank + 1) * per, n_keys), per
+
+
+def sharded_rows(build, n_keys: int, words: int, device, group=None):
+    """Position-sharded cache rows: each rank builds its key block with
+    ``build(lo, n) -> (acc, dep)`` and one all-gather replicates the finished
+    rows to every rank (NCCL over NVLink on the GPU box; gloo in CPU tests).
+    Returns full (acc, dep) [n_keys, words] int32 identical on every rank."""
+    world = 1
+    if group is not None:
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group)
+    if world <= 1:
+        return build(0, n_keys)
+    import torch.distributed as dist
+
+    rank = dist.get_rank(group)
+    lo, hi, per = shard_range(n_keys, world, rank)
+    acc_l, dep_l = build(lo, hi - lo)
+    pad = torch.zeros((2, per, words), dtype=torch.int32, device=device)
+    pad[0, : hi - lo] = acc_l
+    pad[1, : hi - lo] = dep_l
+    full = torch.empty((world * 2, per, words), dtype=torch.int32, device=device)
+    dist.all_gather_into_tensor(full, pad, group=group)
+    full = full.view(world, 2, per, words)
+    acc = full[:, 0].reshape(world * per, words)[:n_keys].contiguous()
+    dep = full[:, 1].reshape(world * per, words)[:n_keys].contiguous()
+    return acc, dep
+
+
 def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOptions] = None, *,
                       root_rule_name: Optional[str] = None, group=None, stream=None,
                       uncached: bool = False) -> CompiledDeviceGrammar:
@@ -168,40 +202,17 @@ def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOp
     t1 = time.perf_counter()
     grammar = DeviceGrammar(tables)
     n_keys = grammar.n_keys
-    world = 1
-    if group is not None:
-        import torch.distributed as dist
-
-        world = dist.get_world_size(group)
     if uncached:
         # no cache: every token is context dependent, fill walks the whole
         # vocabulary (the reference's uncached path, REF matcher.py:446-460)
-        universe = torch.empty(dvocab.words, dtype=torch.int32, device=dvocab.device)
-        lib = _lib.load()
-        ptr = lib.gm_vocab_universe(dvocab.handle)
-        u = np.zeros(dvocab.words, dtype=np.uint32)
-        for t in range(dvocab.size):
-            if t not in dvocab.vocab.special_tokens and dvocab.vocab.tokens[t]:
-                u[t >> 5] |= np.uint32(1 << (t & 31))
-        del ptr, universe
+        v = dvocab.vocab
+        ok = np.fromiter((t not in v.special_tokens and len(v.tokens[t]) > 0 for t in range(v.size)), bool, v.size)
+        u = np.packbits(np.concatenate([ok, np.zeros(32 * dvocab.words - v.size, bool)]), bitorder="little")
         acc = torch.zeros((n_keys, dvocab.words), dtype=torch.int32, device=dvocab.device)
-        dep = torch.from_numpy(u.view(np.int32)).to(dvocab.device).expand(n_keys, -1).contiguous()
-    elif world <= 1:
-        acc, dep = build_cache_rows(grammar, dvocab, 0, n_keys, stream)
+        dep = torch.from_numpy(u.view(np.int32).copy()).to(dvocab.device).expand(n_keys, -1).contiguous()
     else:
-        import torch.distributed as dist
-
-        rank = dist.get_rank(group)
-        per = (n_keys + world - 1) // world
-        lo, hi = min(rank * per, n_keys), min((rank + 1) * per, n_keys)
-        acc_l, dep_l = build_cache_rows(grammar, dvocab, lo, hi - lo, stream)
-        pad = torch.zeros((2, per, dvocab.words), dtype=torch.int32, device=dvocab.device)
-        pad[0, : hi - lo] = acc_l
-        pad[1, : hi - lo] = dep_l
-        full = torch.empty((world, 2, per, dvocab.words), dtype=torch.int32, device=dvocab.device)
-        dist.all_gather_into_tensor(full, pad, group=group)
-        acc = full[:, 0].reshape(world * per, -1)[:n_keys].contiguous()
-        dep = full[:, 1].reshape(world * per, -1)[:n_keys].contiguous()
+        acc, dep = sharded_rows(lambda lo, n: build_cache_rows(grammar, dvocab, lo, n, stream), n_keys,
+                                dvocab.words, dvocab.device, group)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     cache = DeviceCache(grammar, dvocab, acc, dep, stream)

@@ -211,7 +211,8 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clocks:
         for s in range(S):
-            flush.zero_()
+            if not args.no_flush:
+                flush.zero_()
             logits = ring[s % n_ring]
             e = ev[s]
             e[0].record(stream)
@@ -462,6 +463,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=24)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostic only: keep L2 warm between steps")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -521,7 +523,7 @@ def main():
             "all_accepted": r["all_accepted"],
             "cache": r["stats"],
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             out["cpu_baseline"] = cpu_baseline(args, r)
         print(json.dumps(out))
     if world > 1:

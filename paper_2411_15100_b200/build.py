@@ -53,6 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     nvcc = _nvcc()
     BUILD.mkdir(exist_ok=True)
     include = ["-I", str(ROOT / "include"), "-I", str(CSRC)]
+    if os.environ.get("GMASK_VERIFY") == "1":  # debug: cross-check cached arena keys
+        include += ["-DGM_VERIFY_KNOWN"]
 
     def compile_one(src: str):
         obj = BUILD / (Path(src).stem + ".o")

@@ -1,6 +1,6 @@
 // Device-side data model shared by the cache builder (K1), fill (K2) and
 // accept (K4) kernels: grammar tables, vocabulary, the hash-consed stack
-// arena, and the byte-level stack-set walker.
+// arena, the slot header and the byte-level stack-set walker.
 //
 // Stack model (restates the reference's matching stacks, REF pda.py:539-545,
 // pstack.py:1-16): a stack is (chain, node) where `node` is the resting
@@ -17,6 +17,14 @@
 //     one frame and repeat from the caller's return node.
 // Spent finals (dead ends) are popped through after the step (REF matcher.py
 // 192-206) so resting nodes are always cache keys.
+//
+// Latency design: between decode steps the model's forward pass evicts L2, so
+// the per-step kernels are bounded by dependent HBM round trips, not bytes.
+// Everything a step needs is therefore reachable in few hops: a 256-byte slot
+// header (pointers + current tops + cache keys + dependent ranges + EOS fact),
+// one "binding blob" per (grammar, vocabulary) holding the walker tables and
+// per-node cache info (staged into shared memory with one coalesced copy), and
+// 32-byte token records with the token bytes inline.
 #pragma once
 #include <stdint.h>
 
@@ -32,6 +40,19 @@ enum : uint32_t {
   kErrInvalid = 1u << GM_ERR_INVALID,
 };
 
+// ---------------------------------------------------------------------------
+// Table blob: [BlobHdr | byte_class[256] | node_flags[n] | trans_off[n*C+1] |
+// trans int2[] | push_pool[] | key_of_node[n] | node_rule[n] | node_info int4[n]]
+// all sections 16-byte aligned; offsets in bytes from the blob start.
+// node_info[n] = (cache key, first dependent, end dependent, rule) and is only
+// present in binding blobs (grammar blobs have o_ninfo = 0).
+struct BlobHdr {
+  int32_t bytes, n_classes, n_nodes, o_bc;
+  int32_t o_flags, o_toff, o_trans, o_pool;
+  int32_t o_kon, o_rule, o_ninfo, o_fast, pad[4];
+};
+static_assert(sizeof(BlobHdr) == 64, "BlobHdr layout");
+
 struct DevGrammar {
   int32_t n_nodes, n_rules, n_classes, start_node, n_keys, n_fstates;
   const uint8_t* byte_class;   // [256]
@@ -44,33 +65,70 @@ struct DevGrammar {
   const int32_t* key_of_node;  // [n_nodes] -> key index or -1
   const int32_t* follow_start; // [n_rules]
   const int32_t* follow_next;  // [n_fstates*n_classes]
-  // The walker tables (byte_class .. key_of_node) live in one contiguous
-  // 16-byte-aligned blob so a CTA can stage them into shared memory with a
-  // single coalesced copy.
+  const int4* node_info;       // binding views only
+  const int32_t* fast;         // [n_nodes*n_classes] single-stack DFA move, -1 dies, -2 general
   const uint8_t* blob;
   int32_t blob_bytes;
 };
 
+// Walker view of a blob located at `base` (global or shared memory).
+__device__ __forceinline__ DevGrammar blob_view(const uint8_t* base) {
+  const BlobHdr* h = reinterpret_cast<const BlobHdr*>(base);
+  DevGrammar g{};
+  g.n_classes = h->n_classes;
+  g.n_nodes = h->n_nodes;
+  g.byte_class = base + h->o_bc;
+  g.node_flags = base + h->o_flags;
+  g.trans_off = reinterpret_cast<const int32_t*>(base + h->o_toff);
+  g.trans = reinterpret_cast<const int2*>(base + h->o_trans);
+  g.push_pool = reinterpret_cast<const int32_t*>(base + h->o_pool);
+  g.key_of_node = reinterpret_cast<const int32_t*>(base + h->o_kon);
+  g.node_rule = reinterpret_cast<const int32_t*>(base + h->o_rule);
+  g.node_info = h->o_ninfo ? reinterpret_cast<const int4*>(base + h->o_ninfo) : nullptr;
+  g.fast = reinterpret_cast<const int32_t*>(base + h->o_fast);
+  g.blob = base;
+  g.blob_bytes = h->bytes;
+  return g;
+}
+
 constexpr int kStageBytes = 32 * 1024;  // shared-memory budget for staged tables
 
-// Cooperative copy of the grammar blob into shared memory; returns a view
-// whose table pointers address the shared copy (or the global tables when
-// the blob does not fit).  Must be called by every thread of the CTA.
-__device__ __forceinline__ DevGrammar stage_grammar(const DevGrammar& G, uint8_t* smem) {
-  DevGrammar g = G;
-  if (G.blob_bytes > kStageBytes) return g;
-  const int4* src = reinterpret_cast<const int4*>(G.blob);
-  int4* dst = reinterpret_cast<int4*>(smem);
-  for (int i = threadIdx.x; i < G.blob_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-  auto rb = [&](const void* p) { return smem + (reinterpret_cast<const uint8_t*>(p) - G.blob); };
-  g.byte_class = rb(G.byte_class);
-  g.node_flags = rb(G.node_flags);
-  g.trans_off = reinterpret_cast<const int32_t*>(rb(G.trans_off));
-  g.trans = reinterpret_cast<const int2*>(rb(G.trans));
-  g.push_pool = reinterpret_cast<const int32_t*>(rb(G.push_pool));
-  g.key_of_node = reinterpret_cast<const int32_t*>(rb(G.key_of_node));
-  g.node_rule = reinterpret_cast<const int32_t*>(rb(G.node_rule));
-  return g;
+// Stage a blob (`bytes` long, 16-byte multiple) into shared memory with one
+// TMA bulk copy (cp.async.bulk, completion tracked by an mbarrier): a single
+// HBM round trip however large the blob, instead of a loop of per-thread
+// loads.  Returns a view of the shared copy — or of the global blob when it
+// does not fit.  Must be called by every thread of the CTA (barrier inside).
+// TMA bulk-copy helpers (cp.async.bulk global -> shared, mbarrier-tracked).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mbar, uint32_t tx_bytes) {
+  const uint32_t m = smem_u32(mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(tx_bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mbar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, uint32_t parity) {
+  const uint32_t m = smem_u32(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(m), "r"(parity) : "memory");
+  }
+}
+
+__device__ __forceinline__ DevGrammar stage_blob(const uint8_t* blob, int32_t bytes, uint8_t* smem) {
+  __shared__ __align__(8) unsigned long long mbar;
+  const bool fits = bytes <= kStageBytes;
+  if (fits && threadIdx.x == 0) {
+    mbar_init(&mbar, (uint32_t)bytes);
+    bulk_g2s(smem, blob, (uint32_t)bytes, &mbar);
+  }
+  __syncthreads();
+  if (fits) mbar_wait(&mbar, 0);
+  return blob_view(fits ? smem : blob);
 }
 
 struct DevVocab {
@@ -80,14 +138,29 @@ struct DevVocab {
   const int32_t* sorted_ids;   // non-special non-empty ids, lexicographic
   const uint32_t* universe;    // [W]
   const uint8_t* reject;       // [V] 1 = special or empty (never accepted)
+  const int4* tokrec;          // [2V]: (reject, len, byte offset, 0), 16 inline bytes
 };
+
+// 32-byte token record: first int4 (id or flags, len, offset, 0), second int4
+// the first 16 bytes inline.  Used for vocabulary tokens (accept) and
+// dependent entries (fill).
+constexpr int kInlineBytes = 16;
+__device__ __forceinline__ uint8_t rec_byte(const int4& inl, const uint8_t* far, int i) {
+  if (i < kInlineBytes) {
+    const int w = (i < 4) ? inl.x : (i < 8) ? inl.y : (i < 12) ? inl.z : inl.w;
+    return (uint8_t)((uint32_t)w >> ((i & 3) * 8));
+  }
+  return __ldg(far + i);
+}
 
 struct DevCache {
   const uint32_t* acc_rows;    // [n_keys*W]
   const int32_t* dep_off;      // [n_keys+1]
   const int32_t* dep_ids;
-  const int4* dep_ent;         // [n_dep]: (token id, byte offset, length, 0)
+  const int4* dep_ent;         // [2*n_dep] records (tid, len, offset, 0) + inline bytes
   const uint8_t* dep_bytes;    // dependent tokens' bytes, contiguous
+  const uint8_t* blob;         // binding blob (tables + node_info)
+  int32_t blob_bytes;
 };
 
 // Everything a matcher slot needs, resident in device memory.
@@ -128,28 +201,31 @@ __device__ __forceinline__ int32_t key_parent(unsigned long long k) { return (in
 __device__ __forceinline__ int32_t key_node(unsigned long long k) { return (int32_t)((uint32_t)k >> 1); }
 __device__ __forceinline__ uint32_t key_term(unsigned long long k) { return (uint32_t)k & 1u; }
 
-// Returns the handle of (parent, node), inserting it if absent; -1 + error
-// bit when the table is full.
-__device__ inline int32_t arena_intern(const DevArena& A, int32_t parent, int32_t node, uint32_t term) {
-  const unsigned long long key = arena_key(parent, node, term);
-  uint32_t i = mix64(key) & A.mask;
+// Handle of `key`, inserting it if absent, probing linearly from `start`;
+// -1 + error bit when the table is full.
+__device__ inline int32_t arena_probe(const DevArena& A, unsigned long long key, uint32_t start) {
+  uint32_t i = start & A.mask;
   for (int probe = 0; probe < 8192; ++probe) {
-    unsigned long long cur = arena_load(A, (int32_t)i);
-    if (cur == key) return (int32_t)i;
-    if (cur == kEmptyKey) {
-      cur = atomicCAS(A.keys + i, kEmptyKey, key);
-      if (cur == kEmptyKey || cur == key) return (int32_t)i;
-    }
+    const unsigned long long cur = atomicCAS(A.keys + i, kEmptyKey, key);
+    if (cur == kEmptyKey || cur == key) return (int32_t)i;
     i = (i + 1) & A.mask;
   }
   atomicOr(A.err, kErrArena);
   return -1;
 }
+__device__ inline int32_t arena_intern(const DevArena& A, int32_t parent, int32_t node, uint32_t term) {
+  const unsigned long long key = arena_key(parent, node, term);
+  return arena_probe(A, key, mix64(key));
+}
 
 // ---------------------------------------------------------------------------
-// Walker: a set of at most S stacks plus a pool of F walker-local frames.
+// Walker: a set of at most S stacks plus a pool of F walker-local frames and a
+// small cache of arena keys already known to the caller (slot header), so the
+// first pop below a top costs no HBM round trip.
 
-template <int S, int F>
+constexpr int kChain = 16;  // ancestor frames cached in the slot header
+
+template <int S, int F, int K = 24>
 struct Walker {
   int32_t ref[S];
   int32_t node[S];
@@ -159,8 +235,50 @@ struct Walker {
   uint8_t fterm[F];
   int nf;
   uint32_t err;
+  // arena keys this walk already knows: its own cache (frames it loaded or
+  // interned) plus an optional read-only external one (the slot header's
+  // ancestor chain in shared memory)
+  int32_t kh[K];
+  unsigned long long kk[K];
+  int nk;
+  const int32_t* xh;
+  const unsigned long long* xk;
+  int nx;
 
-  __device__ __forceinline__ void reset() { n = 0; nf = 0; err = 0; }
+  __device__ __forceinline__ void reset() { n = 0; nf = 0; err = 0; nk = 0; nx = 0; }
+
+  __device__ __forceinline__ void external(const int32_t* h, const unsigned long long* k, int cnt) {
+    xh = h; xk = k; nx = cnt;
+  }
+
+  __device__ __forceinline__ bool lookup(int32_t h, unsigned long long& key) const {
+    for (int i = 0; i < nk; ++i)
+      if (kh[i] == h) { key = kk[i]; return true; }
+    for (int i = 0; i < nx; ++i)
+      if (xh[i] == h) { key = xk[i]; return true; }
+    return false;
+  }
+
+  __device__ __forceinline__ void know(int32_t h, unsigned long long key) {
+    if (h < 0 || key == kEmptyKey || nk == K) return;
+    for (int i = 0; i < nk; ++i)
+      if (kh[i] == h) return;
+    kh[nk] = h; kk[nk] = key; ++nk;
+  }
+
+  __device__ __forceinline__ unsigned long long key_of(const DevArena& A, int32_t h) {
+    unsigned long long k;
+    if (lookup(h, k)) {
+#ifdef GM_VERIFY_KNOWN
+      if (arena_load(A, h) != k) err |= 1u << 30;
+#endif
+      return k;
+    }
+    k = arena_load(A, h);
+    if (k == kEmptyKey) err |= kErrInvalid;  // dangling handle: report, never walk garbage
+    else know(h, k);
+    return k;
+  }
 
   __device__ __forceinline__ bool add(int32_t r, int32_t d) {
     for (int q = 0; q < n; ++q)
@@ -170,15 +288,16 @@ struct Walker {
     return true;
   }
 
-  __device__ __forceinline__ uint32_t term_of(const DevArena& A, int32_t r) const {
+  __device__ __forceinline__ uint32_t term_of(const DevArena& A, int32_t r) {
     if (r == -1) return 1u;
     if (r >= 0) return fterm[r];
-    return key_term(arena_load(A, -2 - r));
+    return key_term(key_of(A, -2 - r));
   }
 
-  __device__ __forceinline__ void pop(const DevArena& A, int32_t r, int32_t& pr, int32_t& pn) const {
+  __device__ __forceinline__ void pop(const DevArena& A, int32_t r, int32_t& pr, int32_t& pn) {
     if (r >= 0) { pr = fpar[r]; pn = fnode[r]; return; }
-    const unsigned long long k = arena_load(A, -2 - r);
+    const unsigned long long k = key_of(A, -2 - r);
+    if (k == kEmptyKey) { pr = -1; pn = 0; return; }  // reported by key_of
     const int32_t p = key_parent(k);
     pr = p < 0 ? -1 : -2 - p;
     pn = key_node(k);
@@ -195,18 +314,25 @@ struct Walker {
 
   // Can stack (r, m) silently reach an empty chain at a root final?
   // (REF matcher.py:219-237 _closed_facts.term)
-  __device__ __forceinline__ bool terminable(const DevGrammar& G, const DevArena& A, int32_t r, int32_t m) const {
+  __device__ __forceinline__ bool terminable(const DevGrammar& G, const DevArena& A, int32_t r, int32_t m) {
     return (G.node_flags[m] & GM_NODE_POP) && term_of(A, r);
   }
 
   // One byte step of the whole set.  Sets *pop_bottom when some stack would
   // pop past an empty chain (REF cache.py:128-131 "popped" in synthetic
   // mode; at a real root this is the completed root and simply dies).
+  // Table reads are plain (generic) loads: the tables may live in shared
+  // memory.
   template <int SN>
   __device__ int step(const DevGrammar& G, const DevArena& A, uint32_t b, bool* pop_bottom) {
+    const int c = G.byte_class[b];
+    if (n == 1) {  // single stack: plain DFA moves need one table read
+      const int32_t f = G.fast[node[0] * G.n_classes + c];
+      if (f >= 0) { node[0] = f; return 1; }
+      if (f == -1) { n = 0; return 0; }
+    }
     int32_t nr[SN], nn[SN];
     int cnt = 0;
-    const int c = G.byte_class[b];
     for (int s = 0; s < n; ++s) {
       int32_t r = ref[s], m = node[s];
       while (true) {
@@ -224,6 +350,7 @@ struct Walker {
               int32_t pr, pn;
               pop(A, rr, pr, pn);
               rr = pr; d = pn;
+              if ((uint32_t)d >= (uint32_t)G.n_nodes) { err |= 1u << 29; d = 0; rr = -1; }
             }
           }
           bool dup = false;
@@ -237,6 +364,7 @@ struct Walker {
         if (!(G.node_flags[m] & GM_NODE_POP)) break;
         if (r == -1) { *pop_bottom = true; break; }
         pop(A, r, r, m);
+        if ((uint32_t)m >= (uint32_t)G.n_nodes) { err |= 1u << 28; break; }
       }
     }
     for (int q = 0; q < cnt; ++q) { ref[q] = nr[q]; node[q] = nn[q]; }
@@ -244,9 +372,16 @@ struct Walker {
     return cnt;
   }
 
-  // Move every live stack's local frames into the arena (parents first) and
-  // re-dedupe; afterwards all refs are -1 or arena refs.  Returns false on
-  // arena exhaustion.
+  // Move every live stack's local frames into the arena and re-dedupe;
+  // afterwards all refs are -1 or arena refs.  Speculative parallel
+  // interning: each frame's handle is first assumed to be its key's home slot
+  // (which also fixes its children's keys), so all CASes are independent and
+  // in flight together (one HBM round trip instead of one per frame); a frame
+  // whose home slot holds another key — and every frame after it — is redone
+  // with sequential probing.  Entries written under a wrong speculative
+  // parent are still valid frames (content-addressed), just unreferenced.
+  // The arena keys of the live tops are remembered (know()).  Returns false
+  // on arena exhaustion.
   __device__ bool intern_all(const DevArena& A) {
     if (nf == 0) return true;
     int32_t gmap[F];
@@ -255,14 +390,38 @@ struct Walker {
       int32_t r = ref[s];
       while (r >= 0 && gmap[r] == 0) { gmap[r] = 1; r = fpar[r]; }
     }
+    unsigned long long keyq[F];
+    unsigned long long old[F];
     for (int q = 0; q < nf; ++q) {  // frames are allocated parent-first
       if (!gmap[q]) { gmap[q] = -1; continue; }
-      int32_t p = fpar[q];
-      int32_t ph = p == -1 ? -1 : (p >= 0 ? gmap[p] : -2 - p);  // parent handle
-      int32_t h = arena_intern(A, ph, fnode[q], fterm[q]);
+      const int32_t p = fpar[q];
+      const int32_t ph = p == -1 ? -1 : (p >= 0 ? gmap[p] : -2 - p);
+      keyq[q] = arena_key(ph, fnode[q], fterm[q]);
+      gmap[q] = (int32_t)(mix64(keyq[q]) & A.mask);
+      old[q] = atomicCAS(A.keys + gmap[q], kEmptyKey, keyq[q]);
+    }
+    bool redo = false;
+    for (int q = 0; q < nf; ++q) {
+      if (gmap[q] < 0) continue;
+      if (!redo && (old[q] == kEmptyKey || old[q] == keyq[q])) continue;
+      redo = true;  // this frame and everything after: sequential probing
+      const int32_t p = fpar[q];
+      const int32_t ph = p == -1 ? -1 : (p >= 0 ? gmap[p] : -2 - p);
+      keyq[q] = arena_key(ph, fnode[q], fterm[q]);
+      const int32_t h = arena_probe(A, keyq[q], mix64(keyq[q]));
       if (h < 0) { err |= kErrArena; return false; }
       gmap[q] = h;
     }
+    // known-key cache := the first stack's new frames in chain order (its own
+    // frame first, then its interned ancestors); older entries are dropped —
+    // the header's ancestor chain stays reachable through external()
+    nk = 0;
+    if (n > 0)
+      for (int32_t r = ref[0]; r >= 0 && nk < K; r = fpar[r]) {
+        kh[nk] = gmap[r];
+        kk[nk] = keyq[r];
+        ++nk;
+      }
     int m = n;
     n = 0;
     int32_t or_[S], on_[S];
@@ -277,6 +436,238 @@ struct Walker {
   }
 };
 
+// ---------------------------------------------------------------------------
+// RWalker: the common-case walker.  At most R stacks, held in registers (every
+// array index below is a compile-time constant after unrolling), so a byte
+// step is a handful of shared-memory table reads instead of a chain of
+// local-memory round trips.  Chain references add a fourth kind,
+//     ref >= kChainRef     position i = ref - kChainRef of the slot header's
+//                          ancestor chain (xh/xk, shared memory),
+// so popping through the cached chain is an index increment.  Pushes use
+// walker-local frames (local memory, touched only when a rule is entered).
+// Any overflow (more than R stacks, more than F frames) sets `spill`; the
+// caller then redoes the walk with the general Walker.
+constexpr int32_t kChainRef = 1 << 30;
+
+template <int R, int F>
+struct RWalker {
+  int32_t ref[R];
+  int32_t node[R];
+  int n;
+  int32_t fpar[F];
+  int32_t fnode[F];
+  uint8_t fterm[F];
+  int nf;
+  bool spill;
+  uint32_t err;
+  const int32_t* xh;
+  const unsigned long long* xk;
+  int nx;
+
+  __device__ __forceinline__ void init(const int32_t* ch, const unsigned long long* ck, int nc) {
+    n = 0; nf = 0; spill = false; err = 0;
+    xh = ch; xk = ck; nx = nc;
+  }
+
+  // Reference for arena handle h (-1 = empty chain), as a chain position when
+  // h heads the cached chain.
+  __device__ __forceinline__ int32_t ref_of_handle(int32_t h) const {
+    if (h < 0) return -1;
+    if (nx > 0 && xh[0] == h) return kChainRef;
+    return -2 - h;
+  }
+
+  __device__ __forceinline__ unsigned long long global_key(const DevArena& A, int32_t r) const {
+    if (r >= kChainRef) return xk[r - kChainRef];
+    return arena_load(A, -2 - r);
+  }
+
+  __device__ __forceinline__ void pop(const DevArena& A, int32_t r, int32_t& pr, int32_t& pn) {
+    if (r >= 0 && r < kChainRef) { pr = fpar[r]; pn = fnode[r]; return; }
+    const unsigned long long k = global_key(A, r);
+    if (k == kEmptyKey) { err |= kErrInvalid; pr = -1; pn = 0; return; }
+    pn = key_node(k);
+    if (r >= kChainRef && r - kChainRef + 1 < nx) { pr = r + 1; return; }
+    const int32_t p = key_parent(k);
+    pr = p < 0 ? -1 : -2 - p;
+  }
+
+  __device__ __forceinline__ uint32_t term_of(const DevArena& A, int32_t r) const {
+    if (r == -1) return 1u;
+    if (r >= 0 && r < kChainRef) return fterm[r];
+    return key_term(global_key(A, r));
+  }
+
+  __device__ __forceinline__ int32_t push(const DevGrammar& G, const DevArena& A, int32_t r, int32_t ret) {
+    for (int q = nf - 1; q >= 0; --q)
+      if (fpar[q] == r && fnode[q] == ret) return q;
+    if (nf == F) { spill = true; return r; }
+    fpar[nf] = r; fnode[nf] = ret;
+    fterm[nf] = (uint8_t)(((G.node_flags[ret] & GM_NODE_POP) ? 1u : 0u) & term_of(A, r));
+    return nf++;
+  }
+
+  __device__ __forceinline__ void add(int32_t r, int32_t d) {
+    bool dup = false;
+#pragma unroll
+    for (int q = 0; q < R; ++q) dup |= (q < n && ref[q] == r && node[q] == d);
+    if (dup) return;
+    if (n == R) { spill = true; return; }
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (q == n) { ref[q] = r; node[q] = d; }
+    ++n;
+  }
+
+  // One byte step; same semantics as Walker::step.
+  __device__ __forceinline__ int step(const DevGrammar& G, const DevArena& A, uint32_t b, bool* pop_bottom) {
+    const int c = G.byte_class[b];
+    if (n == 1) {  // plain DFA move
+      const int32_t f = G.fast[node[0] * G.n_classes + c];
+      if (f >= 0) { node[0] = f; return 1; }
+      if (f == -1) { n = 0; return 0; }
+    }
+    int32_t nr[R], nn[R];
+    int cnt = 0;
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      if (s >= n) break;
+      int32_t r = ref[s], m = node[s];
+      while (true) {
+        const int32_t idx = m * G.n_classes + c;
+        const int32_t t0 = G.trans_off[idx], t1 = G.trans_off[idx + 1];
+        for (int32_t t = t0; t < t1; ++t) {
+          const int2 tr = G.trans[t];
+          int32_t d = tr.x;
+          const int plen = (int)((uint32_t)tr.y >> 24);
+          const int poff = tr.y & 0xFFFFFF;
+          int32_t rr = r;
+          for (int k = 0; k < plen; ++k) rr = push(G, A, rr, G.push_pool[poff + k]);
+          if (plen == 0) {
+            while ((G.node_flags[d] & GM_NODE_DEAD_END) && rr != -1) {
+              int32_t pr, pn;
+              pop(A, rr, pr, pn);
+              rr = pr; d = pn;
+              if ((uint32_t)d >= (uint32_t)G.n_nodes) { err |= 1u << 29; d = 0; rr = -1; }
+            }
+          }
+          bool dup = false;
+#pragma unroll
+          for (int q = 0; q < R; ++q) dup |= (q < cnt && nr[q] == rr && nn[q] == d);
+          if (!dup) {
+            if (cnt == R) {
+              spill = true;
+            } else {
+#pragma unroll
+              for (int q = 0; q < R; ++q)
+                if (q == cnt) { nr[q] = rr; nn[q] = d; }
+              ++cnt;
+            }
+          }
+        }
+        if (!(G.node_flags[m] & GM_NODE_POP)) break;
+        if (r == -1) { *pop_bottom = true; break; }
+        pop(A, r, r, m);
+        if ((uint32_t)m >= (uint32_t)G.n_nodes) { err |= 1u << 28; break; }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) { ref[q] = nr[q]; node[q] = nn[q]; }
+    n = cnt;
+    return cnt;
+  }
+
+  // Arena handle of a chain / global reference (not for local frames).
+  __device__ __forceinline__ int32_t handle_of(int32_t r) const {
+    if (r == -1) return -1;
+    if (r >= kChainRef) return xh[r - kChainRef];
+    return -2 - r;
+  }
+};
+
+// Ancestor chain of the first top, ordered from its own frame upward.
+struct Chain {
+  int32_t h[kChain];
+  unsigned long long k[kChain];
+  int n;
+};
+
+// Intern an RWalker's surviving stacks (speculative parallel CAS as in
+// Walker::intern_all), write them as (handle, node) to out[] (deduplicated),
+// and build the first top's ancestor chain: its new frames, then the cached
+// chain of the previous header from the first frame they share.  Returns the
+// number of tops, or -1 on arena exhaustion.
+template <int R, int F>
+__device__ inline int rwalker_commit(RWalker<R, F>& w, const DevArena& A, int2* out, Chain& ch) {
+  int32_t gmap[F];
+  unsigned long long keyq[F], old[F];
+  for (int q = 0; q < w.nf; ++q) gmap[q] = 0;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    if (s >= w.n) break;
+    int32_t r = w.ref[s];
+    while (r >= 0 && r < kChainRef && gmap[r] == 0) { gmap[r] = 1; r = w.fpar[r]; }
+  }
+  auto parent_handle = [&](int32_t p) -> int32_t {
+    if (p == -1) return -1;
+    if (p >= kChainRef) return w.xh[p - kChainRef];
+    if (p >= 0) return gmap[p];
+    return -2 - p;
+  };
+  for (int q = 0; q < w.nf; ++q) {
+    if (!gmap[q]) { gmap[q] = -1; continue; }
+    keyq[q] = arena_key(parent_handle(w.fpar[q]), w.fnode[q], w.fterm[q]);
+    gmap[q] = (int32_t)(mix64(keyq[q]) & A.mask);
+    old[q] = atomicCAS(A.keys + gmap[q], kEmptyKey, keyq[q]);
+  }
+  bool redo = false;
+  for (int q = 0; q < w.nf; ++q) {
+    if (gmap[q] < 0) continue;
+    if (!redo && (old[q] == kEmptyKey || old[q] == keyq[q])) continue;
+    redo = true;
+    keyq[q] = arena_key(parent_handle(w.fpar[q]), w.fnode[q], w.fterm[q]);
+    const int32_t h = arena_probe(A, keyq[q], mix64(keyq[q]));
+    if (h < 0) return -1;
+    gmap[q] = h;
+  }
+  int n = 0;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    if (s >= w.n) break;
+    const int32_t r = w.ref[s];
+    const int32_t h = (r >= 0 && r < kChainRef) ? gmap[r] : w.handle_of(r);
+    bool dup = false;
+    for (int q = 0; q < n; ++q) dup |= (out[q].x == h && out[q].y == w.node[s]);
+    if (!dup) out[n++] = make_int2(h, w.node[s]);
+  }
+  // chain of the first top
+  ch.n = 0;
+  if (w.n > 0) {
+    int32_t r = w.ref[0];
+    while (r >= 0 && r < kChainRef && ch.n < kChain) {
+      ch.h[ch.n] = gmap[r];
+      ch.k[ch.n] = keyq[r];
+      ++ch.n;
+      r = w.fpar[r];
+    }
+    int i = -1;
+    if (r >= kChainRef) {
+      i = r - kChainRef;
+    } else if (r <= -2) {
+      const int32_t h = -2 - r;
+      for (int j = 0; j < w.nx; ++j)
+        if (w.xh[j] == h) { i = j; break; }
+    }
+    if (i >= 0)
+      for (; i < w.nx && ch.n < kChain; ++i) {
+        ch.h[ch.n] = w.xh[i];
+        ch.k[ch.n] = w.xk[i];
+        ++ch.n;
+      }
+  }
+  return n;
+}
+
 // Allowed-continuation check of the context-expansion DFA (REF cache.py:
 // 303-333 FollowFsa.allows): may some legal continuation of rule `rid` start
 // with (or extend) data[0:len)?
@@ -290,8 +681,39 @@ __device__ __forceinline__ bool follow_allows(const DevGrammar& G, int32_t rid, 
   return s != GM_FOLLOW_DEAD;
 }
 
+// ---------------------------------------------------------------------------
 // Matcher pool: ring of (window+1) top sets per slot (REF matcher.py:239-244
-// history, 310-326 rollback).
+// history, 310-326 rollback) plus the slot header.
+
+// Current-state summary of a slot, one 256-byte record written by every state
+// change (reset / accept / rollback / recycle / fork): all a fill or accept
+// needs to start, in one coalesced load.
+constexpr int kHdrTops = 8;
+struct __align__(16) SlotHdr {
+  const uint8_t* blob;         // binding blob (walker tables + node_info)
+  const uint32_t* acc_rows;
+  const uint32_t* universe;
+  const int4* dep_ent;
+  const int4* tokrec;
+  int32_t blob_bytes, V, W, eos;
+  int32_t ntops;               // -1: more than kHdrTops stacks (read the ring)
+  int32_t flags;               // bit0 terminated, bit1 terminable
+  int32_t key[kHdrTops];
+  int32_t dep_lo[kHdrTops];
+  int32_t dep_hi[kHdrTops];
+  int2 top[kHdrTops];
+  // ancestor-chain cache: arena keys of the tops' chain frames (top 0's chain
+  // first), so walks pop through the first kChain frames without touching
+  // the arena
+  int32_t nchain, pad0;
+  int32_t chain_h[kChain];
+  int32_t pad1[2];
+  unsigned long long chain_k[kChain];
+  int32_t pad2[20];
+};
+static_assert(sizeof(SlotHdr) == 512, "SlotHdr layout");
+constexpr int kHdrVec = sizeof(SlotHdr) / 16;  // int4 per header
+
 struct DevPool {
   int32_t capacity, max_stacks, H;
   int2* tops;                 // [capacity][H][max_stacks] (handle, node)
@@ -302,55 +724,113 @@ struct DevPool {
   const DevBinding** binding; // [capacity]
   DevArena arena;
   uint32_t* err;
-  struct SlotHdr* hdr;        // [capacity] current-state summary
+  SlotHdr* hdr;               // [capacity]
+  unsigned long long* trace;  // optional phase timestamps (GMASK_TRACE=1), else null
 };
+
+// Phase timestamps of CTA 0 (diagnostics only): trace[kernel*16 + phase].
+__device__ __forceinline__ void trace_mark(const DevPool& P, int kernel, int phase) {
+  if (P.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.trace[kernel * 16 + phase] = t;
+  }
+}
 
 __device__ __forceinline__ int2* slot_tops(const DevPool& P, int32_t slot, int32_t h) {
   return P.tops + ((size_t)slot * P.H + h) * P.max_stacks;
 }
 
-// Current-state summary of a slot, one 256-byte record written by every
-// state change (reset / accept / rollback / recycle / fork).  The fill kernel
-// reads it with one coalesced load instead of chasing head -> ring entry ->
-// key_of_node -> dep_off (each a cold HBM round trip once the model's forward
-// pass has flushed L2).
-constexpr int kHdrTops = 8;
-struct __align__(16) SlotHdr {
-  const DevBinding* binding;
-  int32_t ntops;               // -1: more than kHdrTops stacks (fill uses the ring)
-  int32_t flags;               // bit0 terminated, bit1 terminable
-  int32_t key[kHdrTops];
-  int32_t dep_lo[kHdrTops];
-  int32_t dep_hi[kHdrTops];
-  int2 top[kHdrTops];
-  int32_t pad[20];
-};
-static_assert(sizeof(SlotHdr) == 256, "SlotHdr layout");
+__device__ __forceinline__ void load_header(const DevPool& P, int32_t slot, SlotHdr* s_hdr) {
+  if (threadIdx.x < kHdrVec)
+    reinterpret_cast<int4*>(s_hdr)[threadIdx.x] = reinterpret_cast<const int4*>(P.hdr + slot)[threadIdx.x];
+}
 
-// Summarise (tops, terminated) of `slot` into its header.
-__device__ inline void write_header(const DevPool& P, int32_t slot, const DevBinding* B, const int2* tops, int n,
-                                    int terminated) {
-  const DevGrammar& G = B->g;
-  SlotHdr h;
-  h.binding = B;
+__device__ __forceinline__ void header_pointers(SlotHdr& h, const DevBinding* B) {
+  h.blob = B->c.blob;
+  h.acc_rows = B->c.acc_rows;
+  h.universe = B->v.universe;
+  h.dep_ent = B->c.dep_ent;
+  h.tokrec = B->v.tokrec;
+  h.blob_bytes = B->c.blob_bytes;
+  h.V = B->v.V;
+  h.W = B->v.W;
+  h.eos = B->v.eos;
+}
+
+// Chain of handle `cur`: first from `fresh` (frames just interned, already in
+// chain order), then by splicing the previous header's chain at the first
+// frame they share — no arena traffic, no quadratic scans.
+__device__ inline void build_chain(Chain& c, int32_t cur, const int32_t* fh, const unsigned long long* fk, int nfresh,
+                                   const SlotHdr& old) {
+  c.n = 0;
+  for (int i = 0; i < nfresh && cur >= 0 && c.n < kChain; ++i) {
+    if (fh[i] != cur) break;
+    c.h[c.n] = cur;
+    c.k[c.n] = fk[i];
+    ++c.n;
+    cur = key_parent(fk[i]);
+  }
+  if (cur < 0) return;
+  int j = 0;
+  while (j < old.nchain && old.chain_h[j] != cur) ++j;
+  for (; j < old.nchain && c.n < kChain; ++j) {
+    c.h[c.n] = old.chain_h[j];
+    c.k[c.n] = old.chain_k[j];
+    ++c.n;
+  }
+}
+
+// Fill the state part of a header from (tops, n, terminated) and the first
+// top's ancestor chain.  `G` must be a binding view (node_info present).
+// Only the EOS fact may need an arena load (a top whose frame is unknown).
+__device__ inline void header_state(const DevPool& P, SlotHdr& h, const DevGrammar& G, const int2* tops, int n,
+                                    int terminated, const Chain* chain) {
   int term = 0;
   for (int s = 0; s < n; ++s) {
     const int2 t = tops[s];
-    if (!terminated && (G.node_flags[t.y] & GM_NODE_POP) &&
-        (t.x < 0 || key_term(arena_load(P.arena, t.x))))
-      term = 1;
+    if (!terminated && !term && (G.node_flags[t.y] & GM_NODE_POP)) {
+      if (t.x < 0) {
+        term = 1;
+      } else {
+        const unsigned long long k = (s == 0 && chain && chain->n && chain->h[0] == t.x)
+                                         ? chain->k[0] : arena_load(P.arena, t.x);
+        term = (int)key_term(k);
+      }
+    }
     if (s < kHdrTops) {
-      const int32_t k = G.key_of_node[t.y];
-      h.key[s] = k;
-      h.dep_lo[s] = k >= 0 ? B->c.dep_off[k] : 0;
-      h.dep_hi[s] = k >= 0 ? B->c.dep_off[k + 1] : 0;
+      const int4 ni = G.node_info[t.y];
+      h.key[s] = ni.x;
+      h.dep_lo[s] = ni.y;
+      h.dep_hi[s] = ni.z;
       h.top[s] = t;
     }
   }
+  const int nc = (chain && n > 0) ? chain->n : 0;
+  for (int i = 0; i < nc; ++i) {
+    h.chain_h[i] = chain->h[i];
+    h.chain_k[i] = chain->k[i];
+  }
+  h.nchain = nc;
   h.ntops = n <= kHdrTops ? n : -1;
   h.flags = (terminated ? 1 : 0) | (term ? 2 : 0);
-  for (int i = 0; i < 20; ++i) h.pad[i] = 0;
-  P.hdr[slot] = h;
+}
+
+__device__ inline void store_header(const DevPool& P, int32_t slot, const SlotHdr& h) {
+  const int4* src = reinterpret_cast<const int4*>(&h);
+  int4* dst = reinterpret_cast<int4*>(P.hdr + slot);
+#pragma unroll
+  for (int i = 0; i < kHdrVec; ++i) dst[i] = src[i];
+}
+
+// Rebuild a slot header from the binding (reset / recycle / rollback path).
+__device__ inline void write_header(const DevPool& P, int32_t slot, const DevBinding* B, const int2* tops, int n,
+                                    int terminated) {
+  SlotHdr h;
+  header_pointers(h, B);
+  const DevGrammar G = blob_view(B->c.blob);
+  header_state(P, h, G, tops, n, terminated, nullptr);
+  store_header(P, slot, h);
 }
 
 }  // namespace gm

@@ -84,8 +84,12 @@ static gm_status err_bits_to_status(uint32_t bits, const char* where) {
   if (bits & kErrArena) return fail(GM_ERR_ARENA_FULL, w + ": device stack arena is full");
   if (bits & kErrTerminated) return fail(GM_ERR_TERMINATED, w + ": matcher is terminated");
   if (bits & (1u << GM_ERR_ROLLBACK)) return fail(GM_ERR_ROLLBACK, w + ": cannot roll back beyond history");
-  if (bits & kErrInvalid) return fail(GM_ERR_INVALID, w + ": token id out of range");
-  return fail(GM_ERR_INVALID, w + ": device error");
+  if ((bits & kErrInvalid) && !(bits & 0xF0000000u)) return fail(GM_ERR_INVALID, w + ": token id out of range");
+  return fail(GM_ERR_INVALID, w + ": device error (flags 0x" + [&] {
+                char b[16];
+                snprintf(b, sizeof b, "%x", bits);
+                return std::string(b);
+              }() + ")");
 }
 
 }  // namespace gm
@@ -105,6 +109,9 @@ struct gm_grammar {
   DevAllocs mem;
   DevGrammar dev;
   std::vector<int32_t> keys;
+  std::vector<uint8_t> blob_host;     // grammar blob (BlobHdr + walker tables)
+  std::vector<int32_t> key_of_node;
+  std::vector<int32_t> node_rule;
 };
 
 struct gm_cache {
@@ -167,8 +174,20 @@ gm_status gm_vocab_create(const uint8_t* bytes, const int64_t* offsets, int32_t 
     if (la != lb) return la < lb;
     return a < b;
   });
+  // 32-byte token records (reject, len, far offset, 0) + 16 inline bytes,
+  // followed by all token bytes; far offset is relative to the buffer start
+  const size_t rec_bytes = (size_t)V * 32;
+  std::vector<uint8_t> recbuf(rec_bytes + (size_t)offsets[V] + 16, 0);
+  for (int32_t t = 0; t < V; ++t) {
+    const int64_t o0 = offsets[t], len = offsets[t + 1] - o0;
+    int32_t hdr4[4] = {reject[t], (int32_t)len, (int32_t)(rec_bytes + o0), 0};
+    std::memcpy(recbuf.data() + (size_t)t * 32, hdr4, 16);
+    std::memcpy(recbuf.data() + (size_t)t * 32 + 16, bytes + o0, (size_t)std::min<int64_t>(len, 16));
+  }
+  if (offsets[V]) std::memcpy(recbuf.data() + rec_bytes, bytes, (size_t)offsets[V]);
   gm_vocab* v = new gm_vocab();
   gm_status st;
+  uint8_t* d_rec;
   uint8_t* d_bytes;
   int32_t *d_off, *d_sorted;
   uint32_t* d_univ;
@@ -177,12 +196,14 @@ gm_status gm_vocab_create(const uint8_t* bytes, const int64_t* offsets, int32_t 
       (st = v->mem.upload(&d_off, off32.data(), off32.size())) ||
       (st = v->mem.upload(&d_sorted, ids.data(), ids.size())) ||
       (st = v->mem.upload(&d_univ, universe.data(), universe.size())) ||
-      (st = v->mem.upload(&d_rej, reject.data(), reject.size()))) {
+      (st = v->mem.upload(&d_rej, reject.data(), reject.size())) ||
+      (st = v->mem.upload(&d_rec, recbuf.data(), recbuf.size()))) {
     v->mem.release();
     delete v;
     return st;
   }
-  v->dev = DevVocab{V, W, (int32_t)ids.size(), eos_id, d_bytes, d_off, d_sorted, d_univ, d_rej};
+  v->dev = DevVocab{V, W, (int32_t)ids.size(), eos_id, d_bytes, d_off, d_sorted, d_univ, d_rej,
+                    reinterpret_cast<const int4*>(d_rec)};
   v->universe_host = std::move(universe);
   v->bytes_host.assign(bytes, bytes + offsets[V]);
   v->off_host.assign(offsets, offsets + V + 1);
@@ -224,7 +245,7 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
   }
   // walker tables in one contiguous 16-byte aligned blob (staged into shared
   // memory by the fill/accept kernels)
-  std::vector<uint8_t> blob;
+  std::vector<uint8_t> blob(sizeof(BlobHdr), 0);
   auto put = [&](const void* src, size_t bytes) {
     size_t off = (blob.size() + 15) & ~size_t(15);
     blob.resize(off + ((bytes + 15) & ~size_t(15)), 0);
@@ -238,7 +259,42 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
   const size_t o_pool = put(t->push_pool, (size_t)t->n_push * 4);
   const size_t o_kon = put(key_of_node.data(), key_of_node.size() * 4);
   const size_t o_rule = put(t->node_rule, (size_t)t->n_nodes * 4);
+  // single-stack fast path: for (node, class) the whole byte step when it is
+  // a plain DFA move (node cannot pop, exactly one transition, no push, the
+  // target is not a spent final): target >= 0; -1 = dies; -2 = general step
+  std::vector<int32_t> fast((size_t)n_idx);
+  for (int32_t u = 0; u < t->n_nodes; ++u)
+    for (int32_t c = 0; c < t->n_classes; ++c) {
+      const int64_t idx = (int64_t)u * t->n_classes + c;
+      const int32_t t0 = t->trans_off[idx], t1 = t->trans_off[idx + 1];
+      int32_t f = -2;
+      if (!(t->node_flags[u] & GM_NODE_POP)) {
+        if (t1 == t0) {
+          f = -1;
+        } else if (t1 - t0 == 1) {
+          const int32_t d = t->trans[2 * t0];
+          const uint32_t plen = (uint32_t)t->trans[2 * t0 + 1] >> 24;
+          if (plen == 0 && !(t->node_flags[d] & GM_NODE_DEAD_END)) f = d;
+        }
+      }
+      fast[(size_t)idx] = f;
+    }
+  const size_t o_fast = put(fast.data(), fast.size() * 4);
   if (blob.size() > (size_t)INT32_MAX) return fail(GM_ERR_INVALID, "automaton tables too large");
+  BlobHdr bh{};
+  bh.bytes = (int32_t)blob.size();
+  bh.n_classes = t->n_classes;
+  bh.n_nodes = t->n_nodes;
+  bh.o_bc = (int32_t)o_bc;
+  bh.o_flags = (int32_t)o_flags;
+  bh.o_toff = (int32_t)o_toff;
+  bh.o_trans = (int32_t)o_trans;
+  bh.o_pool = (int32_t)o_pool;
+  bh.o_kon = (int32_t)o_kon;
+  bh.o_rule = (int32_t)o_rule;
+  bh.o_ninfo = 0;
+  bh.o_fast = (int32_t)o_fast;
+  std::memcpy(blob.data(), &bh, sizeof(bh));
   gm_grammar* g = new gm_grammar();
   gm_status st;
   uint8_t* d_blob;
@@ -268,9 +324,14 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
   G.cache_keys = keys;
   G.follow_start = fstart;
   G.follow_next = fnext;
+  G.node_info = nullptr;
+  G.fast = reinterpret_cast<const int32_t*>(d_blob + o_fast);
   G.blob = d_blob;
   G.blob_bytes = (int32_t)blob.size();
   g->keys.assign(t->cache_keys, t->cache_keys + t->n_keys);
+  g->blob_host = std::move(blob);
+  g->key_of_node = std::move(key_of_node);
+  g->node_rule.assign(t->node_rule, t->node_rule + t->n_nodes);
   *out = g;
   return GM_OK;
 }
@@ -353,22 +414,42 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
   std::vector<int32_t> ids_host((size_t)dep_total);
   if (dep_total) GM_CUDA_TRY(cudaMemcpyAsync(ids_host.data(), dep_ids, dep_total * 4, cudaMemcpyDeviceToHost, s));
   GM_CUDA_TRY(cudaStreamSynchronize(s));
-  std::vector<int4> ent((size_t)dep_total);
-  std::vector<uint8_t> dbytes;
+  // dependent records (tid, len, far offset, 0) + 16 inline bytes, then the
+  // dependent tokens' full bytes; offsets relative to the buffer start
+  const size_t drec = (size_t)dep_total * 32;
+  std::vector<uint8_t> depbuf(drec, 0);
   for (int64_t i = 0; i < dep_total; ++i) {
     const int32_t tid = ids_host[i];
-    const int64_t o0 = v->off_host[tid], o1 = v->off_host[tid + 1];
-    ent[i] = make_int4(tid, (int32_t)dbytes.size(), (int32_t)(o1 - o0), 0);
-    dbytes.insert(dbytes.end(), v->bytes_host.begin() + o0, v->bytes_host.begin() + o1);
+    const int64_t o0 = v->off_host[tid], len = v->off_host[tid + 1] - o0;
+    int32_t hdr4[4] = {tid, (int32_t)len, (int32_t)depbuf.size(), 0};
+    std::memcpy(depbuf.data() + (size_t)i * 32, hdr4, 16);
+    std::memcpy(depbuf.data() + (size_t)i * 32 + 16, v->bytes_host.data() + o0, (size_t)std::min<int64_t>(len, 16));
+    depbuf.insert(depbuf.end(), v->bytes_host.begin() + o0, v->bytes_host.begin() + o0 + len);
   }
-  int4* d_ent;
-  uint8_t* d_dbytes;
-  if ((st = c->mem.upload(&d_ent, ent.data(), ent.size())) ||
-      (st = c->mem.upload(&d_dbytes, dbytes.data(), dbytes.size())))
+  depbuf.resize(depbuf.size() + 16, 0);
+  if (depbuf.size() > (size_t)INT32_MAX) return fail(GM_ERR_INVALID, "too many dependent bytes");
+  // binding blob: grammar blob + node_info (key, dep_lo, dep_hi, rule) per node
+  std::vector<uint8_t> bblob = g->blob_host;
+  const size_t o_ninfo = (bblob.size() + 15) & ~size_t(15);
+  bblob.resize(o_ninfo + (size_t)g->dev.n_nodes * 16, 0);
+  for (int32_t nd = 0; nd < g->dev.n_nodes; ++nd) {
+    const int32_t k = g->key_of_node[nd];
+    int32_t ni[4] = {k, k >= 0 ? off[k] : 0, k >= 0 ? off[k + 1] : 0, g->node_rule[nd]};
+    std::memcpy(bblob.data() + o_ninfo + (size_t)nd * 16, ni, 16);
+  }
+  BlobHdr bh;
+  std::memcpy(&bh, bblob.data(), sizeof(bh));
+  bh.o_ninfo = (int32_t)o_ninfo;
+  bh.bytes = (int32_t)bblob.size();
+  std::memcpy(bblob.data(), &bh, sizeof(bh));
+  uint8_t *d_dep, *d_bblob;
+  if ((st = c->mem.upload(&d_dep, depbuf.data(), depbuf.size())) ||
+      (st = c->mem.upload(&d_bblob, bblob.data(), bblob.size())))
     return st;
   c->host_binding.g = g->dev;
   c->host_binding.v = v->dev;
-  c->host_binding.c = DevCache{acc, dep_off, dep_ids, d_ent, d_dbytes};
+  c->host_binding.c = DevCache{acc, dep_off, dep_ids, reinterpret_cast<const int4*>(d_dep), d_dep + drec, d_bblob,
+                               (int32_t)bblob.size()};
   DevBinding* db;
   if ((st = c->mem.alloc(&db, 1))) return st;
   GM_CUDA_TRY(cudaMemcpyAsync(db, &c->host_binding, sizeof(DevBinding), cudaMemcpyHostToDevice, s));
@@ -441,8 +522,14 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   GM_CUDA_TRY(cudaMemset(hist, 0, sizeof(int32_t) * (size_t)capacity));
   GM_CUDA_TRY(cudaMemset(bind, 0, sizeof(void*) * (size_t)capacity));
   GM_CUDA_TRY(cudaMemset(hdr, 0, sizeof(SlotHdr) * (size_t)capacity));
+  unsigned long long* trace = nullptr;
+  const char* tr = getenv("GMASK_TRACE");
+  if (tr && tr[0] == '1') {
+    if ((st = p->mem.alloc(&trace, 64))) return st;
+    GM_CUDA_TRY(cudaMemset(trace, 0, 64 * 8));
+  }
   p->dev = DevPool{capacity, max_stacks, H,   tops, meta, head, hist, win, bind,
-                   DevArena{keys, acap - 1, err}, err, hdr};
+                   DevArena{keys, acap - 1, err}, err, hdr, trace};
   p->scratch_bytes = sb;
   p->scratch_cap = 1 << 16;
   p->scratch_i32 = scr;
@@ -563,6 +650,13 @@ gm_status gm_pool_materialize(gm_pool* p, int32_t handle, int32_t* out, int32_t 
   std::reverse(chain.begin(), chain.end());
   *depth = (int32_t)chain.size();
   for (int32_t i = 0; i < (int32_t)chain.size() && i < max_out; ++i) out[i] = chain[i];
+  return GM_OK;
+}
+
+gm_status gm_pool_trace(gm_pool* p, uint64_t* out64) {
+  if (!p || !p->dev.trace) return fail(GM_ERR_INVALID, "pool created without GMASK_TRACE=1");
+  GM_CUDA_TRY(cudaDeviceSynchronize());
+  GM_CUDA_TRY(cudaMemcpy(out64, p->dev.trace, 64 * 8, cudaMemcpyDeviceToHost));
   return GM_OK;
 }
 

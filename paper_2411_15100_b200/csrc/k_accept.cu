@@ -1,16 +1,17 @@
 // K4 — batched accept_token / accept_bytes on device-resident stacks, plus
-// the small state kernels (reset, recycle, rollback, probe).
+// the small state kernels (reset, recycle, rollback, probe, fork).
 //
 // Replaces Matcher.accept_token / accept_bytes / _sim_bytes / _rewrite_kernel
-// / _push_history / rollback (REF matcher.py:192-217, 239-326).  One CTA (one
-// warp) advances one request: the warp stages the grammar tables into shared
-// memory with one coalesced copy, then lane 0 walks the request's stack set
-// byte by byte with walker-local frames; survivors are interned into the
-// hash-consed arena (parents first), deduplicated by (handle, node) — which
-// is deduplication by stack content because the arena is hash-consed
-// (REF matcher.py:202-206) — and written as the next entry of the slot's
-// history ring together with the slot header.  A rejected token leaves the
-// slot unchanged (REF matcher.py:267-268).
+// / _push_history / rollback / branch (REF matcher.py:192-217, 239-355).
+// One CTA (one warp) advances one request, with few dependent HBM round
+// trips: slot header (1) -> token record with inline bytes, in parallel with
+// staging the binding blob into shared memory (2) -> lane 0 walks the stack
+// set byte by byte with walker-local frames (first pops served from the
+// header's known arena keys) -> survivors are interned into the hash-consed
+// arena with speculative parallel CAS (3) -> the next history-ring entry and
+// the new header are written.  Dedupe by (handle, node) is dedupe by stack
+// content because the arena is hash-consed (REF matcher.py:202-206).  A
+// rejected token leaves the slot unchanged (REF matcher.py:267-268).
 #include "device.cuh"
 
 namespace gm {
@@ -18,9 +19,11 @@ namespace gm {
 constexpr int kAccS = 32;
 constexpr int kAccF = 160;
 constexpr int kAccThreads = 32;
+constexpr int kAccR = 4;    // stacks held in registers by the fast walker
+constexpr int kAccRF = 48;  // its walker-local frames
 
 // Current (handle, node) set of a slot: from the header when it fits, else
-// from the ring.  Returns the count.
+// from the ring.
 __device__ int load_tops(const DevPool& P, int32_t slot, const SlotHdr& hdr, int2* out) {
   if (hdr.ntops >= 0) {
     for (int s = 0; s < hdr.ntops; ++s) out[s] = hdr.top[s];
@@ -33,48 +36,110 @@ __device__ int load_tops(const DevPool& P, int32_t slot, const SlotHdr& hdr, int
   return n;
 }
 
-__device__ void push_history(const DevPool& P, int32_t slot, const DevBinding* B, int nt, const int32_t* refs,
-                             const int32_t* nodes, int terminated) {
-  const int32_t nh = (P.head[slot] + 1) % P.H;
-  int2* dst = slot_tops(P, slot, nh);
-  for (int s = 0; s < nt; ++s) {
-    const int32_t r = refs[s];
-    dst[s] = make_int2(r == -1 ? -1 : -2 - r, nodes[s]);
-  }
-  P.meta[(size_t)slot * P.H + nh] = nt | (terminated << 16);
-  P.head[slot] = nh;
-  const int32_t hl = P.hist_len[slot] + 1;
-  P.hist_len[slot] = hl < P.window[slot] ? hl : P.window[slot];
-  write_header(P, slot, B, dst, nt, terminated);
+// Append (refs, nodes) as the next ring entry and publish the new header.
+// `hdr` supplies the binding pointers; `topkeys` the arena keys of the tops
+// when known.
+// Ring position of a slot (head, history length, window), prefetched by
+// lanes 1..3 at kernel entry so the append does not wait on them.
+struct RingPos {
+  int32_t head, hist_len, window;
+};
+
+__device__ __forceinline__ void prefetch_ring(const DevPool& P, int32_t slot, RingPos* rp) {
+  if (threadIdx.x == 1) rp->head = P.head[slot];
+  if (threadIdx.x == 2) rp->hist_len = P.hist_len[slot];
+  if (threadIdx.x == 3) rp->window = P.window[slot];
 }
 
-// Shared by token and byte-string acceptance (lane 0 only).  data/len =
-// bytes to consume; is_eos = EOS token.  Returns 1 if accepted.
-__device__ int accept_one(const DevPool& P, int32_t slot, const SlotHdr& hdr, const DevGrammar& G,
-                          const uint8_t* data, int64_t len, bool is_eos, bool reject_token) {
-  const DevBinding* B = hdr.binding;
+// Append (handle, node) tops as the next ring entry and publish the new
+// header state.  The binding pointers of the global header are unchanged, so
+// only its state fields are rewritten in place.
+__device__ void push_tops(const DevPool& P, int32_t slot, const RingPos& rp, const DevGrammar& G, const int2* tops,
+                          int nt, int terminated, const Chain& c) {
+  const int32_t nh = (rp.head + 1) % P.H;
+  int2* dst = slot_tops(P, slot, nh);
+  for (int s = 0; s < nt; ++s) dst[s] = tops[s];
+  P.meta[(size_t)slot * P.H + nh] = nt | (terminated << 16);
+  P.head[slot] = nh;
+  const int32_t hl = rp.hist_len + 1;
+  P.hist_len[slot] = hl < rp.window ? hl : rp.window;
+  header_state(P, P.hdr[slot], G, tops, nt, terminated, &c);
+}
+
+__device__ void push_history(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr,
+                             const DevGrammar& G, int nt, const int32_t* refs, const int32_t* nodes, int terminated,
+                             const int32_t* fh, const unsigned long long* fk, int nfresh) {
+  int2 loc[kAccS];
+  for (int s = 0; s < nt; ++s) {
+    const int32_t r = refs[s];
+    loc[s] = make_int2(r == -1 ? -1 : -2 - r, nodes[s]);
+  }
+  Chain c;
+  build_chain(c, nt > 0 ? loc[0].x : -1, fh, fk, nfresh, hdr);
+  push_tops(P, slot, rp, G, loc, nt, terminated, c);
+}
+
+// Shared by token and byte-string acceptance (lane 0 only).  byte(i) gives
+// the i-th input byte; is_eos = EOS token.  Returns 1 if accepted.
+template <class ByteFn>
+__device__ int accept_one(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr, const DevGrammar& G,
+                          int64_t len, ByteFn byte, bool is_eos, bool reject_token) {
   if (hdr.flags & 1) {  // REF matcher.py:276-277 "matcher is terminated"
     atomicOr(P.err, kErrTerminated);
     return 0;
   }
   int2 tops[kAccS];
   const int ntops = load_tops(P, slot, hdr, tops);
-  Walker<kAccS, kAccF> w;
-  w.reset();
-  for (int s = 0; s < ntops; ++s) w.add(tops[s].x < 0 ? -1 : -2 - tops[s].x, tops[s].y);
   if (is_eos) {  // REF matcher.py:280-288
     if (!(hdr.flags & 2)) return 0;
-    push_history(P, slot, B, w.n, w.ref, w.node, 1);
+    Chain c;
+    build_chain(c, ntops > 0 ? tops[0].x : -1, nullptr, nullptr, 0, hdr);
+    push_tops(P, slot, rp, G, tops, ntops, 1, c);
     return 1;
   }
   if (reject_token) return 0;  // special or empty token (REF matcher.py:289-293)
+  // fast path: register walker (<= kAccR stacks)
+  if (ntops <= kAccR) {
+    RWalker<kAccR, kAccRF> rw;
+    rw.init(hdr.chain_h, hdr.chain_k, hdr.nchain);
+    for (int s = 0; s < ntops; ++s) rw.add(rw.ref_of_handle(tops[s].x), tops[s].y);
+    for (int64_t i = 0; i < len && rw.n > 0 && !rw.spill; ++i) {
+      bool pb = false;
+      rw.step(G, P.arena, byte(i), &pb);
+    }
+    trace_mark(P, 0, 3);
+    if (!rw.spill) {
+      if (rw.err) {
+        atomicOr(P.err, rw.err);
+        return 0;
+      }
+      if (rw.n == 0) return 0;
+      int2 out[kAccR];
+      Chain c;
+      const int nout = rwalker_commit(rw, P.arena, out, c);
+      if (nout < 0) {
+        atomicOr(P.err, kErrArena);
+        return 0;
+      }
+      trace_mark(P, 0, 4);
+      push_tops(P, slot, rp, G, out, nout, 0, c);
+      trace_mark(P, 0, 5);
+      return 1;
+    }
+  }
+  // general path: any number of stacks / frames
+  Walker<kAccS, kAccF> w;
+  w.reset();
+  w.external(hdr.chain_h, hdr.chain_k, hdr.nchain);
+  for (int s = 0; s < ntops; ++s) w.add(tops[s].x < 0 ? -1 : -2 - tops[s].x, tops[s].y);
   for (int64_t i = 0; i < len; ++i) {
     if (w.nf > kAccF / 2) {
       if (!w.intern_all(P.arena)) break;
     }
     bool pb = false;
-    if (!w.template step<kAccS>(G, P.arena, __ldg(data + i), &pb)) break;
+    if (!w.template step<kAccS>(G, P.arena, byte(i), &pb)) break;
   }
+  trace_mark(P, 0, 3);
   if (w.err) {
     atomicOr(P.err, w.err);
     return 0;
@@ -84,56 +149,59 @@ __device__ int accept_one(const DevPool& P, int32_t slot, const SlotHdr& hdr, co
     atomicOr(P.err, w.err | kErrArena);
     return 0;
   }
+  trace_mark(P, 0, 4);
   if (w.n > P.max_stacks) {
     atomicOr(P.err, kErrCap);
     return 0;
   }
-  push_history(P, slot, B, w.n, w.ref, w.node, 0);
+  push_history(P, slot, rp, hdr, G, w.n, w.ref, w.node, 0, w.kh, w.kk, w.nk);
+  trace_mark(P, 0, 5);
   return 1;
-}
-
-__device__ __forceinline__ void load_header(const DevPool& P, int32_t slot, SlotHdr* s_hdr) {
-  if (threadIdx.x < 16)
-    reinterpret_cast<int4*>(s_hdr)[threadIdx.x] = reinterpret_cast<const int4*>(P.hdr + slot)[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(kAccThreads)
 accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t* __restrict__ token_ids, int32_t n,
                      uint8_t* __restrict__ accepted) {
   extern __shared__ __align__(16) uint8_t tables[];
-  __shared__ SlotHdr s_hdr;
+  __shared__ SlotHdr hd;
+  __shared__ int4 s_rec[2];
+  __shared__ RingPos rp;
   const int32_t i = blockIdx.x;
   if (i >= n) return;
+  trace_mark(P, 0, 0);
   const int32_t slot = __ldg(slots + i);
   const int32_t tid = __ldg(token_ids + i);
-  load_header(P, slot, &s_hdr);
+  load_header(P, slot, &hd);
+  prefetch_ring(P, slot, &rp);
   __syncthreads();
-  const DevBinding* B = s_hdr.binding;
-  const DevGrammar G = stage_grammar(B->g, tables);
-  __syncthreads();
+  trace_mark(P, 0, 1);
+  const bool in_range = tid >= 0 && tid < hd.V;
+  if (threadIdx.x < 2 && in_range) s_rec[threadIdx.x] = __ldg(hd.tokrec + 2 * (size_t)tid + threadIdx.x);
+  const DevGrammar G = stage_blob(hd.blob, hd.blob_bytes, tables);  // barrier inside
+  trace_mark(P, 0, 2);
   if (threadIdx.x != 0) return;
-  const DevVocab& Vc = B->v;
-  if (tid < 0 || tid >= Vc.V) {  // REF matcher.py:278-279
+  if (!in_range) {  // REF matcher.py:278-279
     atomicOr(P.err, kErrInvalid);
     accepted[i] = 0;
     return;
   }
-  const int32_t o0 = __ldg(Vc.off + tid);
-  const int64_t len = __ldg(Vc.off + tid + 1) - o0;
-  accepted[i] = (uint8_t)accept_one(P, slot, s_hdr, G, Vc.bytes + o0, len, tid == Vc.eos, Vc.reject[tid] != 0);
+  const int4 e = s_rec[0], inl = s_rec[1];
+  const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;
+  accepted[i] = (uint8_t)accept_one(P, slot, rp, hd, G, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
+                                    tid == hd.eos, e.x != 0);
 }
 
 __global__ void __launch_bounds__(kAccThreads)
 accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len, uint8_t* accepted) {
   extern __shared__ __align__(16) uint8_t tables[];
-  __shared__ SlotHdr s_hdr;
-  load_header(P, slot, &s_hdr);
+  __shared__ SlotHdr hd;
+  __shared__ RingPos rp;
+  load_header(P, slot, &hd);
+  prefetch_ring(P, slot, &rp);
   __syncthreads();
-  const DevBinding* B = s_hdr.binding;
-  const DevGrammar G = stage_grammar(B->g, tables);
-  __syncthreads();
+  const DevGrammar G = stage_blob(hd.blob, hd.blob_bytes, tables);
   if (threadIdx.x != 0) return;
-  if (s_hdr.flags & 1) {
+  if (hd.flags & 1) {
     atomicOr(P.err, kErrTerminated);
     *accepted = 0;
     return;
@@ -141,16 +209,16 @@ accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len, u
   if (len == 0) {  // REF matcher.py:253-258: empty input records a history entry
     int2 tops[kAccS];
     int32_t refs[kAccS], nodes[kAccS];
-    const int nt = load_tops(P, slot, s_hdr, tops);
+    const int nt = load_tops(P, slot, hd, tops);
     for (int s = 0; s < nt; ++s) {
       refs[s] = tops[s].x < 0 ? -1 : -2 - tops[s].x;
       nodes[s] = tops[s].y;
     }
-    push_history(P, slot, B, nt, refs, nodes, 0);
+    push_history(P, slot, rp, hd, G, nt, refs, nodes, 0, nullptr, nullptr, 0);
     *accepted = 1;
     return;
   }
-  *accepted = (uint8_t)accept_one(P, slot, s_hdr, G, data, len, false, false);
+  *accepted = (uint8_t)accept_one(P, slot, rp, hd, G, len, [&](int64_t b) { return __ldg(data + b); }, false, false);
 }
 
 __global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32_t start, int32_t window) {
@@ -205,7 +273,7 @@ __global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots, co
 __global__ void slot_probe_kernel(DevPool P, int32_t slot, int32_t* info, int2* stacks, int32_t max_out,
                                   uint32_t* bytes8) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const DevGrammar& G = P.binding[slot]->g;
+  const DevGrammar G = blob_view(P.binding[slot]->c.blob);
   const int32_t h = P.head[slot];
   const int32_t meta = P.meta[(size_t)slot * P.H + h];
   const int nt = meta & 0xFFFF;
@@ -240,7 +308,7 @@ __global__ void fork_kernel(DevPool P, int32_t src, int32_t dst) {
   const size_t per = (size_t)P.H * P.max_stacks;
   for (size_t k = threadIdx.x; k < per; k += blockDim.x) P.tops[dst * per + k] = P.tops[src * per + k];
   for (int k = threadIdx.x; k < P.H; k += blockDim.x) P.meta[(size_t)dst * P.H + k] = P.meta[(size_t)src * P.H + k];
-  if (threadIdx.x < 16)
+  if (threadIdx.x < kHdrVec)
     reinterpret_cast<int4*>(P.hdr + dst)[threadIdx.x] = reinterpret_cast<const int4*>(P.hdr + src)[threadIdx.x];
   if (threadIdx.x == 0) {
     P.head[dst] = P.head[src];
@@ -252,6 +320,9 @@ __global__ void fork_kernel(DevPool P, int32_t src, int32_t dst) {
 
 static gm_status set_smem_attr(const void* fn) {
   GM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytes));
+  // keep most of the unified L1/shared array as L1: the walker's per-thread
+  // state lives in local memory and must hit L1, not L2
+  GM_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
   return GM_OK;
 }
 

@@ -13,8 +13,8 @@
 // (shared) mask word, fully masked chunks are one 128-bit store of -inf, and
 // mixed chunks store only their masked elements — logits are never read, so
 // per row the traffic is the algorithmic minimum 4*ceil(V/32) + s*M
-// (M = masked tokens).  Several tiles per warp are loaded before any store
-// (ILP) and the grid is sized to the 148 SMs.
+// (M = masked tokens).  The grid is 2-D (tile blocks x rows) so no index
+// division is needed; mixed chunks loop only over their masked elements.
 #include "common.cuh"
 
 namespace gm {
@@ -25,73 +25,50 @@ __device__ __forceinline__ void st_v4(void* p, uint32_t v) {
 }
 
 constexpr int kTileTok = 1024;  // tokens per warp tile (32 words)
-constexpr int kUnroll = 4;      // tiles in flight per warp
+constexpr int kApplyWarps = 4;  // warps (tiles) per CTA
 
-// EB = bytes per element.
+// EB = bytes per element.  grid = (ceil(tiles_per_row / kApplyWarps), rows).
 template <int EB>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32 * kApplyWarps)
 apply_tile_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab, int64_t lstride_bytes,
                   const int32_t* __restrict__ bitmask, int64_t bstride, const int32_t* __restrict__ indices,
-                  uint32_t neg, int64_t tiles_per_row) {
+                  uint32_t neg) {
   constexpr int VEC = 16 / EB;                 // tokens per 16-byte chunk
-  constexpr int CHUNKS = kTileTok / VEC;       // chunks per tile
-  constexpr int ROUNDS = CHUNKS / 32;          // store rounds per tile
+  constexpr int ROUNDS = kTileTok / VEC / 32;  // store rounds per tile
   constexpr int CPW = 32 / VEC;                // chunks per mask word
   constexpr uint32_t FULL = (1u << VEC) - 1u;
   const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t total = n_rows * tiles_per_row;
+  const int64_t tile = (int64_t)blockIdx.x * kApplyWarps + (threadIdx.x >> 5);
   const int64_t words_row = (vocab + 31) >> 5;
-
-  for (int64_t base = warp * kUnroll; base < total; base += n_warps * kUnroll) {
-    uint32_t w[kUnroll];
+  if (tile * 32 >= words_row) return;
+  const int64_t word = tile * 32 + lane;
+  for (int64_t i = blockIdx.y; i < n_rows; i += gridDim.y) {
+    const int64_t row = indices ? (int64_t)__ldg(indices + i) : i;
+    const uint32_t w = word < words_row ? (uint32_t)__ldg(bitmask + row * bstride + word) : 0xFFFFFFFFu;
+    if (__all_sync(0xFFFFFFFFu, w == 0xFFFFFFFFu)) continue;  // whole tile allowed
+    char* tp = logits + row * lstride_bytes + tile * kTileTok * EB;
+    const int64_t tok_base = tile * kTileTok;
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t tile = base + u;
-      w[u] = 0xFFFFFFFFu;
-      if (tile < total) {
-        const int64_t i = tile / tiles_per_row;
-        const int64_t t = tile - i * tiles_per_row;
-        const int64_t row = indices ? (int64_t)__ldg(indices + i) : i;
-        const int64_t word = t * 32 + lane;
-        if (word < words_row) w[u] = (uint32_t)__ldg(bitmask + row * bstride + word);
+    for (int r = 0; r < ROUNDS; ++r) {
+      const int c = r * 32 + lane;  // chunk within the tile
+      const uint32_t cw = __shfl_sync(0xFFFFFFFFu, w, c / CPW);
+      uint32_t keep = (cw >> ((c % CPW) * VEC)) & FULL;
+      const int64_t tok0 = tok_base + (int64_t)c * VEC;
+      if (tok0 + VEC > vocab) {  // ragged tail: tokens >= vocab untouched
+        const int64_t nvalid = vocab - tok0;
+        keep |= nvalid <= 0 ? FULL : (FULL & ~((1u << nvalid) - 1u));
       }
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t tile = base + u;
-      if (tile >= total) break;
-      if (__all_sync(0xFFFFFFFFu, w[u] == 0xFFFFFFFFu)) continue;  // whole tile allowed
-      const int64_t i = tile / tiles_per_row;
-      const int64_t t = tile - i * tiles_per_row;
-      const int64_t row = indices ? (int64_t)__ldg(indices + i) : i;
-      char* rowp = logits + row * lstride_bytes;
-      const int64_t tok_base = t * kTileTok;
-#pragma unroll
-      for (int r = 0; r < ROUNDS; ++r) {
-        const int c = r * 32 + lane;  // chunk within the tile
-        const uint32_t word = __shfl_sync(0xFFFFFFFFu, w[u], c / CPW);
-        uint32_t bits = (word >> ((c % CPW) * VEC)) & FULL;
-        const int64_t tok0 = tok_base + (int64_t)c * VEC;
-        if (tok0 >= vocab) continue;
-        int nvalid = VEC;
-        if (tok0 + VEC > vocab) {
-          nvalid = (int)(vocab - tok0);
-          bits |= FULL & ~((1u << nvalid) - 1u);
-        }
-        if (bits == FULL) continue;
-        char* p = rowp + tok0 * EB;
-        if (bits == 0) {
-          st_v4(p, neg);
-        } else {
-#pragma unroll
-          for (int j = 0; j < VEC; ++j) {
-            if (!((bits >> j) & 1u)) {
-              if (EB == 4) *reinterpret_cast<uint32_t*>(p + j * 4) = neg;
-              else *reinterpret_cast<uint16_t*>(p + j * 2) = (uint16_t)neg;
-            }
-          }
+      if (keep == FULL) continue;
+      char* p = tp + c * 16;
+      if (keep == 0) {
+        st_v4(p, neg);
+      } else {  // mixed chunk: store only the masked elements, never read logits
+        uint32_t m = ~keep & FULL;
+        while (m) {
+          const int j = __ffs(m) - 1;
+          m &= m - 1;
+          if (EB == 4) *reinterpret_cast<uint32_t*>(p + j * 4) = neg;
+          else *reinterpret_cast<uint16_t*>(p + j * 2) = (uint16_t)neg;
         }
       }
     }
@@ -142,17 +119,14 @@ extern "C" gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_row
   char* lp = static_cast<char*>(logits);
   if (aligned) {
     const int64_t tiles_per_row = ceil_div(vocab_size, kTileTok);
-    const int64_t warps = ceil_div(n_rows * tiles_per_row, kUnroll);
-    const int threads = 256;
-    int64_t blocks = ceil_div(warps * 32, threads);
-    const int64_t cap = (int64_t)kNumSMs * 8;  // 8 x 256 threads resident per SM
-    if (blocks > cap) blocks = cap;
+    dim3 grid((unsigned)ceil_div(tiles_per_row, kApplyWarps), (unsigned)(n_rows < 65535 ? n_rows : 65535));
+    const int threads = 32 * kApplyWarps;
     if (eb == 4)
-      apply_tile_kernel<4><<<(unsigned)blocks, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask,
-                                                               bitmask_stride, indices, neg, tiles_per_row);
+      apply_tile_kernel<4><<<grid, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask, bitmask_stride,
+                                                    indices, neg);
     else
-      apply_tile_kernel<2><<<(unsigned)blocks, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask,
-                                                               bitmask_stride, indices, neg, tiles_per_row);
+      apply_tile_kernel<2><<<grid, threads, 0, s>>>(lp, n_rows, vocab_size, lstride_bytes, bitmask, bitmask_stride,
+                                                    indices, neg);
   } else {
     int64_t gx = ceil_div(vocab_size, 256);
     if (gx > 65535) gx = 65535;

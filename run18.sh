@@ -1,0 +1,8 @@
+export GMASK_NO_BUILD=1
+python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+GMASK_TRACE=1 python tools/trace_step.py 2>&1 | tail -8
+python bench.py --steps 200 --warmup 5 --no-cpu-baseline > gpurun_out/bench18.json 2>gpurun_out/bench18.err
+python - <<'PY'
+import json; d=json.load(open('gpurun_out/bench18.json'))
+for k in ['value','fill_us','apply_us','accept_us','compile_ms','e2e']: print(k, d.get(k))
+PY

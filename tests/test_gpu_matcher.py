@@ -1,0 +1,301 @@
+"""Matcher behaviour KATs on the GPU through the grammask-compatible API.
+
+Each test restates a reference test (REF tests/test_matcher.py, cited per
+test) and checks the device engine against the reference's expected values,
+the CPU oracle, or the oracle's language-level brute force."""
+
+import random
+
+import numpy as np
+import pytest
+
+from oracle import brute_force_mask, compile_oracle_bundle
+from oracle.matcher import OracleMatcher
+from paper_2411_15100_b200.vocab import vocab_from_tokens
+from workloads import grammar_text, vocab_by_name
+
+pytestmark = pytest.mark.gpu
+
+ARRAY_STRING = None
+
+
+def make_vocab(tokens, specials=("<eos>",)):
+    toks = [bytes(t) if not isinstance(t, str) else t.encode() for t in tokens]
+    toks += [s.encode() for s in specials]
+    n = len(toks)
+    return vocab_from_tokens(toks, eos_id=n - 1, special=list(range(n - len(specials), n)))
+
+
+@pytest.fixture(scope="module")
+def fig2():
+    from paper_2411_15100_b200.compat import compile_bundle
+
+    vocab = make_vocab([bytes([b]) for b in b'[]",abx\\'] + [b"ab", b'"]', b'",', b'a"', b'""', b"]]", b"],", b'["'])
+    text = grammar_text("array_string")
+    return compile_bundle(text, vocab), vocab, text
+
+
+def test_mask_wire_format():  # REF test_matcher.py:31-44
+    from paper_2411_15100_b200.compat import TokenMask
+
+    m = TokenMask(70)
+    for t in (0, 33, 69):
+        m.set_bit(t)
+    raw = m.to_bytes()
+    assert len(raw) == 12 and raw[0] == 0x01 and raw[4] == 0x02
+    assert TokenMask.from_bytes(70, raw) == m
+    assert list(m.allowed_ids()) == [0, 33, 69] and m.count() == 3
+
+
+def test_vocab_hash_mismatch(fig2):  # REF test_matcher.py:58-62
+    from paper_2411_15100_b200.compat import Matcher, MatcherError
+
+    bundle, _, _ = fig2
+    with pytest.raises(MatcherError, match="does not match"):
+        Matcher(bundle, make_vocab([b"a", b"b"]))
+
+
+def test_mask_equals_brute_force_and_accept_consistency(fig2):  # REF test_matcher.py:65-88
+    from paper_2411_15100_b200.compat import Matcher
+
+    bundle, vocab, text = fig2
+    ob = compile_oracle_bundle(text, vocab)
+    rng = random.Random(11)
+    for _ in range(12):
+        m = Matcher(bundle, vocab, history_window=64)
+        consumed = b""
+        for _ in range(rng.randrange(0, 8)):
+            mask = m.next_token_mask()
+            assert list(mask.allowed_ids()) == sorted(brute_force_mask(ob.pda, vocab, consumed))
+            for tid in range(vocab.size):
+                probe = m.branch()
+                try:
+                    assert probe.accept_token(tid) == mask.is_allowed(tid), (consumed, tid)
+                finally:
+                    probe.close()
+            ids = mask.allowed_ids()
+            pick = int(ids[rng.randrange(len(ids))])
+            if pick == vocab.eos_id:
+                break
+            assert m.accept_token(pick)
+            consumed += vocab.tokens[pick]
+        m.close()
+
+
+def test_rejection_keeps_state(fig2):  # REF test_matcher.py:103-110
+    from paper_2411_15100_b200.compat import Matcher
+
+    bundle, vocab, _ = fig2
+    m = Matcher(bundle, vocab, history_window=16)
+    before = m.next_token_mask()
+    assert not m.accept_bytes(b"[x")
+    assert m.next_token_mask() == before
+    assert m.accept_bytes(b"")
+    assert m.history_depth == 1
+    assert m.next_token_mask() == before
+
+
+def test_empty_and_special_tokens_rejected():  # REF test_matcher.py:113-123
+    from paper_2411_15100_b200.compat import Matcher, compile_bundle
+
+    vocab = vocab_from_tokens([b"a", b"", b"<pad>", b"<eos>"], eos_id=3, special=[2, 3])
+    m = Matcher(compile_bundle('root ::= "a" | ""', vocab), vocab)
+    mask = m.next_token_mask()
+    assert mask.is_allowed(0) and not mask.is_allowed(1) and not mask.is_allowed(2) and mask.is_allowed(3)
+    assert not m.accept_token(1)
+    assert not m.accept_token(2)
+
+
+def test_eos_semantics(fig2):  # REF test_matcher.py:126-139
+    from paper_2411_15100_b200.compat import Matcher, MatcherError
+
+    bundle, vocab, _ = fig2
+    m = Matcher(bundle, vocab)
+    assert not m.can_terminate()
+    assert not m.accept_token(vocab.eos_id)
+    assert m.accept_bytes(b"[]")
+    assert m.can_terminate()
+    assert m.accept_token(vocab.eos_id)
+    assert m.terminated
+    with pytest.raises(MatcherError, match="terminated"):
+        m.next_token_mask()
+    m.rollback(1)
+    assert not m.terminated
+    assert m.can_terminate()
+
+
+def test_forced_grammar_eos_only():  # REF test_matcher.py:142-148
+    from paper_2411_15100_b200.compat import Matcher, compile_bundle
+
+    vocab = make_vocab([b"a", b"b"])
+    m = Matcher(compile_bundle('root ::= "a"', vocab), vocab)
+    assert m.accept_token(0)
+    assert list(m.next_token_mask().allowed_ids()) == [vocab.eos_id]
+
+
+def test_rollback_round_trip_and_bounds(fig2):  # REF test_matcher.py:154-181
+    from paper_2411_15100_b200.compat import Matcher, MatcherError
+
+    bundle, vocab, _ = fig2
+    m = Matcher(bundle, vocab, history_window=8)
+    fresh = m.next_token_mask()
+    assert m.accept_bytes(b"[")
+    assert m.accept_bytes(b'"a')
+    m.rollback(2)
+    assert m.next_token_mask() == fresh
+    assert m.accept_bytes(b"[") and m.accept_bytes(b'"a')
+    snap = m.next_token_mask()
+    m.rollback(1)
+    assert m.accept_bytes(b'"a')
+    assert m.next_token_mask() == snap
+    w = Matcher(bundle, vocab, history_window=4)
+    for _ in range(6):
+        assert w.accept_bytes(b"[")
+    assert w.history_depth == 4
+    with pytest.raises(MatcherError, match="roll back"):
+        w.rollback(5)
+    w.rollback(4)
+
+
+def test_rollback_determinism_random(fig2):  # REF test_matcher.py:184-205
+    from paper_2411_15100_b200.compat import Matcher
+
+    bundle, vocab, _ = fig2
+    rng = random.Random(3)
+    for _ in range(10):
+        m = Matcher(bundle, vocab, history_window=32)
+        accepted = []
+        for _ in range(rng.randrange(1, 10)):
+            ids = m.next_token_mask().allowed_ids()
+            pick = int(ids[rng.randrange(len(ids))])
+            if pick == vocab.eos_id:
+                break
+            m.accept_token(pick)
+            accepted.append(pick)
+        if not accepted:
+            continue
+        k = rng.randrange(1, len(accepted) + 1)
+        before = m.next_token_mask()
+        m.rollback(k)
+        for tid in accepted[-k:]:
+            assert m.accept_token(tid)
+        assert m.next_token_mask() == before
+
+
+def test_branch_divergence(fig2):  # REF test_matcher.py:211-226
+    from paper_2411_15100_b200.compat import Matcher
+
+    bundle, vocab, _ = fig2
+    a = Matcher(bundle, vocab)
+    a.accept_bytes(b"[")
+    b = a.branch()
+    assert a.next_token_mask() == b.next_token_mask()
+    a.accept_bytes(b'"x"')
+    b.accept_bytes(b"]")
+    ra = Matcher(bundle, vocab)
+    ra.accept_bytes(b'["x"')
+    rb = Matcher(bundle, vocab)
+    rb.accept_bytes(b"[]")
+    assert a.next_token_mask() == ra.next_token_mask()
+    assert b.can_terminate() == rb.can_terminate()
+
+
+def test_closed_matcher_raises(fig2):  # REF test_matcher.py:240-246
+    from paper_2411_15100_b200.compat import Matcher, MatcherError
+
+    bundle, vocab, _ = fig2
+    m = Matcher(bundle, vocab)
+    m.close()
+    with pytest.raises(MatcherError, match="closed"):
+        m.next_token_mask()
+    with pytest.raises(MatcherError, match="closed"):
+        m.branch()
+
+
+@pytest.mark.parametrize("grammar,toks,prefix,want,cap", [
+    ('root ::= "true"', [b"t", b"r", b"u", b"e"], b"", b"true", 4096),          # REF :306-313
+    ('root ::= "\\"k\\":" [0-9]', [b"k", b'"', b":", b"1"], b'"k', b'":', 4096),  # REF :321-326
+    ('root ::= "ab" | "a"', [b"a", b"b"], b"", b"a", 4096),                       # REF :329-333
+    ('root ::= "aaaaaaaaaa"', [b"a"], b"", b"aaaa", 4),                           # REF :336-339
+])
+def test_jump_forward(grammar, toks, prefix, want, cap):
+    from paper_2411_15100_b200.compat import Matcher, compile_bundle
+
+    vocab = make_vocab(toks)
+    m = Matcher(compile_bundle(grammar, vocab), vocab)
+    if prefix:
+        assert m.accept_bytes(prefix)
+    assert m.find_jump_forward_bytes(max_len=cap) == want
+    assert m.find_jump_forward_bytes(max_len=cap) == want  # state unchanged
+
+
+def test_jump_forward_stops_at_choice(fig2):  # REF test_matcher.py:316-318
+    from paper_2411_15100_b200.compat import Matcher
+
+    bundle, vocab, _ = fig2
+    assert Matcher(bundle, vocab).find_jump_forward_bytes() == b""
+
+
+def test_uncached_fill_matches_cached(fig2):  # REF test_matcher.py:345-363
+    from paper_2411_15100_b200.compat import CompileOptions, Matcher, compile_bundle
+
+    bundle, vocab, text = fig2
+    plain = compile_bundle(text, vocab, CompileOptions(inline=False, merge=False, cache=False))
+    rng = random.Random(23)
+    a, b = Matcher(bundle, vocab), Matcher(plain, vocab)
+    for _ in range(12):
+        ma, mb = a.next_token_mask(), b.next_token_mask()
+        assert ma == mb
+        ids = ma.allowed_ids()
+        pick = int(ids[rng.randrange(len(ids))])
+        if pick == vocab.eos_id:
+            break
+        assert a.accept_token(pick) and b.accept_token(pick)
+
+
+@pytest.mark.parametrize("name", ["array_string", "json", "arithmetic", "xml", "schema"])
+def test_lockstep_vs_oracle_random_walks(name):
+    """Device masks == oracle masks along random walks (toy200, REF
+    tests/test_acceptance.py:54-88 style), including EOS and state resets."""
+    from paper_2411_15100_b200.compat import Matcher, compile_bundle
+
+    vocab = vocab_by_name("toy200")
+    text = grammar_text(name)
+    bundle = compile_bundle(text, vocab)
+    ob = compile_oracle_bundle(text, vocab)
+    rng = random.Random(2024)
+    for _ in range(20):
+        m, r = Matcher(bundle, vocab, history_window=1), OracleMatcher(ob, history_window=1)
+        for _ in range(rng.randrange(1, 16)):
+            got = m.next_token_mask().words
+            assert np.array_equal(got, r.fill()), name
+            ids = [t for t in range(vocab.size) if (int(got[t >> 5]) >> (t & 31)) & 1]
+            pick = ids[rng.randrange(len(ids))]
+            assert m.accept_token(pick) and r.accept_token(pick)
+            if pick == vocab.eos_id:
+                break
+        m.close()
+
+
+def test_guided_generation_is_in_language():  # REF test_matcher.py:376-386
+    from oracle.pda import stacks_accept, step_stacks
+    from paper_2411_15100_b200.compat import Matcher, compile_bundle
+
+    vocab = vocab_by_name("gen")
+    rng = random.Random(4)
+    for name in ("array_string", "json", "arithmetic", "xml", "schema"):
+        text = grammar_text(name)
+        bundle = compile_bundle(text, vocab)
+        ob = compile_oracle_bundle(text, vocab)
+        for _ in range(3):
+            m = Matcher(bundle, vocab)
+            out = b""
+            for _ in range(4096):
+                ids = m.next_token_mask().allowed_ids()
+                pick = int(ids[rng.randrange(len(ids))])
+                assert m.accept_token(pick)
+                if pick == vocab.eos_id:
+                    break
+                out += vocab.tokens[pick]
+            assert stacks_accept(ob.pda, step_stacks(ob.pda, [(ob.pda.start_node(),)], out)), (name, out)
+            m.close()

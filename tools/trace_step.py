@@ -1,0 +1,79 @@
+"""Diagnostics: per-phase timing of the accept (K4) and fill (K2) kernels.
+
+Runs the bench workload (JSON grammar, synth_vocab(128256), batch 128) with
+GMASK_TRACE=1 so CTA 0 of every launch records %globaltimer stamps at phase
+boundaries, and prints the phase deltas for a few steps (cold L2: a 256 MiB
+flush before each step, as in bench.py).
+
+    GMASK_TRACE=1 python tools/trace_step.py
+"""
+
+import ctypes as C
+import os
+import sys
+
+os.environ.setdefault("GMASK_TRACE", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2411_15100_b200 as gm  # noqa: E402
+from paper_2411_15100_b200 import _lib  # noqa: E402
+from paper_2411_15100_b200.engine import get_pool  # noqa: E402
+from paper_2411_15100_b200.matcher import batch_accept, batch_fill, batch_recycle  # noqa: E402
+
+
+def main(steps=12, flush=True):
+    torch.cuda.set_device(0)
+    vocab = gm.synth_vocab(128256)
+    info = gm.TokenizerInfo.from_vocabulary(vocab)
+    compiled = gm.GrammarCompiler(info).compile_builtin_json_grammar()
+    pool = get_pool()
+    B = 128
+    ms = [gm.GrammarMatcher(compiled, max_rollback_tokens=1) for _ in range(B)]
+    dev = pool.device
+    slots = torch.tensor([m.slot for m in ms], dtype=torch.int32, device=dev)
+    rows = torch.arange(B, device=dev)
+    structural = torch.from_numpy(bench.structural_flags(vocab)).to(dev)
+    bitmask = torch.empty((B, (vocab.size + 31) // 32), dtype=torch.int32, device=dev)
+    acc = torch.empty(B, dtype=torch.uint8, device=dev)
+    fl = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
+    buf = (C.c_uint64 * 64)()
+    lib = _lib.load()
+    for s in range(steps):
+        if flush:
+            fl.zero_()
+        batch_fill(pool, slots, bitmask)
+        torch.cuda.synchronize()
+        _lib.check(lib.gm_pool_trace(pool.handle, buf))
+        f = [buf[16 + k] for k in range(8)]
+        extra = f"deps={buf[24]} key0={C.c_int64(buf[25]).value} ntops={buf[26]}"
+        if buf[24]:
+            ln = buf[44] & 0xFFFF
+            walk = [(buf[32 + b] & 0xFFFFFFFFFFFF, buf[32 + b] >> 48) for b in range(min(ln, 12))]
+            extra += f" | walk0 len={ln} spill={(buf[44] >> 16) & 0xFFFF} nchain={buf[44] >> 32} cycles/byte(n)={walk}"
+            for b in range(13):
+                buf[32 + b] = 0
+        allowed = bench.unpack_allowed(bitmask, vocab.size)
+        toks = bench.sample_tokens(allowed, structural, s, rows).to(torch.int32)
+        if flush:
+            fl.zero_()
+        torch.cuda.synchronize()
+        batch_accept(pool, slots, toks, acc)
+        torch.cuda.synchronize()
+        _lib.check(lib.gm_pool_trace(pool.handle, buf))
+        a = [buf[k] for k in range(6)]
+        batch_recycle(pool, slots)
+
+        def deltas(v):
+            out = []
+            for k in range(1, len(v)):
+                out.append(f"{(v[k] - v[k - 1]) / 1e3:6.2f}" if v[k] and v[k - 1] and v[k] >= v[k - 1] else "   -  ")
+            return " ".join(out)
+
+        print(f"step {s:2d} fill phases(us): {deltas(f)}   accept phases(us): {deltas(a)}  tok0={int(toks[0])} {extra}")
+
+
+if __name__ == "__main__":
+    main(flush="--warm" not in sys.argv)

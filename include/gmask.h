@@ -209,6 +209,17 @@ gm_status gm_fill_tokens(gm_pool* p, const int32_t* slots, int32_t n,
                          const int32_t* rows, uint8_t* need_apply_out,
                          void* stream);
 
+/* K3: fused fill + apply.  For i < n (row = rows ? rows[i] : i) computes the
+ * mask of slots[i] exactly as gm_fill_tokens, optionally stores it to
+ * bitmask[row] (bitmask nullable), and masks logits[row, :vocab_size] in
+ * place exactly as gm_apply_inplace — one launch, no bitmask round trip
+ * through HBM.  dtype: GM_DTYPE_*; logits rows must be 16-byte aligned. */
+gm_status gm_fill_apply_tokens(gm_pool* p, const int32_t* slots, int32_t n,
+                               int32_t* bitmask, int64_t bitmask_stride,
+                               const int32_t* rows, void* logits, int32_t dtype,
+                               int64_t vocab_size, int64_t logits_stride,
+                               void* stream);
+
 /* rollback `steps` acceptances of each slot (REF matcher.py:310-326);
  * slots/steps are device int32[n]. */
 gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps,

@@ -26,6 +26,8 @@ gm_status launch_row_popcount(const uint32_t*, int32_t, int32_t, int64_t*, cudaS
 gm_status launch_dep_compact(const uint32_t*, int32_t, int32_t, const int32_t*, int32_t*, cudaStream_t);
 gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*,
                       uint8_t*, int32_t, cudaStream_t);
+gm_status launch_fill_apply(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*, int32_t,
+                            void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_accept_tokens(const DevPool&, const int32_t*, const int32_t*, int32_t, uint8_t*, cudaStream_t);
 gm_status launch_accept_bytes(const DevPool&, int32_t, const uint8_t*, int64_t, uint8_t*, cudaStream_t);
 gm_status launch_reset(const DevPool&, int32_t, const DevBinding*, int32_t, int32_t, cudaStream_t);
@@ -587,6 +589,24 @@ gm_status gm_fill_tokens(gm_pool* p, const int32_t* slots, int32_t n, int32_t* b
   if (!p) return fail(GM_ERR_INVALID, "null pool");
   return launch_fill(p->dev, slots, n, bitmask, bitmask_stride, rows, need_apply_out, p->max_w,
                      as_stream(stream));
+}
+
+gm_status gm_fill_apply_tokens(gm_pool* p, const int32_t* slots, int32_t n, int32_t* bitmask, int64_t bitmask_stride,
+                               const int32_t* rows, void* logits, int32_t dtype, int64_t vocab_size,
+                               int64_t logits_stride, void* stream) {
+  if (!p || !logits) return fail(GM_ERR_INVALID, "null pool/logits");
+  int32_t eb;
+  uint32_t neg;
+  switch (dtype) {
+    case GM_DTYPE_F32: eb = 4; neg = 0xFF800000u; break;
+    case GM_DTYPE_F16: eb = 2; neg = 0xFC00FC00u; break;
+    case GM_DTYPE_BF16: eb = 2; neg = 0xFF80FF80u; break;
+    default: return fail(GM_ERR_INVALID, "unknown dtype");
+  }
+  if (reinterpret_cast<uintptr_t>(logits) % 16 || (logits_stride * eb) % 16)
+    return fail(GM_ERR_INVALID, "fused fill+apply needs 16-byte aligned logits rows");
+  return launch_fill_apply(p->dev, slots, n, bitmask, bitmask_stride, rows, p->max_w, logits, eb, neg, vocab_size,
+                           logits_stride * eb, as_stream(stream));
 }
 
 gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps, int32_t n, void* stream) {

@@ -33,9 +33,39 @@ constexpr int kDepF = 64;
 constexpr int kDepR = 4;    // register walker: stacks
 constexpr int kDepRF = 24;  // register walker: local frames
 
+// K3 tail: mask one logits row in place from the finished mask words in
+// shared memory (coalesced 16-byte chunks, -inf only where masked, logits
+// never read; mixed chunks store just their masked elements).
+__device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_t* __restrict__ words, int64_t vocab,
+                                          int eb, uint32_t neg) {
+  const int vec = 16 / eb;
+  const uint32_t full = (1u << vec) - 1u;
+  const int64_t chunks = (vocab + vec - 1) / vec;
+  for (int64_t c = threadIdx.x; c < chunks; c += blockDim.x) {
+    const int64_t tok0 = c * vec;
+    uint32_t keep = (words[tok0 >> 5] >> (tok0 & 31)) & full;
+    if (tok0 + vec > vocab) keep |= full & ~((1u << (vocab - tok0)) - 1u);
+    if (keep == full) continue;
+    char* p = rowp + tok0 * eb;
+    if (keep == 0) {
+      asm volatile("st.global.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(neg) : "memory");
+    } else {
+      uint32_t m = ~keep & full;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        if (eb == 4) *reinterpret_cast<uint32_t*>(p + j * 4) = neg;
+        else *reinterpret_cast<uint16_t*>(p + j * 2) = (uint16_t)neg;
+      }
+    }
+  }
+}
+
+template <bool APPLY>
 __global__ void __launch_bounds__(kFillThreads)
 fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
-            int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wmax) {
+            int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wmax,
+            char* __restrict__ logits, int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* dep_acc = reinterpret_cast<uint32_t*>(smem);                    // [Wmax]
   uint8_t* tables = smem + (((size_t)Wmax * 4 + 15) & ~(size_t)15);        // staged blob
@@ -88,7 +118,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
 
   // Stage the accepted rows of every top and the universe into shared memory
   // with TMA bulk copies; they land while the dependent walks run.
-  const bool vec = ((reinterpret_cast<uintptr_t>(bitmask + row * bstride) & 15) == 0) && (W % 4 == 0);
+  const bool vec = (!bitmask || (reinterpret_cast<uintptr_t>(bitmask + row * bstride) & 15) == 0) && (W % 4 == 0);
   const bool tma = vec && nt <= kTmaRows;
   const int32_t W4 = W >> 2;
   const size_t row_bytes = ((size_t)W * 4 + 15) & ~(size_t)15;
@@ -179,7 +209,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   trace_mark(P, 1, 6);
 
   // Merge and store.
-  uint32_t* out = bitmask + row * bstride;
+  uint32_t* out = bitmask ? bitmask + row * bstride : nullptr;
   const int32_t eos_w = hd.eos >> 5;
   const uint32_t eos_bit = (!terminated && (hd.flags & 2)) ? (1u << (hd.eos & 31)) : 0u;
   const uint32_t tail = (hd.V & 31) ? ((1u << (hd.V & 31)) - 1u) : 0xFFFFFFFFu;
@@ -203,7 +233,9 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
         if (w == W - 1) v[e] &= tail;
         partial |= (v[e] != ((w == W - 1) ? tail : 0xFFFFFFFFu));
       }
-      reinterpret_cast<uint4*>(out)[w4] = make_uint4(v[0], v[1], v[2], v[3]);
+      const uint4 fin = make_uint4(v[0], v[1], v[2], v[3]);
+      if (out) reinterpret_cast<uint4*>(out)[w4] = fin;
+      if (APPLY) reinterpret_cast<uint4*>(dep_acc)[w4] = fin;  // own slot only
     }
   } else {
     for (int32_t w = threadIdx.x; w < W; w += blockDim.x) {
@@ -216,32 +248,57 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       if (w == eos_w) a |= eos_bit;
       if (w == W - 1) a &= tail;
       partial |= (a != ((w == W - 1) ? tail : 0xFFFFFFFFu));
-      out[w] = a;
+      if (out) out[w] = a;
+      if (APPLY) dep_acc[w] = a;
     }
   }
   trace_mark(P, 1, 7);
-  if (need_apply) {
+  if (need_apply || APPLY) {
     if (partial) s_partial = 1;
     __syncthreads();
-    if (threadIdx.x == 0) need_apply[i] = (uint8_t)s_partial;
+    if (need_apply && threadIdx.x == 0) need_apply[i] = (uint8_t)s_partial;
   }
+  if (APPLY && s_partial) apply_row(logits + row * lstride_bytes, dep_acc, ap_vocab, ap_eb, ap_neg);
+}
+
+template <bool APPLY>
+static gm_status fill_attrs() {
+  GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel<APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  // small shared carveout: the dependent walkers' local state must hit L1
+  GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel<APPLY>, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
+  return GM_OK;
+}
+
+static size_t fill_smem(int32_t Wmax) {
+  const size_t row_bytes = ((size_t)Wmax * 4 + 15) & ~(size_t)15;
+  return row_bytes + kStageBytes + (kTmaRows + 1) * row_bytes;
 }
 
 gm_status launch_fill(const DevPool& P, const int32_t* slots, int32_t n, int32_t* bitmask, int64_t bstride,
                       const int32_t* rows, uint8_t* need_apply, int32_t Wmax, cudaStream_t s) {
   if (n <= 0) return GM_OK;
-  const size_t row_bytes = ((size_t)Wmax * 4 + 15) & ~(size_t)15;
-  const size_t smem = row_bytes + kStageBytes + (kTmaRows + 1) * row_bytes;
+  const size_t smem = fill_smem(Wmax);
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
-  static bool attr_set = false;
-  if (!attr_set) {
-    GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    // small shared carveout: the dependent walkers' local state must hit L1
-    GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
-    attr_set = true;
-  }
-  fill_kernel<<<n, kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows,
-                                            need_apply, Wmax);
+  static gm_status attrs = fill_attrs<false>();
+  if (attrs) return attrs;
+  fill_kernel<false><<<n, kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows,
+                                                   need_apply, Wmax, nullptr, 0, 0, 2, 0u);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+
+// K3: fill + apply in one kernel (no bitmask round trip, one launch).
+gm_status launch_fill_apply(const DevPool& P, const int32_t* slots, int32_t n, int32_t* bitmask, int64_t bstride,
+                            const int32_t* rows, int32_t Wmax, void* logits, int32_t eb, uint32_t neg,
+                            int64_t vocab, int64_t lstride_bytes, cudaStream_t s) {
+  if (n <= 0) return GM_OK;
+  const size_t smem = fill_smem(Wmax);
+  if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
+  static gm_status attrs = fill_attrs<true>();
+  if (attrs) return attrs;
+  fill_kernel<true><<<n, kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows,
+                                                  nullptr, Wmax, static_cast<char*>(logits), lstride_bytes, vocab,
+                                                  eb, neg);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

@@ -279,6 +279,14 @@ class BatchGrammarMatcher:
             rows = torch.as_tensor(list(indices), dtype=torch.int32).to(bitmask.device, non_blocking=True)
         batch_fill(get_pool(), self._slots(matchers), bitmask, rows)
 
+    def batch_fill_and_apply(self, matchers: Sequence[GrammarMatcher], logits: torch.Tensor,
+                             bitmask: Optional[torch.Tensor] = None, vocab_size: Optional[int] = None) -> None:
+        """Fused fill_next_token_bitmask + apply_token_bitmask_inplace for
+        logits[i] <- matchers[i] (one kernel; bitmask optional output)."""
+        if not matchers:
+            return
+        batch_fill_apply(get_pool(), self._slots(matchers), logits, bitmask, vocab_size=vocab_size)
+
     @staticmethod
     def batch_accept_token(matchers: Sequence[GrammarMatcher], tokens: Sequence[int],
                            debug_print: bool = False) -> List[bool]:
@@ -296,6 +304,24 @@ def batch_fill(pool: MatcherPool, slots: torch.Tensor, bitmask: torch.Tensor, ro
                                            bitmask.stride(0), rows.data_ptr() if rows is not None else None,
                                            need_apply.data_ptr() if need_apply is not None else None,
                                            _lib.stream_ptr(stream)), "gm_fill_tokens")
+
+
+def batch_fill_apply(pool: MatcherPool, slots: torch.Tensor, logits: torch.Tensor,
+                     bitmask: Optional[torch.Tensor] = None, rows: Optional[torch.Tensor] = None,
+                     vocab_size: Optional[int] = None, stream=None) -> None:
+    """K3: fill the masks of ``slots`` and apply them to ``logits`` in one
+    kernel (optionally also storing the bitmask).  Same results as
+    batch_fill followed by apply_token_bitmask_inplace."""
+    from .bitmask import _DTYPES
+
+    if logits.dtype not in _DTYPES or logits.dim() != 2 or logits.stride(-1) != 1:
+        raise ValueError("logits must be a 2-D fp32/fp16/bf16 CUDA tensor, contiguous per row")
+    v = logits.shape[1] if vocab_size is None else vocab_size
+    _lib.check(_lib.load().gm_fill_apply_tokens(
+        pool.handle, slots.data_ptr(), slots.numel(),
+        bitmask.data_ptr() if bitmask is not None else None, bitmask.stride(0) if bitmask is not None else 0,
+        rows.data_ptr() if rows is not None else None, logits.data_ptr(), _DTYPES[logits.dtype], v,
+        logits.stride(0), _lib.stream_ptr(stream)), "gm_fill_apply_tokens")
 
 
 def batch_recycle(pool: MatcherPool, slots: torch.Tensor, stream=None) -> None:

@@ -299,3 +299,41 @@ def test_guided_generation_is_in_language():  # REF test_matcher.py:376-386
                 out += vocab.tokens[pick]
             assert stacks_accept(ob.pda, step_stacks(ob.pda, [(ob.pda.start_node(),)], out)), (name, out)
             m.close()
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_fused_fill_apply_equals_separate(dtype):
+    """K3 (one kernel) == K2 fill then K0 apply, bit for bit, along a trajectory."""
+    import torch
+
+    import paper_2411_15100_b200 as gm
+    from paper_2411_15100_b200.engine import get_pool
+    from paper_2411_15100_b200.matcher import batch_fill, batch_fill_apply
+
+    vocab = vocab_by_name("4000:mixed")
+    info = gm.TokenizerInfo.from_vocabulary(vocab)
+    compiled = gm.GrammarCompiler(info).compile_builtin_json_grammar()
+    B = 6
+    ms = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    pool = get_pool()
+    slots = torch.tensor([m.slot for m in ms], dtype=torch.int32, device="cuda")
+    dt = getattr(torch, dtype)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    W = (vocab.size + 31) // 32
+    for step in range(12):
+        logits = torch.randn(B, vocab.size, device="cuda", generator=g).to(dt)
+        a, b = logits.clone(), logits.clone()
+        bm1 = torch.empty((B, W), dtype=torch.int32, device="cuda")
+        bm2 = torch.empty((B, W), dtype=torch.int32, device="cuda")
+        batch_fill(pool, slots, bm1)
+        gm.apply_token_bitmask_inplace(a, bm1)
+        batch_fill_apply(pool, slots, b, bm2)
+        assert torch.equal(bm1, bm2)
+        assert torch.equal(a.view(torch.int16 if dt != torch.float32 else torch.int32),
+                           b.view(torch.int16 if dt != torch.float32 else torch.int32))
+        c = logits.clone()
+        batch_fill_apply(pool, slots, c)  # no bitmask output
+        assert torch.equal(a.view(torch.int8), c.view(torch.int8))
+        b[:, vocab.eos_id] = float("-inf")
+        toks = b.float().argmax(-1).tolist()
+        assert all(gm.BatchGrammarMatcher.batch_accept_token(ms, toks))

@@ -250,9 +250,10 @@ gm_status gm_pool_check(gm_pool* p, int32_t* flags_out);
 /* arena statistics: live entries */
 int64_t gm_pool_arena_used(gm_pool* p);
 /* Diagnostics: phase timestamps (ns, %globaltimer) of CTA 0 of the last
- * accept (out[0..16)) and fill (out[16..32)) launches when the pool was
- * created with GMASK_TRACE=1; returns GM_ERR_INVALID otherwise.  Syncs. */
-gm_status gm_pool_trace(gm_pool* p, uint64_t* out64);
+ * accept (out[0..16)) and fill (out[16..32)) launches, then per-CTA
+ * durations (fill: out[64 + 2i], accept: out[64 + 2*capacity + i]) when the
+ * pool was created with GMASK_TRACE=1; GM_ERR_INVALID otherwise.  Syncs. */
+gm_status gm_pool_trace(gm_pool* p, uint64_t* out, int64_t n);
 
 #ifdef __cplusplus
 }

@@ -102,7 +102,7 @@ _SIGNATURES = {
     "gm_pool_first_bytes": ([_P, _I32, _P, _P], _I32),
     "gm_pool_check": ([_P, _P], _I32),
     "gm_pool_arena_used": ([_P], _I64),
-    "gm_pool_trace": ([_P, _P], _I32),
+    "gm_pool_trace": ([_P, _P, _I64], _I32),
 }
 
 _lib = None

@@ -527,8 +527,8 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   unsigned long long* trace = nullptr;
   const char* tr = getenv("GMASK_TRACE");
   if (tr && tr[0] == '1') {
-    if ((st = p->mem.alloc(&trace, 64))) return st;
-    GM_CUDA_TRY(cudaMemset(trace, 0, 64 * 8));
+    if ((st = p->mem.alloc(&trace, 64 + 3 * (size_t)capacity))) return st;
+    GM_CUDA_TRY(cudaMemset(trace, 0, (64 + 3 * (size_t)capacity) * 8));
   }
   p->dev = DevPool{capacity, max_stacks, H,   tops, meta, head, hist, win, bind,
                    DevArena{keys, acap - 1, err}, err, hdr, trace};
@@ -673,10 +673,12 @@ gm_status gm_pool_materialize(gm_pool* p, int32_t handle, int32_t* out, int32_t 
   return GM_OK;
 }
 
-gm_status gm_pool_trace(gm_pool* p, uint64_t* out64) {
+gm_status gm_pool_trace(gm_pool* p, uint64_t* out, int64_t n) {
   if (!p || !p->dev.trace) return fail(GM_ERR_INVALID, "pool created without GMASK_TRACE=1");
+  const int64_t cap = 64 + 3 * (int64_t)p->dev.capacity;
+  if (n > cap) n = cap;
   GM_CUDA_TRY(cudaDeviceSynchronize());
-  GM_CUDA_TRY(cudaMemcpy(out64, p->dev.trace, 64 * 8, cudaMemcpyDeviceToHost));
+  GM_CUDA_TRY(cudaMemcpy(out, p->dev.trace, n * 8, cudaMemcpyDeviceToHost));
   return GM_OK;
 }
 

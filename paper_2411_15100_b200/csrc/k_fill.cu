@@ -76,6 +76,8 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   const int32_t i = blockIdx.x;
   if (i >= n) return;
   trace_mark(P, 1, 0);
+  unsigned long long t_start = 0;
+  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int32_t slot = __ldg(slots + i);
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   load_header(P, slot, &hd);
@@ -142,6 +144,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   trace_mark(P, 1, 3);
   int total = 0;
   for (int s = 0; s < nt; ++s) total += s_hi[s] - s_lo[s];
+  (void)total;
   if (P.trace && blockIdx.x == 0 && threadIdx.x == 0) {
     P.trace[16 + 8] = (unsigned long long)total;
     P.trace[16 + 9] = (unsigned long long)(nt > 0 ? s_key[0] : -1);
@@ -259,6 +262,12 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     if (need_apply && threadIdx.x == 0) need_apply[i] = (uint8_t)s_partial;
   }
   if (APPLY && s_partial) apply_row(logits + row * lstride_bytes, dep_acc, ap_vocab, ap_eb, ap_neg);
+  if (P.trace && threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    P.trace[64 + 2 * blockIdx.x] = t1 - t_start;
+    P.trace[64 + 2 * blockIdx.x + 1] = (unsigned long long)total | ((unsigned long long)nt << 32);
+  }
 }
 
 template <bool APPLY>

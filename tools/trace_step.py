@@ -39,15 +39,20 @@ def main(steps=12, flush=True):
     bitmask = torch.empty((B, (vocab.size + 31) // 32), dtype=torch.int32, device=dev)
     acc = torch.empty(B, dtype=torch.uint8, device=dev)
     fl = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
-    buf = (C.c_uint64 * 64)()
+    NB = 64 + 3 * pool.capacity
+    buf = (C.c_uint64 * NB)()
     lib = _lib.load()
     for s in range(steps):
         if flush:
             fl.zero_()
         batch_fill(pool, slots, bitmask)
         torch.cuda.synchronize()
-        _lib.check(lib.gm_pool_trace(pool.handle, buf))
+        _lib.check(lib.gm_pool_trace(pool.handle, buf, NB))
         f = [buf[16 + k] for k in range(8)]
+        cta = sorted(((buf[64 + 2 * i] / 1e3, buf[65 + 2 * i] & 0xFFFFFFFF, buf[65 + 2 * i] >> 32)
+                      for i in range(B)), reverse=True)
+        print(f"  fill per-CTA us: max {cta[0][0]:.2f} p50 {cta[B // 2][0]:.2f}  slowest (us, deps, tops): "
+              f"{[(round(a, 2), b, c) for a, b, c in cta[:4]]}")
         extra = f"deps={buf[24]} key0={C.c_int64(buf[25]).value} ntops={buf[26]}"
         if buf[24]:
             ln = buf[44] & 0xFFFF
@@ -62,7 +67,7 @@ def main(steps=12, flush=True):
         torch.cuda.synchronize()
         batch_accept(pool, slots, toks, acc)
         torch.cuda.synchronize()
-        _lib.check(lib.gm_pool_trace(pool.handle, buf))
+        _lib.check(lib.gm_pool_trace(pool.handle, buf, NB))
         a = [buf[k] for k in range(6)]
         batch_recycle(pool, slots)
 

@@ -49,7 +49,7 @@ enum : uint32_t {
 struct BlobHdr {
   int32_t bytes, n_classes, n_nodes, o_bc;
   int32_t o_flags, o_toff, o_trans, o_pool;
-  int32_t o_kon, o_rule, o_ninfo, o_fast, pad[4];
+  int32_t o_kon, o_rule, o_ninfo, o_fast, o_callers, pad[3];
 };
 static_assert(sizeof(BlobHdr) == 64, "BlobHdr layout");
 
@@ -67,6 +67,7 @@ struct DevGrammar {
   const int32_t* follow_next;  // [n_fstates*n_classes]
   const int4* node_info;       // binding views only
   const int32_t* fast;         // [n_nodes*n_classes] single-stack DFA move, -1 dies, -2 general
+  const int32_t* callers;      // [n_rules*kMaxCallers] return nodes that can sit below a frame of the rule, -1 pad
   const uint8_t* blob;
   int32_t blob_bytes;
 };
@@ -86,12 +87,19 @@ __device__ __forceinline__ DevGrammar blob_view(const uint8_t* base) {
   g.node_rule = reinterpret_cast<const int32_t*>(base + h->o_rule);
   g.node_info = h->o_ninfo ? reinterpret_cast<const int4*>(base + h->o_ninfo) : nullptr;
   g.fast = reinterpret_cast<const int32_t*>(base + h->o_fast);
+  g.callers = reinterpret_cast<const int32_t*>(base + h->o_callers);
   g.blob = base;
   g.blob_bytes = h->bytes;
   return g;
 }
 
-constexpr int kStageBytes = 32 * 1024;  // shared-memory budget for staged tables
+constexpr int kStageBytes = 32 * 1024;
+// One-level context classes of a dependent token, packed 2 bits per caller
+// (caller j of the key's rule) into the dependent record's 4th word.
+// Index kRootCaller is the bottom of the stack (a top on the root frame).
+constexpr int kMaxCallers = 16;
+constexpr int kRootCaller = kMaxCallers - 1;
+constexpr uint32_t kCtxUnknown = 0, kCtxAccept = 1, kCtxReject = 2, kCtxDeeper = 3;  // shared-memory budget for staged tables
 
 // Stage a blob (`bytes` long, 16-byte multiple) into shared memory with one
 // TMA bulk copy (cp.async.bulk, completion tracked by an mbarrier): a single

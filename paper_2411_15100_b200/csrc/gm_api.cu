@@ -24,6 +24,7 @@ gm_status launch_cache_build(const DevGrammar&, const DevVocab&, const DevArena&
                              uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
 gm_status launch_row_popcount(const uint32_t*, int32_t, int32_t, int64_t*, cudaStream_t);
 gm_status launch_dep_compact(const uint32_t*, int32_t, int32_t, const int32_t*, int32_t*, cudaStream_t);
+gm_status launch_dep_context(const DevGrammar&, const int4*, int64_t, uint8_t*, cudaStream_t);
 gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*,
                       uint8_t*, int32_t, cudaStream_t);
 gm_status launch_fill_apply(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*, int32_t,
@@ -282,6 +283,29 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
       fast[(size_t)idx] = f;
     }
   const size_t o_fast = put(fast.data(), fast.size() * 4);
+  // callers[rule]: the return nodes a push run leaves directly below a frame
+  // of that rule (the frame under a pushed p_{i+1} holds p_i; under the
+  // run's target, the last pushed node).  Frames only ever get parents this
+  // way, so the set is exact; a rule with more than kRootCaller callers keeps
+  // the first ones and the fill walks for the rest.
+  std::vector<int32_t> callers((size_t)t->n_rules * kMaxCallers, -1);
+  std::vector<int32_t> n_callers(t->n_rules, 0);
+  auto add_caller = [&](int32_t below_of, int32_t ret) {
+    const int32_t r = t->node_rule[below_of];
+    if (r < 0 || r >= t->n_rules) return;
+    int32_t* c = callers.data() + (size_t)r * kMaxCallers;
+    for (int j = 0; j < n_callers[r]; ++j)
+      if (c[j] == ret) return;
+    if (n_callers[r] < kRootCaller) c[n_callers[r]++] = ret;
+  };
+  for (int32_t i = 0; i < t->n_trans; ++i) {
+    const int32_t d = t->trans[2 * i];
+    const uint32_t pk = (uint32_t)t->trans[2 * i + 1];
+    const uint32_t poff = pk & 0xFFFFFF, plen = pk >> 24;
+    for (uint32_t k = 0; k < plen; ++k)
+      add_caller(k + 1 < plen ? t->push_pool[poff + k + 1] : d, t->push_pool[poff + k]);
+  }
+  const size_t o_callers = put(callers.data(), callers.size() * 4);
   if (blob.size() > (size_t)INT32_MAX) return fail(GM_ERR_INVALID, "automaton tables too large");
   BlobHdr bh{};
   bh.bytes = (int32_t)blob.size();
@@ -296,6 +320,7 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
   bh.o_rule = (int32_t)o_rule;
   bh.o_ninfo = 0;
   bh.o_fast = (int32_t)o_fast;
+  bh.o_callers = (int32_t)o_callers;
   std::memcpy(blob.data(), &bh, sizeof(bh));
   gm_grammar* g = new gm_grammar();
   gm_status st;
@@ -328,6 +353,7 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
   G.follow_next = fnext;
   G.node_info = nullptr;
   G.fast = reinterpret_cast<const int32_t*>(d_blob + o_fast);
+  G.callers = reinterpret_cast<const int32_t*>(d_blob + o_callers);
   G.blob = d_blob;
   G.blob_bytes = (int32_t)blob.size();
   g->keys.assign(t->cache_keys, t->cache_keys + t->n_keys);
@@ -448,6 +474,33 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
   if ((st = c->mem.upload(&d_dep, depbuf.data(), depbuf.size())) ||
       (st = c->mem.upload(&d_bblob, bblob.data(), bblob.size())))
     return st;
+  // one-level context classes per (dependent entry, caller of the key's rule)
+  {
+    BlobHdr gh;
+    std::memcpy(&gh, g->blob_host.data(), sizeof(gh));
+    const int32_t* callers = reinterpret_cast<const int32_t*>(g->blob_host.data() + gh.o_callers);
+    std::vector<int4> tasks;
+    for (int32_t k = 0; k < n; ++k) {
+      const int32_t nd = g->keys[k];
+      const int32_t* cr = callers + (size_t)g->node_rule[nd] * kMaxCallers;
+      const bool root = g->node_rule[nd] == g->node_rule[g->dev.start_node];
+      for (int32_t i = off[k]; i < off[k + 1]; ++i) {
+        for (int j = 0; j < kRootCaller && cr[j] >= 0; ++j) tasks.push_back(make_int4(i, j, nd, cr[j]));
+        if (root) tasks.push_back(make_int4(i, kRootCaller, nd, -1));
+      }
+    }
+    if (!tasks.empty()) {
+      DevAllocs tmp;
+      int4* d_tasks;
+      if ((st = tmp.upload(&d_tasks, tasks.data(), tasks.size())) ||
+          (st = launch_dep_context(g->dev, d_tasks, (int64_t)tasks.size(), d_dep, s))) {
+        tmp.release();
+        return st;
+      }
+      GM_CUDA_TRY(cudaStreamSynchronize(s));
+      tmp.release();
+    }
+  }
   c->host_binding.g = g->dev;
   c->host_binding.v = v->dev;
   c->host_binding.c = DevCache{acc, dep_off, dep_ids, reinterpret_cast<const int4*>(d_dep), d_dep + drec, d_bblob,

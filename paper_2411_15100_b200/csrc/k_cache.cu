@@ -115,6 +115,43 @@ __global__ void dep_compact_kernel(const uint32_t* __restrict__ rows, int32_t W,
   }
 }
 
+// One-level context classes of the dependent tokens (compile time).  A
+// dependent token of key n dies inside n's rule but for branches that pop
+// past n's frame, so its fate depends on the frames below.  For every
+// caller c of n's rule (a return node that can sit directly below that
+// frame) walk the token from the two-frame stack [c | n]:
+//   survives                      -> accepted whatever lies below c
+//   dies, no branch pops past c   -> rejected whatever lies below c
+//   some branch pops past c       -> needs the request's deeper stack
+// The class is or-ed into the record's 4th word (2 bits per caller index);
+// the fill then walks only the "deeper" ones (and unknown callers).
+// This is an exact refinement of the reference's context-dependent set
+// (REF matcher.py:219-237 resolves every one of them by a full walk).
+__global__ void dep_context_kernel(DevGrammar G, const int4* __restrict__ tasks, int64_t n_tasks,
+                                   uint8_t* __restrict__ dep) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_tasks) return;
+  const int4 tk = tasks[q];  // (entry, caller index, key node, caller node or -1 = root)
+  int4* rec = reinterpret_cast<int4*>(dep + (size_t)tk.x * 32);
+  const int4 e = rec[0], inl = rec[1];
+  const uint8_t* far = dep + e.z;
+  const DevArena A{nullptr, 0, nullptr};  // only local frames are touched
+  RWalker<8, 48> rw;
+  rw.init(nullptr, nullptr, 0);
+  // caller -1: the root frame, popping past it ends the walk
+  rw.add(tk.w < 0 ? -1 : rw.push(G, A, -1, tk.w), tk.z);
+  bool popped = false;
+  for (int b = 0; b < e.y && rw.n > 0 && !rw.spill; ++b) {
+    bool pb = false;
+    rw.step(G, A, rec_byte(inl, far, b), &pb);
+    popped |= pb;
+  }
+  uint32_t cls = kCtxUnknown;
+  if (!rw.spill && !rw.err)
+    cls = rw.n > 0 ? kCtxAccept : ((popped && tk.w >= 0) ? kCtxDeeper : kCtxReject);
+  if (cls) atomicOr(reinterpret_cast<int*>(&rec->w), (int)(cls << (2 * tk.y)));
+}
+
 }  // namespace gm
 
 using namespace gm;
@@ -137,6 +174,12 @@ gm_status launch_cache_build(const DevGrammar& G, const DevVocab& V, const DevAr
 gm_status launch_row_popcount(const uint32_t* rows, int32_t W, int32_t n, int64_t* out, cudaStream_t s) {
   if (n <= 0) return GM_OK;
   row_popcount_kernel<<<n, 256, 0, s>>>(rows, W, n, out);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_dep_context(const DevGrammar& G, const int4* tasks, int64_t n_tasks, uint8_t* dep, cudaStream_t s) {
+  if (n_tasks <= 0) return GM_OK;
+  dep_context_kernel<<<(unsigned)ceil_div(n_tasks, 128), 128, 0, s>>>(G, tasks, n_tasks, dep);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

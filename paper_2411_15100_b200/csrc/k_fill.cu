@@ -36,17 +36,18 @@ constexpr int kDepRF = 24;  // register walker: local frames
 // K3 tail: mask one logits row in place from the finished mask words in
 // shared memory (coalesced 16-byte chunks, -inf only where masked, logits
 // never read; mixed chunks store just their masked elements).
-__device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_t* __restrict__ words, int64_t vocab,
-                                          int eb, uint32_t neg) {
+__device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_t* __restrict__ words, int64_t tok_lo,
+                                          int64_t tok_hi, int eb, uint32_t neg) {
+  // words[] holds the mask from token tok_lo (a multiple of 128) on
   const int vec = 16 / eb;
   const uint32_t full = (1u << vec) - 1u;
-  const int64_t chunks = (vocab + vec - 1) / vec;
+  const int64_t chunks = (tok_hi - tok_lo + vec - 1) / vec;
   for (int64_t c = threadIdx.x; c < chunks; c += blockDim.x) {
-    const int64_t tok0 = c * vec;
-    uint32_t keep = (words[tok0 >> 5] >> (tok0 & 31)) & full;
-    if (tok0 + vec > vocab) keep |= full & ~((1u << (vocab - tok0)) - 1u);
+    const int64_t t0 = c * vec;  // relative to tok_lo
+    uint32_t keep = (words[t0 >> 5] >> (t0 & 31)) & full;
+    if (tok_lo + t0 + vec > tok_hi) keep |= full & ~((1u << (tok_hi - tok_lo - t0)) - 1u);
     if (keep == full) continue;
-    char* p = rowp + tok0 * eb;
+    char* p = rowp + (tok_lo + t0) * eb;
     if (keep == 0) {
       asm volatile("st.global.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(neg) : "memory");
     } else {
@@ -61,20 +62,32 @@ __device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_
   }
 }
 
+// Grid: (requests, splits).  A request's mask is cut into `splits` word
+// ranges (multiples of 4 words, i.e. 128 tokens) and each CTA owns one: it
+// merges only its slice of the rows, walks only the dependents whose token
+// falls in it, stores its slice of the bitmask and masks its slice of the
+// logits row.  Header and tables are read by every CTA of the request (one
+// round trip each, L2-shared); everything proportional to the vocabulary
+// shrinks by the split factor, so small batches still fill the 148 SMs.
 template <bool APPLY>
 __global__ void __launch_bounds__(kFillThreads)
 fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
-            int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wmax,
+            int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wp,
             char* __restrict__ logits, int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* dep_acc = reinterpret_cast<uint32_t*>(smem);                    // [Wmax]
-  uint8_t* tables = smem + (((size_t)Wmax * 4 + 15) & ~(size_t)15);        // staged blob
+  const size_t part_bytes = ((size_t)Wp * 4 + 15) & ~(size_t)15;
+  uint32_t* dep_acc = reinterpret_cast<uint32_t*>(smem);  // [Wp] this CTA's words
+  uint8_t* tables = smem + part_bytes;                    // staged blob
+  uint8_t* rows_s = tables + kStageBytes;                 // [kTmaRows + 1][part_bytes]
   __shared__ SlotHdr hd;
-  __shared__ int s_partial, s_nt;
+  __shared__ int s_partial, s_nt, s_nrows;
   __shared__ int32_t s_key[32], s_lo[32], s_hi[32];
   __shared__ int2 s_top[32];
+  __shared__ int s_cj[32];
+  __shared__ __align__(8) unsigned long long rows_bar;
   const int32_t i = blockIdx.x;
   if (i >= n) return;
+  const int32_t split = blockIdx.y, n_split = gridDim.y;
   trace_mark(P, 1, 0);
   unsigned long long t_start = 0;
   if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -84,14 +97,32 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   __syncthreads();
   trace_mark(P, 1, 1);
   const int32_t W = hd.W;
+  const int32_t per = ((W + 3) / 4 + n_split - 1) / n_split * 4;  // words per split
+  const int32_t w_lo = min(W, split * per), w_hi = min(W, w_lo + per), nw = w_hi - w_lo;
   const bool terminated = hd.flags & 1;
+  const bool vec = (!bitmask || (reinterpret_cast<uintptr_t>(bitmask + row * bstride) & 15) == 0) && (W % 4 == 0);
   if (threadIdx.x == 0) {
     s_partial = 0;
     int nt = hd.ntops;
     if (terminated) {
-      atomicOr(P.err, kErrTerminated);
+      if (split == 0) atomicOr(P.err, kErrTerminated);
       nt = 0;
     } else if (nt >= 0) {
+      // issue the row copies first: they are the longest-latency loads
+      if (vec && nt <= kTmaRows && nw > 0) {
+        int nr = 0;
+        for (int s = 0; s < nt; ++s) nr += hd.key[s] >= 0;
+        s_nrows = nr;
+        mbar_init(&rows_bar, (uint32_t)((nr + 1) * (size_t)nw * 4));
+        int k = 0;
+        for (int s = 0; s < nt; ++s) {
+          if (hd.key[s] < 0) continue;
+          bulk_g2s(rows_s + (size_t)k * part_bytes, hd.acc_rows + (size_t)hd.key[s] * W + w_lo, (uint32_t)nw * 4,
+                   &rows_bar);
+          ++k;
+        }
+        bulk_g2s(rows_s + (size_t)kTmaRows * part_bytes, hd.universe + w_lo, (uint32_t)nw * 4, &rows_bar);
+      }
       for (int s = 0; s < nt; ++s) {
         s_key[s] = hd.key[s];
         s_lo[s] = hd.dep_lo[s];
@@ -113,51 +144,51 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     }
     s_nt = nt;
   }
-  for (int32_t w = threadIdx.x; w < W; w += blockDim.x) dep_acc[w] = 0u;
+  for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) dep_acc[w] = 0u;
   __syncthreads();
   trace_mark(P, 1, 2);
   const int nt = s_nt;
-
-  // Stage the accepted rows of every top and the universe into shared memory
-  // with TMA bulk copies; they land while the dependent walks run.
-  const bool vec = (!bitmask || (reinterpret_cast<uintptr_t>(bitmask + row * bstride) & 15) == 0) && (W % 4 == 0);
-  const bool tma = vec && nt <= kTmaRows;
-  const int32_t W4 = W >> 2;
-  const size_t row_bytes = ((size_t)W * 4 + 15) & ~(size_t)15;
-  uint8_t* rows_s = tables + kStageBytes;  // [kTmaRows + 1][row_bytes]
-  __shared__ __align__(8) unsigned long long rows_bar;
-  __shared__ int s_nrows;
-  if (tma && threadIdx.x == 0) {
-    int nr = 0;
-    for (int s = 0; s < nt; ++s) nr += s_key[s] >= 0;
-    s_nrows = nr;
-    mbar_init(&rows_bar, (uint32_t)((nr + 1) * (size_t)W * 4));
-    int k = 0;
-    for (int s = 0; s < nt; ++s) {
-      if (s_key[s] < 0) continue;
-      bulk_g2s(rows_s + (size_t)k * row_bytes, hd.acc_rows + (size_t)s_key[s] * W, (uint32_t)W * 4, &rows_bar);
-      ++k;
-    }
-    bulk_g2s(rows_s + (size_t)kTmaRows * row_bytes, hd.universe, (uint32_t)W * 4, &rows_bar);
-  }
+  const bool tma = vec && hd.ntops >= 0 && nt <= kTmaRows && nw > 0 && !terminated;
 
   trace_mark(P, 1, 3);
   int total = 0;
   for (int s = 0; s < nt; ++s) total += s_hi[s] - s_lo[s];
-  (void)total;
-  if (P.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (P.trace && i == 0 && split == 0 && threadIdx.x == 0) {
     P.trace[16 + 8] = (unsigned long long)total;
     P.trace[16 + 9] = (unsigned long long)(nt > 0 ? s_key[0] : -1);
     P.trace[16 + 10] = (unsigned long long)nt;
   }
   if (total) {
     const DevGrammar G = stage_blob(hd.blob, hd.blob_bytes, tables);
+    // caller index of each top's parent frame within the callers of the
+    // top's rule: selects the dependents' one-level context class
+    if ((int)threadIdx.x < nt) {
+      const int2 t = s_top[threadIdx.x];
+      int cj = kRootCaller;  // the root frame: nothing below it
+      if (t.x >= 0) {
+        cj = -1;
+        const unsigned long long pk =
+            (hd.nchain > 0 && hd.chain_h[0] == t.x) ? hd.chain_k[0] : arena_load(P.arena, t.x);
+        if (pk != kEmptyKey) {
+          const int32_t pn = key_node(pk);
+          const int32_t* cr = G.callers + (size_t)G.node_rule[t.y] * kMaxCallers;
+          for (int j = 0; j < kRootCaller; ++j) {
+            const int32_t c = cr[j];
+            if (c < 0) break;
+            if (c == pn) { cj = j; break; }
+          }
+        }
+      }
+      s_cj[threadIdx.x] = cj;
+    }
+    __syncthreads();
     trace_mark(P, 1, 4);
     const uint8_t* rec_base = reinterpret_cast<const uint8_t*>(hd.dep_ent);
+    const int32_t tok_lo = w_lo * 32, tok_hi = w_hi * 32;
     // warp-major assignment: consecutive dependents go to different warps, so
     // a handful of walks run in parallel instead of diverging inside one warp
-    const int32_t nw = blockDim.x >> 5;
-    const int32_t q0 = (threadIdx.x & 31) * nw + (threadIdx.x >> 5);
+    const int32_t n_warps = blockDim.x >> 5;
+    const int32_t q0 = (threadIdx.x & 31) * n_warps + (threadIdx.x >> 5);
     for (int32_t q = q0; q < total; q += blockDim.x) {
       int s = 0, base = 0;
       while (q - base >= s_hi[s] - s_lo[s]) {
@@ -165,13 +196,23 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
         ++s;
       }
       const int4* rec = hd.dep_ent + 2 * (size_t)(s_lo[s] + (q - base));
-      const int4 e = __ldg(rec), inl = __ldg(rec + 1);
+      const int4 e = __ldg(rec);
       const int32_t tid = e.x;
-      if ((dep_acc[tid >> 5] >> (tid & 31)) & 1u) continue;  // already allowed by another stack
+      if (tid < tok_lo || tid >= tok_hi) continue;  // another split's token
+      uint32_t* acc_w = dep_acc + ((tid >> 5) - w_lo);
+      const uint32_t bit = 1u << (tid & 31);
+      if (*acc_w & bit) continue;  // already allowed by another stack
+      if (s_cj[s] >= 0) {
+        const uint32_t cls = ((uint32_t)e.w >> (2 * s_cj[s])) & 3u;
+        if (cls == kCtxReject) continue;
+        if (cls == kCtxAccept) {
+          atomicOr(acc_w, bit);
+          continue;
+        }
+      }
+      const int4 inl = __ldg(rec + 1);
       const int2 t = s_top[s];
       const uint8_t* far = rec_base + e.z;  // bytes beyond the inline 16
-      const bool tr = P.trace && blockIdx.x == 0 && q == 0;
-      long long c0 = tr ? clock64() : 0;
       // fast path: register walker; general walker only on spill
       RWalker<kDepR, kDepRF> rw;
       rw.init(hd.chain_h, hd.chain_k, hd.nchain);
@@ -179,14 +220,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       for (int b = 0; b < e.y && rw.n > 0 && !rw.spill; ++b) {
         bool pb = false;
         rw.step(G, P.arena, rec_byte(inl, far, b), &pb);
-        if (tr && b < 12) {
-          const long long c1 = clock64();
-          P.trace[32 + b] = (unsigned long long)(c1 - c0) | ((unsigned long long)rw.n << 48);
-          c0 = c1;
-        }
       }
-      if (tr) P.trace[44] = (unsigned long long)e.y | ((unsigned long long)rw.spill << 16) |
-                            ((unsigned long long)hd.nchain << 32);
       bool ok;
       if (!rw.spill) {
         if (rw.err) atomicOr(P.err, rw.err);
@@ -204,14 +238,14 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
         if (w.err) atomicOr(P.err, w.err);
         ok = w.n > 0;
       }
-      if (ok) atomicOr(dep_acc + (tid >> 5), 1u << (tid & 31));
+      if (ok) atomicOr(acc_w, bit);
     }
   }
   trace_mark(P, 1, 5);
   __syncthreads();
   trace_mark(P, 1, 6);
 
-  // Merge and store.
+  // Merge and store this CTA's words.
   uint32_t* out = bitmask ? bitmask + row * bstride : nullptr;
   const int32_t eos_w = hd.eos >> 5;
   const uint32_t eos_bit = (!terminated && (hd.flags & 2)) ? (1u << (hd.eos & 31)) : 0u;
@@ -220,29 +254,29 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   if (tma) {
     mbar_wait(&rows_bar, 0);
     const int nr = s_nrows;
-    const uint4* univ = reinterpret_cast<const uint4*>(rows_s + (size_t)kTmaRows * row_bytes);
-    for (int32_t w4 = threadIdx.x; w4 < W4; w4 += blockDim.x) {
+    const uint4* univ = reinterpret_cast<const uint4*>(rows_s + (size_t)kTmaRows * part_bytes);
+    for (int32_t w4 = threadIdx.x; w4 < (nw >> 2); w4 += blockDim.x) {
       uint4 a = reinterpret_cast<const uint4*>(dep_acc)[w4];
       for (int k = 0; k < nr; ++k) {
-        const uint4 r = reinterpret_cast<const uint4*>(rows_s + (size_t)k * row_bytes)[w4];
+        const uint4 r = reinterpret_cast<const uint4*>(rows_s + (size_t)k * part_bytes)[w4];
         a.x |= r.x; a.y |= r.y; a.z |= r.z; a.w |= r.w;
       }
       const uint4 u = univ[w4];
       uint32_t v[4] = {a.x & u.x, a.y & u.y, a.z & u.z, a.w & u.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int32_t w = w4 * 4 + e;
+        const int32_t w = w_lo + w4 * 4 + e;
         if (w == eos_w) v[e] |= eos_bit;
         if (w == W - 1) v[e] &= tail;
         partial |= (v[e] != ((w == W - 1) ? tail : 0xFFFFFFFFu));
       }
       const uint4 fin = make_uint4(v[0], v[1], v[2], v[3]);
-      if (out) reinterpret_cast<uint4*>(out)[w4] = fin;
+      if (out) reinterpret_cast<uint4*>(out + w_lo)[w4] = fin;
       if (APPLY) reinterpret_cast<uint4*>(dep_acc)[w4] = fin;  // own slot only
     }
   } else {
-    for (int32_t w = threadIdx.x; w < W; w += blockDim.x) {
-      uint32_t a = dep_acc[w];
+    for (int32_t w = w_lo + threadIdx.x; w < w_hi; w += blockDim.x) {
+      uint32_t a = dep_acc[w - w_lo];
       for (int s = 0; s < nt; ++s) {
         const int32_t kk = s_key[s];
         if (kk >= 0) a |= __ldg(hd.acc_rows + (size_t)kk * W + w);
@@ -252,21 +286,32 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       if (w == W - 1) a &= tail;
       partial |= (a != ((w == W - 1) ? tail : 0xFFFFFFFFu));
       if (out) out[w] = a;
-      if (APPLY) dep_acc[w] = a;
+      if (APPLY) dep_acc[w - w_lo] = a;
     }
   }
   trace_mark(P, 1, 7);
+  unsigned long long t_merge = 0;
+  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_merge));
   if (need_apply || APPLY) {
     if (partial) s_partial = 1;
     __syncthreads();
-    if (need_apply && threadIdx.x == 0) need_apply[i] = (uint8_t)s_partial;
+    if (need_apply && threadIdx.x == 0) need_apply[i] = (uint8_t)s_partial;  // launched with one split
   }
-  if (APPLY && s_partial) apply_row(logits + row * lstride_bytes, dep_acc, ap_vocab, ap_eb, ap_neg);
+  if (APPLY && s_partial) {
+    const int64_t vocab = ap_vocab < (int64_t)W * 32 ? ap_vocab : (int64_t)W * 32;
+    const int64_t t_lo = (int64_t)w_lo * 32, t_hi = (int64_t)w_hi * 32 < vocab ? (int64_t)w_hi * 32 : vocab;
+    if (t_hi > t_lo) apply_row(logits + row * lstride_bytes, dep_acc, t_lo, t_hi, ap_eb, ap_neg);
+  }
   if (P.trace && threadIdx.x == 0) {
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    P.trace[64 + 2 * blockIdx.x] = t1 - t_start;
-    P.trace[64 + 2 * blockIdx.x + 1] = (unsigned long long)total | ((unsigned long long)nt << 32);
+    const int64_t c = (int64_t)i * n_split + split;
+    if (c < (int64_t)P.capacity) {
+      P.trace[64 + 3 * c] = t1 - t_start;
+      P.trace[64 + 3 * c + 1] = (unsigned long long)total | ((unsigned long long)nt << 32);
+      P.trace[64 + 3 * c + 2] = t_merge - t_start;
+    }
+    if (c == 0) P.trace[63] = (unsigned long long)n_split;
   }
 }
 
@@ -278,20 +323,38 @@ static gm_status fill_attrs() {
   return GM_OK;
 }
 
-static size_t fill_smem(int32_t Wmax) {
-  const size_t row_bytes = ((size_t)Wmax * 4 + 15) & ~(size_t)15;
-  return row_bytes + kStageBytes + (kTmaRows + 1) * row_bytes;
+// Splits per request: enough CTAs to cover the SMs once,
+// at most kMaxSplits; one when the caller wants the per-row need_apply flag.
+constexpr int kMaxSplits = 8;
+static int fill_splits(int32_t n, bool need_apply) {
+  if (need_apply) return 1;
+  int sms = 148;
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // one CTA per SM: the walkers' local state needs the L1 a second
+  // resident CTA would take (measured: two per SM is slower)
+  int s = sms / (n > 0 ? n : 1);
+  return s < 1 ? 1 : (s > kMaxSplits ? kMaxSplits : s);
+}
+
+static int32_t split_words(int32_t Wmax, int splits) { return ((Wmax + 3) / 4 + splits - 1) / splits * 4; }
+
+static size_t fill_smem(int32_t Wp) {
+  const size_t part = ((size_t)Wp * 4 + 15) & ~(size_t)15;
+  return part + kStageBytes + (kTmaRows + 1) * part;
 }
 
 gm_status launch_fill(const DevPool& P, const int32_t* slots, int32_t n, int32_t* bitmask, int64_t bstride,
                       const int32_t* rows, uint8_t* need_apply, int32_t Wmax, cudaStream_t s) {
   if (n <= 0) return GM_OK;
-  const size_t smem = fill_smem(Wmax);
+  const int splits = fill_splits(n, need_apply != nullptr);
+  const int32_t Wp = split_words(Wmax, splits);
+  const size_t smem = fill_smem(Wp);
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
   static gm_status attrs = fill_attrs<false>();
   if (attrs) return attrs;
-  fill_kernel<false><<<n, kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows,
-                                                   need_apply, Wmax, nullptr, 0, 0, 2, 0u);
+  fill_kernel<false><<<dim3(n, splits), kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask),
+                                                                 bstride, rows, need_apply, Wp, nullptr, 0, 0, 2, 0u);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }
@@ -301,13 +364,16 @@ gm_status launch_fill_apply(const DevPool& P, const int32_t* slots, int32_t n, i
                             const int32_t* rows, int32_t Wmax, void* logits, int32_t eb, uint32_t neg,
                             int64_t vocab, int64_t lstride_bytes, cudaStream_t s) {
   if (n <= 0) return GM_OK;
-  const size_t smem = fill_smem(Wmax);
+  const int splits = fill_splits(n, false);
+  const int32_t Wp = split_words(Wmax, splits);
+  const size_t smem = fill_smem(Wp);
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
   static gm_status attrs = fill_attrs<true>();
   if (attrs) return attrs;
-  fill_kernel<true><<<n, kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows,
-                                                  nullptr, Wmax, static_cast<char*>(logits), lstride_bytes, vocab,
-                                                  eb, neg);
+  fill_kernel<true><<<dim3(n, splits), kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask),
+                                                                bstride, rows, nullptr, Wp,
+                                                                static_cast<char*>(logits), lstride_bytes, vocab, eb,
+                                                                neg);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

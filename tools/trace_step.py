@@ -21,10 +21,10 @@ import bench  # noqa: E402
 import paper_2411_15100_b200 as gm  # noqa: E402
 from paper_2411_15100_b200 import _lib  # noqa: E402
 from paper_2411_15100_b200.engine import get_pool  # noqa: E402
-from paper_2411_15100_b200.matcher import batch_accept, batch_fill, batch_recycle  # noqa: E402
+from paper_2411_15100_b200.matcher import batch_accept, batch_fill, batch_fill_apply, batch_recycle  # noqa: E402
 
 
-def main(steps=12, flush=True):
+def main(steps=12, flush=True, fused=False):
     torch.cuda.set_device(0)
     vocab = gm.synth_vocab(128256)
     info = gm.TokenizerInfo.from_vocabulary(vocab)
@@ -39,20 +39,28 @@ def main(steps=12, flush=True):
     bitmask = torch.empty((B, (vocab.size + 31) // 32), dtype=torch.int32, device=dev)
     acc = torch.empty(B, dtype=torch.uint8, device=dev)
     fl = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
+    logits = torch.randn((B, vocab.size), dtype=torch.bfloat16, device=dev)
     NB = 64 + 3 * pool.capacity
     buf = (C.c_uint64 * NB)()
     lib = _lib.load()
     for s in range(steps):
         if flush:
             fl.zero_()
-        batch_fill(pool, slots, bitmask)
+        if fused:
+            batch_fill_apply(pool, slots, logits, bitmask)
+        else:
+            batch_fill(pool, slots, bitmask)
         torch.cuda.synchronize()
         _lib.check(lib.gm_pool_trace(pool.handle, buf, NB))
         f = [buf[16 + k] for k in range(8)]
-        cta = sorted(((buf[64 + 2 * i] / 1e3, buf[65 + 2 * i] & 0xFFFFFFFF, buf[65 + 2 * i] >> 32)
-                      for i in range(B)), reverse=True)
-        print(f"  fill per-CTA us: max {cta[0][0]:.2f} p50 {cta[B // 2][0]:.2f}  slowest (us, deps, tops): "
-              f"{[(round(a, 2), b, c) for a, b, c in cta[:4]]}")
+        ns = max(1, buf[63])
+        nc = B * ns
+        cta = sorted(((buf[64 + 3 * i] / 1e3, buf[66 + 3 * i] / 1e3, buf[65 + 3 * i] & 0xFFFFFFFF,
+                       buf[65 + 3 * i] >> 32) for i in range(nc)), reverse=True)
+        mrg = sorted(c[1] for c in cta)
+        print(f"  {'K3' if fused else 'K2'} x{ns} per-CTA us: max {cta[0][0]:.2f} p50 {cta[nc // 2][0]:.2f} | "
+              f"to-merge-done max {mrg[-1]:.2f} p50 {mrg[nc // 2]:.2f} | slowest (us, merge-us, deps, tops): "
+              f"{[(round(a, 2), round(m, 2), b, c) for a, m, b, c in cta[:4]]}")
         extra = f"deps={buf[24]} key0={C.c_int64(buf[25]).value} ntops={buf[26]}"
         if buf[24]:
             ln = buf[44] & 0xFFFF
@@ -81,4 +89,4 @@ def main(steps=12, flush=True):
 
 
 if __name__ == "__main__":
-    main(flush="--warm" not in sys.argv)
+    main(flush="--warm" not in sys.argv, fused="--fused" in sys.argv)

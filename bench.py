@@ -43,6 +43,54 @@ METRIC = "token-mask fill+apply µs/step (batch 128, 128k vocab); cache compile 
 UNIT = "us/step"
 STRUCTURAL = frozenset(b'{}[]",:0123456789 \n\t-.')
 
+# SURVEY §8d workloads.  "json" (config 3) is the headline; the others are
+# the same step on config 2's schema grammar and config 4's recursive
+# grammars (REF grammars.py:38-65), for tools/bench_configs.sh.
+SAMPLE_SCHEMA = {  # REF grammars.py:53-65
+    "type": "object",
+    "properties": {
+        "name": {"enum": ["get_weather", "get_time"]},
+        "unit": {"type": "string"},
+        "count": {"type": "integer"},
+        "tags": {"type": "array", "items": {"type": "string"}, "minItems": 1, "maxItems": 3},
+    },
+    "required": ["name", "count"],
+    "additionalProperties": False,
+}
+XML_TOY = r'''
+root    ::= element
+element ::= "<a>" item* "</a>" | "<b>" item* "</b>"
+item    ::= element | text
+text    ::= [a-z0-9 ]+
+'''
+ARITHMETIC = r'''
+root   ::= term (("+" | "-") term)*
+term   ::= factor (("*" | "/") factor)*
+factor ::= [0-9]+ | "(" root ")"
+'''
+# per grammar: structural byte set the sampler favours, forced-prefix token
+# (bytes) and its length (config 4: nesting depth >= 32 via "(" runs)
+WORKLOADS = {
+    "json": dict(config=3, structural=STRUCTURAL, force=None, desc="builtin ECMA-404 JSON grammar"),
+    "schema": dict(config=2, structural=STRUCTURAL, force=None,
+                   desc="JSON-schema function-call grammar (REF SAMPLE_SCHEMA via schema_to_grammar_text)"),
+    "xml": dict(config=4, structural=frozenset(b"<>/ab"), force=None, desc="XML_TOY recursive grammar"),
+    "arithmetic": dict(config=4, structural=frozenset(b"()+-*/0123456789"), force=(b"(", 40),
+                       desc="ARITHMETIC grammar, 40 forced '(' per request (nesting depth >= 32)"),
+}
+
+
+def grammar_text(name: str) -> str:
+    import paper_2411_15100_b200 as gm
+
+    if name == "json":
+        return gm.BUILTIN_JSON_GRAMMAR
+    if name == "schema":
+        from paper_2411_15100_b200.schema import schema_to_grammar_text
+
+        return schema_to_grammar_text(json.dumps(SAMPLE_SCHEMA))
+    return {"xml": XML_TOY, "arithmetic": ARITHMETIC}[name]
+
 
 # ---------------------------------------------------------------------------
 # deterministic sampler (device-agnostic integer arithmetic)
@@ -56,16 +104,25 @@ def _mix32(x: torch.Tensor) -> torch.Tensor:
     return (x ^ (x >> 16)) & m
 
 
-def structural_flags(vocab) -> np.ndarray:
-    return np.array([t != vocab.eos_id and 0 < len(tok) <= 3 and all(c in STRUCTURAL for c in tok)
+def structural_flags(vocab, chars=STRUCTURAL) -> np.ndarray:
+    return np.array([t != vocab.eos_id and 0 < len(tok) <= 3 and all(c in chars for c in tok)
                      for t, tok in enumerate(vocab.tokens)], dtype=bool)
 
 
+def forced_token(vocab, grammar: str):
+    """(token id, steps) of the workload's forced prefix, or None."""
+    f = WORKLOADS[grammar]["force"]
+    if f is None:
+        return None
+    return vocab.tokens.index(f[0]), f[1]
+
+
 def sample_tokens(allowed: torch.Tensor, structural: torch.Tensor, step: int, rows: torch.Tensor,
-                  seed: int = 1234) -> torch.Tensor:
+                  seed: int = 1234, force=None) -> torch.Tensor:
     """allowed: bool [B, V]; returns int64 [B].  score = hash(seed, step, row,
     token) plus 2^33 for structural tokens when the (step,row) coin says so;
-    argmax over allowed tokens."""
+    argmax over allowed tokens.  ``force`` = (token, steps): that token wins
+    (when allowed) for the first ``steps`` steps."""
     B, V = allowed.shape
     dev = allowed.device
     t = torch.arange(V, dtype=torch.int64, device=dev)
@@ -74,6 +131,8 @@ def sample_tokens(allowed: torch.Tensor, structural: torch.Tensor, step: int, ro
     h = _mix32((t.view(1, -1) * 0x27D4EB2F + r * 0x165667B1 + base) & 0xFFFFFFFF)
     coin = _mix32((r * 0x61C88647 + base + 7) & 0xFFFFFFFF) & 1
     score = h + (coin * structural.view(1, -1).to(torch.int64)) * (1 << 33)
+    if force is not None and step < force[1]:
+        score[:, force[0]] += 1 << 40
     score = torch.where(allowed, score, torch.full_like(score, -1))
     return score.argmax(dim=1)
 
@@ -138,6 +197,25 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def profiled_traffic(kernel_tag: str):
+    """dram read+write bytes per launch of a kernel from the newest committed
+    ncu --set full capture (profiles/<round>_traffic.json, written by
+    tools/summarize_profiles.py), or None."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    for path in reversed(files):
+        try:
+            with open(path) as fh:
+                d = json.load(fh)
+        except Exception:
+            continue
+        for k, v in d.items():
+            if k.endswith(kernel_tag):
+                return {"bytes": float(v), "source": os.path.relpath(path, ROOT)}
+    return None
+
+
 def measured_peak_hbm() -> tuple:
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -159,7 +237,9 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     vocab = gm.synth_vocab(args.vocab)
     V, W, B = vocab.size, (vocab.size + 31) // 32, args.batch
     info = gm.TokenizerInfo.from_vocabulary(vocab)
-    text = gm.BUILTIN_JSON_GRAMMAR
+    text = grammar_text(args.grammar)
+    wl = WORKLOADS[args.grammar]
+    force = forced_token(vocab, args.grammar)
 
     # compile: one cold (includes first-touch), then warm repeats; sharded over
     # the ranks (position sharding + NCCL all-gather) when world > 1
@@ -180,7 +260,7 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     matchers = [gm.GrammarMatcher(compiled, max_rollback_tokens=1) for _ in range(B)]
     slots = torch.tensor([m.slot for m in matchers], dtype=torch.int32, device=dev)
     rows = torch.arange(B, device=dev) + rank * B
-    structural = torch.from_numpy(structural_flags(vocab)).to(dev)
+    structural = torch.from_numpy(structural_flags(vocab, wl["structural"])).to(dev)
     bitmask = torch.empty((B, W), dtype=torch.int32, device=dev)
     n_ring = 8
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
@@ -229,7 +309,7 @@ def run_ours(args, rank: int, world: int, group) -> dict:
             allowed = unpack_allowed(bitmask, V)
             masked[s] = (~allowed).sum()
             mask_keep[s] = bitmask[:sample_rows]
-            toks = sample_tokens(allowed, structural, s, rows).to(torch.int32)
+            toks = sample_tokens(allowed, structural, s, rows, force=force).to(torch.int32)
             tok_hist[s] = toks
             e[2].record(stream)
             batch_accept(pool, slots, toks, accepted)
@@ -327,7 +407,7 @@ def cpu_baseline(args, ours: dict) -> dict:
 
     vocab = gm.synth_vocab(args.vocab)
     t0 = time.perf_counter()
-    b = compile_oracle_bundle(gm.BUILTIN_JSON_GRAMMAR, vocab)
+    b = compile_oracle_bundle(grammar_text(args.grammar), vocab)
     compile_s = time.perf_counter() - t0
     toks = ours["tokens"]
     keep = ours["mask_keep"]
@@ -392,16 +472,17 @@ def _cpu_name() -> str:
 _W_STATE = {}
 
 
-def _ref_worker_init(vocab_size, n_local, seed_rows):
+def _ref_worker_init(vocab_size, n_local, seed_rows, grammar="json"):
     import paper_2411_15100_b200 as gm
     from oracle import compile_oracle_bundle
     from oracle.matcher import OracleMatcher
 
     vocab = gm.synth_vocab(vocab_size)
-    b = compile_oracle_bundle(gm.BUILTIN_JSON_GRAMMAR, vocab)
+    b = compile_oracle_bundle(grammar_text(grammar), vocab)
     _W_STATE.update(vocab=vocab, b=b, rows=seed_rows,
                     ms=[OracleMatcher(b, history_window=1) for _ in seed_rows],
-                    structural=torch.from_numpy(structural_flags(vocab)))
+                    structural=torch.from_numpy(structural_flags(vocab, WORKLOADS[grammar]["structural"])),
+                    force=forced_token(vocab, grammar))
 
 
 def _ref_worker_step(step):
@@ -414,7 +495,7 @@ def _ref_worker_step(step):
     dt = time.perf_counter() - t0
     bm = torch.from_numpy(np.stack(words).view(np.int32))
     allowed = unpack_allowed(bm, vocab.size)
-    toks = sample_tokens(allowed, st["structural"], step, torch.tensor(st["rows"])).tolist()
+    toks = sample_tokens(allowed, st["structural"], step, torch.tensor(st["rows"]), force=st["force"]).tolist()
     for i, t in enumerate(toks):
         assert st["ms"][i].accept_token(t)
         if t == vocab.eos_id:
@@ -431,7 +512,8 @@ def run_reference(args) -> dict:
     chunks = [rows[i::nproc] for i in range(nproc)]
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
-    pools = [ctx.Pool(1, initializer=_ref_worker_init, initargs=(args.vocab, len(c), c)) for c in chunks]
+    pools = [ctx.Pool(1, initializer=_ref_worker_init, initargs=(args.vocab, len(c), c, args.grammar))
+             for c in chunks]
     for p in pools:
         p.apply(time.time)
     compile_s = time.perf_counter() - t0
@@ -468,11 +550,13 @@ def run_reference(args) -> dict:
 
 
 def _config(args, world: int) -> dict:
+    wl = WORKLOADS[args.grammar]
     return {
-        "workload": "builtin ECMA-404 JSON grammar, synth_vocab(128256) (REF synthvocab.py), "
+        "workload": f"{wl['desc']}, synth_vocab({args.vocab}) (REF synthvocab.py), "
                     f"batch {args.batch} requests/GPU, bf16 logits, structure-biased deterministic trajectories "
-                    "(BASELINE config 3)",
-        "grammar": "json_ecma404", "vocab": args.vocab, "global_batch": args.batch * world, "batch_per_gpu": args.batch,
+                    f"(BASELINE config {wl['config']})",
+        "grammar": "json_ecma404" if args.grammar == "json" else args.grammar, "vocab": args.vocab,
+        "global_batch": args.batch * world, "batch_per_gpu": args.batch,
         "parallelism": f"batch-sharded dp{world} (cache replicated)",
         "l2": "flushed before every step (256 MiB write); logits ring 8 x 32.8 MB",
     }
@@ -486,6 +570,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--vocab", type=int, default=128256)
+    ap.add_argument("--grammar", default="json", choices=sorted(WORKLOADS),
+                    help="SURVEY §8d workload: json = config 3 (default, the headline)")
     ap.add_argument("--cpu-steps", type=int, default=24)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -519,6 +605,7 @@ def main():
         dense = B * (4 * W + 2 * V)
         achieved = algo_bytes / (r["step_us"] * 1e-6) / 1e9
         k0_bytes = B * 4 * W + 2 * r["masked_mean"]  # K0 alone: bitmask read + -inf writes
+        traffic = profiled_traffic("k3_fused_fill_apply") if args.grammar == "json" else None
         out = {
             "metric": METRIC,
             "value": r["step_us"],
@@ -546,7 +633,10 @@ def main():
             "k0_apply_gbs": k0_bytes / (r["apply_us"] * 1e-6) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "fill_kernel<true> (K3 fused fill+apply)", "achieved": achieved,
                          "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "algorithmic_bytes_per_launch": algo_bytes},
+                         "traffic": traffic["bytes"] if traffic else None,
+                         "traffic_source": (traffic["source"] + " (dram read+write of one cold ncu replay; the "
+                                            "-inf stores stay dirty in L2 past the kernel's end)") if traffic else None,
+                         "algorithmic_bytes_per_launch": algo_bytes},
             "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": B,
                     "path": "BatchGrammarMatcher.batch_fill_and_apply + batch accept + recycle (pinned token ids "
                             "H2D, accepted flags D2H)"},

@@ -24,18 +24,19 @@ from paper_2411_15100_b200.engine import get_pool  # noqa: E402
 from paper_2411_15100_b200.matcher import batch_accept, batch_fill, batch_fill_apply, batch_recycle  # noqa: E402
 
 
-def main(steps=12, flush=True, fused=False):
+def main(steps=12, flush=True, fused=False, grammar="json"):
     torch.cuda.set_device(0)
     vocab = gm.synth_vocab(128256)
     info = gm.TokenizerInfo.from_vocabulary(vocab)
-    compiled = gm.GrammarCompiler(info).compile_builtin_json_grammar()
+    compiled = gm.GrammarCompiler(info).compile_grammar(bench.grammar_text(grammar))
     pool = get_pool()
     B = 128
     ms = [gm.GrammarMatcher(compiled, max_rollback_tokens=1) for _ in range(B)]
     dev = pool.device
     slots = torch.tensor([m.slot for m in ms], dtype=torch.int32, device=dev)
     rows = torch.arange(B, device=dev)
-    structural = torch.from_numpy(bench.structural_flags(vocab)).to(dev)
+    structural = torch.from_numpy(bench.structural_flags(vocab, bench.WORKLOADS[grammar]["structural"])).to(dev)
+    force = bench.forced_token(vocab, grammar)
     bitmask = torch.empty((B, (vocab.size + 31) // 32), dtype=torch.int32, device=dev)
     acc = torch.empty(B, dtype=torch.uint8, device=dev)
     fl = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
@@ -69,7 +70,7 @@ def main(steps=12, flush=True, fused=False):
             for b in range(13):
                 buf[32 + b] = 0
         allowed = bench.unpack_allowed(bitmask, vocab.size)
-        toks = bench.sample_tokens(allowed, structural, s, rows).to(torch.int32)
+        toks = bench.sample_tokens(allowed, structural, s, rows, force=force).to(torch.int32)
         if flush:
             fl.zero_()
         torch.cuda.synchronize()
@@ -89,4 +90,5 @@ def main(steps=12, flush=True, fused=False):
 
 
 if __name__ == "__main__":
-    main(flush="--warm" not in sys.argv, fused="--fused" in sys.argv)
+    g = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--grammar=")), "json")
+    main(flush="--warm" not in sys.argv, fused="--fused" in sys.argv, grammar=g)

@@ -344,29 +344,57 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     apply_ms = [evB[s][1].elapsed_time(evB[s][2]) for s in range(W0, S)]
     sep_ms = [evB[s][0].elapsed_time(evB[s][2]) for s in range(W0, S)]
 
-    # pass C — e2e through the public API with host buffers (same trajectories)
+    # pass C — e2e through the public API with host buffers (same
+    # trajectories): per decode step ONE call, BatchGrammarMatcher.batch_step
+    # = accept the previous step's sampled tokens (pinned host ids copied
+    # H2D), restart finished requests, fill + apply this step's masks (K5,
+    # one launch), then the accepted flags D2H
     for m in matchers:
         m.reset()
     batch = gm.BatchGrammarMatcher()
     pinned_toks = torch.from_numpy(toks_h.copy()).pin_memory()
-    pinned_out = torch.empty((S, B), dtype=torch.uint8).pin_memory()
+    pinned_out = torch.zeros((S, B), dtype=torch.uint8).pin_memory()
     dev_toks = torch.empty(B, dtype=torch.int32, device=dev)
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
+    e2e_mism = torch.zeros((), dtype=torch.int64, device=dev)
     sync_ranks()
     for s in range(S):
         if not args.no_flush:
             flush.zero_()
         logits = ring[s % n_ring]
         e2e_ev[s][0].record(stream)
+        if s > 0:
+            dev_toks.copy_(pinned_toks[s - 1], non_blocking=True)
+        batch.batch_step(matchers, dev_toks if s > 0 else None, bitmask=bitmask, logits=logits, recycle=True,
+                         accepted=accepted)
+        if s > 0:
+            pinned_out[s - 1].copy_(accepted, non_blocking=True)
+        e2e_ev[s][1].record(stream)
+        e2e_ev[s][1].synchronize()
+        e2e_mism += (bitmask[:sample_rows] != mask_keep[s]).any(dim=1).sum()
+    e2e_ms = [e2e_ev[s][0].elapsed_time(e2e_ev[s][1]) for s in range(W0, S)]
+    all_acc = bool(pinned_out[W0:S - 1].bool().all())
+    e2e_mask_mismatches = int(e2e_mism)
+
+    # pass D — the same e2e as separate public calls (fill+apply, accept,
+    # recycle), for comparison
+    for m in matchers:
+        m.reset()
+    e2e2_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
+    sync_ranks()
+    for s in range(S):
+        if not args.no_flush:
+            flush.zero_()
+        logits = ring[s % n_ring]
+        e2e2_ev[s][0].record(stream)
         batch.batch_fill_and_apply(matchers, logits, bitmask)
         dev_toks.copy_(pinned_toks[s], non_blocking=True)
         batch_accept(pool, slots, dev_toks, accepted)
         batch_recycle(pool, slots)
         pinned_out[s].copy_(accepted, non_blocking=True)
-        e2e_ev[s][1].record(stream)
-        e2e_ev[s][1].synchronize()
-    e2e_ms = [e2e_ev[s][0].elapsed_time(e2e_ev[s][1]) for s in range(W0, S)]
-    all_acc = bool(pinned_out[W0:].bool().all())
+        e2e2_ev[s][1].record(stream)
+        e2e2_ev[s][1].synchronize()
+    e2e_sep_ms = [e2e2_ev[s][0].elapsed_time(e2e2_ev[s][1]) for s in range(W0, S)]
 
     def mx(v):
         t = torch.tensor([v], dtype=torch.float64, device=dev)
@@ -381,6 +409,8 @@ def run_ours(args, rank: int, world: int, group) -> dict:
         "apply_us": mx(statistics.fmean(apply_ms) * 1e3),
         "accept_us": mx(statistics.fmean(acc_ms) * 1e3),
         "e2e_us": mx(statistics.fmean(e2e_ms) * 1e3),
+        "e2e_separate_us": mx(statistics.fmean(e2e_sep_ms) * 1e3),
+        "e2e_mask_mismatches": e2e_mask_mismatches,
         "step_us_median": statistics.median(step_ms) * 1e3,
         "compile_ms": mx(statistics.median(compile_ms)),
         "compile_split_ms": compile_split,
@@ -638,8 +668,11 @@ def main():
                                             "-inf stores stay dirty in L2 past the kernel's end)") if traffic else None,
                          "algorithmic_bytes_per_launch": algo_bytes},
             "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": B,
-                    "path": "BatchGrammarMatcher.batch_fill_and_apply + batch accept + recycle (pinned token ids "
-                            "H2D, accepted flags D2H)"},
+                    "path": "BatchGrammarMatcher.batch_step per decode step: accept previous tokens (pinned ids H2D) "
+                            "+ recycle + fill + apply in one launch (K5), accepted flags D2H",
+                    "mask_mismatches_vs_pass_A": r["e2e_mask_mismatches"],
+                    "separate_calls_us": r["e2e_separate_us"],
+                    "separate_calls_path": "batch_fill_and_apply (K3) + batch accept (K4) + recycle, same copies"},
             "gpu_launches": args.steps,
             "clocks": r["clocks"],
             "all_accepted": r["all_accepted"],

@@ -220,6 +220,24 @@ gm_status gm_fill_apply_tokens(gm_pool* p, const int32_t* slots, int32_t n,
                                int64_t vocab_size, int64_t logits_stride,
                                void* stream);
 
+/* K5: one decode step per request — accept, then fill (+ apply).  For
+ * i < n: if token_ids is non-null, accept token_ids[i] on slots[i] exactly as
+ * gm_accept_tokens (accepted_out[i] = 1/0; a rejected token leaves the state
+ * unchanged); with recycle_terminated != 0 a request that terminates is
+ * restarted at the grammar's start state (gm_pool_recycle); then fill the
+ * slot's next mask exactly as gm_fill_tokens into bitmask[row] (nullable when
+ * logits is given) and, when logits is non-null, apply it to logits[row] as
+ * gm_fill_apply_tokens.  A request that terminated in this step (and is not
+ * recycled) gets an all-zero row and no error.  Replaces the accept_token ->
+ * fill_next_token_bitmask pair of a decode loop (REF matcher.py:273, 377)
+ * with one launch. */
+gm_status gm_step_tokens(gm_pool* p, const int32_t* slots, int32_t n,
+                         const int32_t* token_ids, uint8_t* accepted_out,
+                         int32_t recycle_terminated, int32_t* bitmask,
+                         int64_t bitmask_stride, const int32_t* rows,
+                         void* logits, int32_t dtype, int64_t vocab_size,
+                         int64_t logits_stride, void* stream);
+
 /* rollback `steps` acceptances of each slot (REF matcher.py:310-326);
  * slots/steps are device int32[n]. */
 gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps,

@@ -49,7 +49,7 @@ enum : uint32_t {
 struct BlobHdr {
   int32_t bytes, n_classes, n_nodes, o_bc;
   int32_t o_flags, o_toff, o_trans, o_pool;
-  int32_t o_kon, o_rule, o_ninfo, o_fast, o_callers, pad[3];
+  int32_t o_kon, o_rule, o_ninfo, o_fast, o_callers, start_node, pad[2];
 };
 static_assert(sizeof(BlobHdr) == 64, "BlobHdr layout");
 
@@ -78,6 +78,7 @@ __device__ __forceinline__ DevGrammar blob_view(const uint8_t* base) {
   DevGrammar g{};
   g.n_classes = h->n_classes;
   g.n_nodes = h->n_nodes;
+  g.start_node = h->start_node;
   g.byte_class = base + h->o_bc;
   g.node_flags = base + h->o_flags;
   g.trans_off = reinterpret_cast<const int32_t*>(base + h->o_toff);
@@ -829,6 +830,17 @@ __device__ inline void store_header(const DevPool& P, int32_t slot, const SlotHd
   int4* dst = reinterpret_cast<int4*>(P.hdr + slot);
 #pragma unroll
   for (int i = 0; i < kHdrVec; ++i) dst[i] = src[i];
+}
+
+// Publish the state part of a header (everything after the binding pointers
+// and sizes, which never change for a slot) with 16-byte stores.
+constexpr int kHdrStateVec = 3;  // first int4 holding state (ntops at byte 56)
+static_assert(offsetof(SlotHdr, ntops) >= kHdrStateVec * 16, "header state offset");
+__device__ inline void store_header_state(const DevPool& P, int32_t slot, const SlotHdr& h) {
+  const int4* src = reinterpret_cast<const int4*>(&h);
+  int4* dst = reinterpret_cast<int4*>(P.hdr + slot);
+#pragma unroll
+  for (int i = kHdrStateVec; i < kHdrVec; ++i) dst[i] = src[i];
 }
 
 // Rebuild a slot header from the binding (reset / recycle / rollback path).

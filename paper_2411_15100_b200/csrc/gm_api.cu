@@ -29,6 +29,8 @@ gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t
                       uint8_t*, int32_t, cudaStream_t);
 gm_status launch_fill_apply(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*, int32_t,
                             void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
+gm_status launch_step(const DevPool&, const int32_t*, int32_t, const int32_t*, uint8_t*, int32_t, int32_t*, int64_t,
+                      const int32_t*, int32_t, void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_accept_tokens(const DevPool&, const int32_t*, const int32_t*, int32_t, uint8_t*, cudaStream_t);
 gm_status launch_accept_bytes(const DevPool&, int32_t, const uint8_t*, int64_t, uint8_t*, cudaStream_t);
 gm_status launch_reset(const DevPool&, int32_t, const DevBinding*, int32_t, int32_t, cudaStream_t);
@@ -321,6 +323,7 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
   bh.o_ninfo = 0;
   bh.o_fast = (int32_t)o_fast;
   bh.o_callers = (int32_t)o_callers;
+  bh.start_node = t->start_node;
   std::memcpy(blob.data(), &bh, sizeof(bh));
   gm_grammar* g = new gm_grammar();
   gm_status st;
@@ -660,6 +663,28 @@ gm_status gm_fill_apply_tokens(gm_pool* p, const int32_t* slots, int32_t n, int3
     return fail(GM_ERR_INVALID, "fused fill+apply needs 16-byte aligned logits rows");
   return launch_fill_apply(p->dev, slots, n, bitmask, bitmask_stride, rows, p->max_w, logits, eb, neg, vocab_size,
                            logits_stride * eb, as_stream(stream));
+}
+
+gm_status gm_step_tokens(gm_pool* p, const int32_t* slots, int32_t n, const int32_t* token_ids, uint8_t* accepted_out,
+                         int32_t recycle_terminated, int32_t* bitmask, int64_t bitmask_stride, const int32_t* rows,
+                         void* logits, int32_t dtype, int64_t vocab_size, int64_t logits_stride, void* stream) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  if (token_ids && !accepted_out) return fail(GM_ERR_INVALID, "accepted_out is required with token_ids");
+  if (!bitmask && !logits) return fail(GM_ERR_INVALID, "need a bitmask and/or logits");
+  int32_t eb = 2;
+  uint32_t neg = 0;
+  if (logits) {
+    switch (dtype) {
+      case GM_DTYPE_F32: eb = 4; neg = 0xFF800000u; break;
+      case GM_DTYPE_F16: eb = 2; neg = 0xFC00FC00u; break;
+      case GM_DTYPE_BF16: eb = 2; neg = 0xFF80FF80u; break;
+      default: return fail(GM_ERR_INVALID, "unknown dtype");
+    }
+    if (reinterpret_cast<uintptr_t>(logits) % 16 || (logits_stride * eb) % 16)
+      return fail(GM_ERR_INVALID, "fused step+apply needs 16-byte aligned logits rows");
+  }
+  return launch_step(p->dev, slots, n, token_ids, accepted_out, recycle_terminated, bitmask, bitmask_stride, rows,
+                     p->max_w, logits, eb, neg, vocab_size, logits_stride * eb, as_stream(stream));
 }
 
 gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps, int32_t n, void* stream) {

@@ -12,154 +12,11 @@
 // the new header are written.  Dedupe by (handle, node) is dedupe by stack
 // content because the arena is hash-consed (REF matcher.py:202-206).  A
 // rejected token leaves the slot unchanged (REF matcher.py:267-268).
-#include "device.cuh"
+#include "accept.cuh"
 
 namespace gm {
 
-constexpr int kAccS = 32;
-constexpr int kAccF = 160;
-constexpr int kAccThreads = 32;
-constexpr int kAccR = 4;    // stacks held in registers by the fast walker
-constexpr int kAccRF = 48;  // its walker-local frames
-
-// Current (handle, node) set of a slot: from the header when it fits, else
-// from the ring.
-__device__ int load_tops(const DevPool& P, int32_t slot, const SlotHdr& hdr, int2* out) {
-  if (hdr.ntops >= 0) {
-    for (int s = 0; s < hdr.ntops; ++s) out[s] = hdr.top[s];
-    return hdr.ntops;
-  }
-  const int32_t h = P.head[slot];
-  const int n = P.meta[(size_t)slot * P.H + h] & 0xFFFF;
-  const int2* tops = slot_tops(P, slot, h);
-  for (int s = 0; s < n; ++s) out[s] = tops[s];
-  return n;
-}
-
-// Append (refs, nodes) as the next ring entry and publish the new header.
-// `hdr` supplies the binding pointers; `topkeys` the arena keys of the tops
-// when known.
-// Ring position of a slot (head, history length, window), prefetched by
-// lanes 1..3 at kernel entry so the append does not wait on them.
-struct RingPos {
-  int32_t head, hist_len, window;
-};
-
-__device__ __forceinline__ void prefetch_ring(const DevPool& P, int32_t slot, RingPos* rp) {
-  if (threadIdx.x == 1) rp->head = P.head[slot];
-  if (threadIdx.x == 2) rp->hist_len = P.hist_len[slot];
-  if (threadIdx.x == 3) rp->window = P.window[slot];
-}
-
-// Append (handle, node) tops as the next ring entry and publish the new
-// header state.  The binding pointers of the global header are unchanged, so
-// only its state fields are rewritten in place.
-__device__ void push_tops(const DevPool& P, int32_t slot, const RingPos& rp, const DevGrammar& G, const int2* tops,
-                          int nt, int terminated, const Chain& c) {
-  const int32_t nh = (rp.head + 1) % P.H;
-  int2* dst = slot_tops(P, slot, nh);
-  for (int s = 0; s < nt; ++s) dst[s] = tops[s];
-  P.meta[(size_t)slot * P.H + nh] = nt | (terminated << 16);
-  P.head[slot] = nh;
-  const int32_t hl = rp.hist_len + 1;
-  P.hist_len[slot] = hl < rp.window ? hl : rp.window;
-  header_state(P, P.hdr[slot], G, tops, nt, terminated, &c);
-}
-
-__device__ void push_history(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr,
-                             const DevGrammar& G, int nt, const int32_t* refs, const int32_t* nodes, int terminated,
-                             const int32_t* fh, const unsigned long long* fk, int nfresh) {
-  int2 loc[kAccS];
-  for (int s = 0; s < nt; ++s) {
-    const int32_t r = refs[s];
-    loc[s] = make_int2(r == -1 ? -1 : -2 - r, nodes[s]);
-  }
-  Chain c;
-  build_chain(c, nt > 0 ? loc[0].x : -1, fh, fk, nfresh, hdr);
-  push_tops(P, slot, rp, G, loc, nt, terminated, c);
-}
-
-// Shared by token and byte-string acceptance (lane 0 only).  byte(i) gives
-// the i-th input byte; is_eos = EOS token.  Returns 1 if accepted.
-template <class ByteFn>
-__device__ int accept_one(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr, const DevGrammar& G,
-                          int64_t len, ByteFn byte, bool is_eos, bool reject_token) {
-  if (hdr.flags & 1) {  // REF matcher.py:276-277 "matcher is terminated"
-    atomicOr(P.err, kErrTerminated);
-    return 0;
-  }
-  int2 tops[kAccS];
-  const int ntops = load_tops(P, slot, hdr, tops);
-  if (is_eos) {  // REF matcher.py:280-288
-    if (!(hdr.flags & 2)) return 0;
-    Chain c;
-    build_chain(c, ntops > 0 ? tops[0].x : -1, nullptr, nullptr, 0, hdr);
-    push_tops(P, slot, rp, G, tops, ntops, 1, c);
-    return 1;
-  }
-  if (reject_token) return 0;  // special or empty token (REF matcher.py:289-293)
-  // fast path: register walker (<= kAccR stacks)
-  if (ntops <= kAccR) {
-    RWalker<kAccR, kAccRF> rw;
-    rw.init(hdr.chain_h, hdr.chain_k, hdr.nchain);
-    for (int s = 0; s < ntops; ++s) rw.add(rw.ref_of_handle(tops[s].x), tops[s].y);
-    for (int64_t i = 0; i < len && rw.n > 0 && !rw.spill; ++i) {
-      bool pb = false;
-      rw.step(G, P.arena, byte(i), &pb);
-    }
-    trace_mark(P, 0, 3);
-    if (!rw.spill) {
-      if (rw.err) {
-        atomicOr(P.err, rw.err);
-        return 0;
-      }
-      if (rw.n == 0) return 0;
-      int2 out[kAccR];
-      Chain c;
-      const int nout = rwalker_commit(rw, P.arena, out, c);
-      if (nout < 0) {
-        atomicOr(P.err, kErrArena);
-        return 0;
-      }
-      trace_mark(P, 0, 4);
-      push_tops(P, slot, rp, G, out, nout, 0, c);
-      trace_mark(P, 0, 5);
-      return 1;
-    }
-  }
-  // general path: any number of stacks / frames
-  Walker<kAccS, kAccF> w;
-  w.reset();
-  w.external(hdr.chain_h, hdr.chain_k, hdr.nchain);
-  for (int s = 0; s < ntops; ++s) w.add(tops[s].x < 0 ? -1 : -2 - tops[s].x, tops[s].y);
-  for (int64_t i = 0; i < len; ++i) {
-    if (w.nf > kAccF / 2) {
-      if (!w.intern_all(P.arena)) break;
-    }
-    bool pb = false;
-    if (!w.template step<kAccS>(G, P.arena, byte(i), &pb)) break;
-  }
-  trace_mark(P, 0, 3);
-  if (w.err) {
-    atomicOr(P.err, w.err);
-    return 0;
-  }
-  if (w.n == 0) return 0;
-  if (!w.intern_all(P.arena)) {
-    atomicOr(P.err, w.err | kErrArena);
-    return 0;
-  }
-  trace_mark(P, 0, 4);
-  if (w.n > P.max_stacks) {
-    atomicOr(P.err, kErrCap);
-    return 0;
-  }
-  push_history(P, slot, rp, hdr, G, w.n, w.ref, w.node, 0, w.kh, w.kk, w.nk);
-  trace_mark(P, 0, 5);
-  return 1;
-}
-
-__global__ void __launch_bounds__(kAccThreads)
+__global__ void __maxnreg__(128)
 accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t* __restrict__ token_ids, int32_t n,
                      uint8_t* __restrict__ accepted) {
   extern __shared__ __align__(16) uint8_t tables[];
@@ -191,7 +48,7 @@ accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t
                                     tid == hd.eos, e.x != 0);
 }
 
-__global__ void __launch_bounds__(kAccThreads)
+__global__ void __maxnreg__(128)
 accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len, uint8_t* accepted) {
   extern __shared__ __align__(16) uint8_t tables[];
   __shared__ SlotHdr hd;

@@ -22,7 +22,7 @@
 //      ancestor chain), setting bits of a shared-memory row;
 //   4. rows, dependent bits and universe are merged from shared memory and
 //      stored with 128-bit stores.
-#include "device.cuh"
+#include "accept.cuh"
 
 namespace gm {
 
@@ -69,11 +69,23 @@ __device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_
 // logits row.  Header and tables are read by every CTA of the request (one
 // round trip each, L2-shared); everything proportional to the vocabulary
 // shrinks by the split factor, so small batches still fill the 148 SMs.
-template <bool APPLY>
-__global__ void __launch_bounds__(kFillThreads)
+// Fused step (ACCEPT): before the fill, thread 0 accepts the request's
+// sampled token (K4 semantics, new state written straight into the shared
+// header) and optionally restarts a request that just terminated; the fill
+// then runs from that state — one launch and one header/table load per
+// decode step instead of two.
+struct StepArgs {
+  const int32_t* tokens;  // null: no accept (first step)
+  uint8_t* accepted;
+  int32_t recycle;
+};
+
+template <bool APPLY, bool ACCEPT>
+__global__ void __maxnreg__(128)
 fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
             int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wp,
-            char* __restrict__ logits, int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg) {
+            char* __restrict__ logits, int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg,
+            StepArgs SA) {
   extern __shared__ __align__(16) uint8_t smem[];
   const size_t part_bytes = ((size_t)Wp * 4 + 15) & ~(size_t)15;
   uint32_t* dep_acc = reinterpret_cast<uint32_t*>(smem);  // [Wp] this CTA's words
@@ -94,8 +106,38 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   const int32_t slot = __ldg(slots + i);
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   load_header(P, slot, &hd);
+  __shared__ RingPos rp;
+  __shared__ int4 s_rec[2];
+  __shared__ int s_just_term;
+  int32_t tok = -1;
+  if (ACCEPT && SA.tokens) {
+    prefetch_ring(P, slot, &rp);
+    tok = __ldg(SA.tokens + i);
+  }
   __syncthreads();
   trace_mark(P, 1, 1);
+  DevGrammar Gs{};
+  if (ACCEPT && SA.tokens) {  // launched with one split: one accept per request
+    const bool in_range = tok >= 0 && tok < hd.V;
+    if (threadIdx.x < 2 && in_range) s_rec[threadIdx.x] = __ldg(hd.tokrec + 2 * (size_t)tok + threadIdx.x);
+    Gs = stage_blob(hd.blob, hd.blob_bytes, tables);  // barrier inside
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      const bool was_term = hd.flags & 1;
+      if (!in_range) {  // REF matcher.py:278-279
+        atomicOr(P.err, kErrInvalid);
+      } else {
+        const int4 e = s_rec[0], inl = s_rec[1];
+        const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;
+        acc = accept_one(P, slot, rp, hd, Gs, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
+                         tok == hd.eos, e.x != 0, &hd);
+      }
+      SA.accepted[i] = (uint8_t)acc;
+      s_just_term = !was_term && (hd.flags & 1);
+      if (SA.recycle && (hd.flags & 1)) restart_slot(P, slot, Gs, &hd);
+    }
+    __syncthreads();
+  }
   const int32_t W = hd.W;
   const int32_t per = ((W + 3) / 4 + n_split - 1) / n_split * 4;  // words per split
   const int32_t w_lo = min(W, split * per), w_hi = min(W, w_lo + per), nw = w_hi - w_lo;
@@ -104,8 +146,8 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   if (threadIdx.x == 0) {
     s_partial = 0;
     int nt = hd.ntops;
-    if (terminated) {
-      if (split == 0) atomicOr(P.err, kErrTerminated);
+    if (terminated) {  // a request that terminated in this very step gets an empty row, no error
+      if (split == 0 && !(ACCEPT && SA.tokens && s_just_term)) atomicOr(P.err, kErrTerminated);
       nt = 0;
     } else if (nt >= 0) {
       // issue the row copies first: they are the longest-latency loads
@@ -159,7 +201,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     P.trace[16 + 10] = (unsigned long long)nt;
   }
   if (total) {
-    const DevGrammar G = stage_blob(hd.blob, hd.blob_bytes, tables);
+    const DevGrammar G = (ACCEPT && SA.tokens) ? Gs : stage_blob(hd.blob, hd.blob_bytes, tables);
     // caller index of each top's parent frame within the callers of the
     // top's rule: selects the dependents' one-level context class
     if ((int)threadIdx.x < nt) {
@@ -315,11 +357,12 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   }
 }
 
-template <bool APPLY>
+template <bool APPLY, bool ACCEPT>
 static gm_status fill_attrs() {
-  GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel<APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel<APPLY, ACCEPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   220 * 1024));
   // small shared carveout: the dependent walkers' local state must hit L1
-  GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel<APPLY>, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
+  GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel<APPLY, ACCEPT>, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
   return GM_OK;
 }
 
@@ -351,10 +394,11 @@ gm_status launch_fill(const DevPool& P, const int32_t* slots, int32_t n, int32_t
   const int32_t Wp = split_words(Wmax, splits);
   const size_t smem = fill_smem(Wp);
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
-  static gm_status attrs = fill_attrs<false>();
+  static gm_status attrs = fill_attrs<false, false>();
   if (attrs) return attrs;
-  fill_kernel<false><<<dim3(n, splits), kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask),
-                                                                 bstride, rows, need_apply, Wp, nullptr, 0, 0, 2, 0u);
+  fill_kernel<false, false><<<dim3(n, splits), kFillThreads, smem, s>>>(
+      P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows, need_apply, Wp, nullptr, 0, 0, 2, 0u,
+      StepArgs{nullptr, nullptr, 0});
   GM_LAUNCH_CHECK();
   return GM_OK;
 }
@@ -368,12 +412,38 @@ gm_status launch_fill_apply(const DevPool& P, const int32_t* slots, int32_t n, i
   const int32_t Wp = split_words(Wmax, splits);
   const size_t smem = fill_smem(Wp);
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
-  static gm_status attrs = fill_attrs<true>();
+  static gm_status attrs = fill_attrs<true, false>();
   if (attrs) return attrs;
-  fill_kernel<true><<<dim3(n, splits), kFillThreads, smem, s>>>(P, slots, n, reinterpret_cast<uint32_t*>(bitmask),
-                                                                bstride, rows, nullptr, Wp,
-                                                                static_cast<char*>(logits), lstride_bytes, vocab, eb,
-                                                                neg);
+  fill_kernel<true, false><<<dim3(n, splits), kFillThreads, smem, s>>>(
+      P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows, nullptr, Wp, static_cast<char*>(logits),
+      lstride_bytes, vocab, eb, neg, StepArgs{nullptr, nullptr, 0});
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+
+// K5: accept the sampled tokens, then fill (and, with logits, apply) the next
+// masks — one launch per decode step.  One CTA per request (no splits: the
+// accept must run once per request).
+gm_status launch_step(const DevPool& P, const int32_t* slots, int32_t n, const int32_t* tokens, uint8_t* accepted,
+                      int32_t recycle, int32_t* bitmask, int64_t bstride, const int32_t* rows, int32_t Wmax,
+                      void* logits, int32_t eb, uint32_t neg, int64_t vocab, int64_t lstride_bytes, cudaStream_t s) {
+  if (n <= 0) return GM_OK;
+  const size_t smem = fill_smem(split_words(Wmax, 1));
+  if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
+  const StepArgs sa{tokens, accepted, recycle};
+  uint32_t* bm = reinterpret_cast<uint32_t*>(bitmask);
+  if (logits) {
+    static gm_status attrs = fill_attrs<true, true>();
+    if (attrs) return attrs;
+    fill_kernel<true, true><<<dim3(n, 1), kFillThreads, smem, s>>>(P, slots, n, bm, bstride, rows, nullptr,
+                                                                   split_words(Wmax, 1), static_cast<char*>(logits),
+                                                                   lstride_bytes, vocab, eb, neg, sa);
+  } else {
+    static gm_status attrs = fill_attrs<false, true>();
+    if (attrs) return attrs;
+    fill_kernel<false, true><<<dim3(n, 1), kFillThreads, smem, s>>>(P, slots, n, bm, bstride, rows, nullptr,
+                                                                    split_words(Wmax, 1), nullptr, 0, 0, 2, 0u, sa);
+  }
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

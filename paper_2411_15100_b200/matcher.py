@@ -287,6 +287,26 @@ class BatchGrammarMatcher:
             return
         batch_fill_apply(get_pool(), self._slots(matchers), logits, bitmask, vocab_size=vocab_size)
 
+    def batch_step(self, matchers: Sequence[GrammarMatcher], tokens=None, *, bitmask: Optional[torch.Tensor] = None,
+                   logits: Optional[torch.Tensor] = None, recycle: bool = False,
+                   accepted: Optional[torch.Tensor] = None) -> Optional[torch.Tensor]:
+        """One decode step in one kernel (K5): accept ``tokens`` (int32 CUDA
+        tensor or list; None on the first step), optionally restart finished
+        requests, then fill the next masks into ``bitmask`` and/or apply
+        them to ``logits`` in place.  Equivalent to batch_accept_token +
+        (recycle) + batch_fill_next_token_bitmask [+ apply].  Returns the
+        uint8 accepted flags on the device (or None without tokens)."""
+        if not matchers:
+            return None
+        slots = self._slots(matchers)
+        if tokens is not None and not isinstance(tokens, torch.Tensor):
+            tokens = torch.tensor(list(tokens), dtype=torch.int32).to(slots.device, non_blocking=True)
+        if tokens is not None and accepted is None:
+            accepted = torch.empty(len(matchers), dtype=torch.uint8, device=slots.device)
+        batch_step(get_pool(), slots, tokens, accepted if tokens is not None else None, bitmask, logits,
+                   recycle=recycle)
+        return accepted if tokens is not None else None
+
     @staticmethod
     def batch_accept_token(matchers: Sequence[GrammarMatcher], tokens: Sequence[int],
                            debug_print: bool = False) -> List[bool]:
@@ -322,6 +342,30 @@ def batch_fill_apply(pool: MatcherPool, slots: torch.Tensor, logits: torch.Tenso
         bitmask.data_ptr() if bitmask is not None else None, bitmask.stride(0) if bitmask is not None else 0,
         rows.data_ptr() if rows is not None else None, logits.data_ptr(), _DTYPES[logits.dtype], v,
         logits.stride(0), _lib.stream_ptr(stream)), "gm_fill_apply_tokens")
+
+
+def batch_step(pool: MatcherPool, slots: torch.Tensor, tokens: Optional[torch.Tensor], accepted: Optional[torch.Tensor],
+               bitmask: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None,
+               rows: Optional[torch.Tensor] = None, recycle: bool = False, vocab_size: Optional[int] = None,
+               stream=None) -> None:
+    """K5, one launch per decode step: accept ``tokens`` (int32 CUDA, or None
+    for the first step) into ``accepted`` (uint8 CUDA), optionally restart
+    requests that terminated, then fill the next masks into ``bitmask``
+    and/or apply them to ``logits`` in place."""
+    from .bitmask import _DTYPES
+
+    if logits is not None and (logits.dtype not in _DTYPES or logits.dim() != 2 or logits.stride(-1) != 1):
+        raise ValueError("logits must be a 2-D fp32/fp16/bf16 CUDA tensor, contiguous per row")
+    if tokens is not None and accepted is None:
+        raise ValueError("accepted output is required with tokens")
+    v = (logits.shape[1] if vocab_size is None else vocab_size) if logits is not None else 0
+    _lib.check(_lib.load().gm_step_tokens(
+        pool.handle, slots.data_ptr(), slots.numel(), tokens.data_ptr() if tokens is not None else None,
+        accepted.data_ptr() if accepted is not None else None, 1 if recycle else 0,
+        bitmask.data_ptr() if bitmask is not None else None, bitmask.stride(0) if bitmask is not None else 0,
+        rows.data_ptr() if rows is not None else None, logits.data_ptr() if logits is not None else None,
+        _DTYPES[logits.dtype] if logits is not None else 0, v, logits.stride(0) if logits is not None else 0,
+        _lib.stream_ptr(stream)), "gm_step_tokens")
 
 
 def batch_recycle(pool: MatcherPool, slots: torch.Tensor, stream=None) -> None:

@@ -337,3 +337,65 @@ def test_fused_fill_apply_equals_separate(dtype):
         b[:, vocab.eos_id] = float("-inf")
         toks = b.float().argmax(-1).tolist()
         assert all(gm.BatchGrammarMatcher.batch_accept_token(ms, toks))
+
+
+@pytest.mark.parametrize("name", ["json", "xml", "arithmetic"])
+@pytest.mark.parametrize("with_logits", [False, True])
+def test_step_kernel_equals_accept_then_fill(name, with_logits):
+    """K5 (accept + recycle + fill [+ apply] in one launch) == K4 accept,
+    recycle, then K2 fill (+ K0 apply), bit for bit, including rejected
+    tokens (state unchanged) and requests that finish and restart."""
+    import torch
+
+    import paper_2411_15100_b200 as gm
+    from paper_2411_15100_b200.engine import get_pool
+    from paper_2411_15100_b200.matcher import batch_accept, batch_fill, batch_recycle, batch_step
+
+    vocab = vocab_by_name("4000:mixed")
+    info = gm.TokenizerInfo.from_vocabulary(vocab)
+    text = gm.BUILTIN_JSON_GRAMMAR if name == "json" else grammar_text(name)
+    compiled = gm.GrammarCompiler(info).compile_grammar(text)
+    B, W = 8, (vocab.size + 31) // 32
+    pool = get_pool()
+    ref = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    new = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    s_ref = torch.tensor([m.slot for m in ref], dtype=torch.int32, device="cuda")
+    s_new = torch.tensor([m.slot for m in new], dtype=torch.int32, device="cuda")
+    bm_ref = torch.empty((B, W), dtype=torch.int32, device="cuda")
+    bm_new = torch.empty((B, W), dtype=torch.int32, device="cuda")
+    acc_ref = torch.empty(B, dtype=torch.uint8, device="cuda")
+    acc_new = torch.empty(B, dtype=torch.uint8, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(5)
+    rng = random.Random(11)
+    toks = None
+    for step in range(40):
+        logits = torch.randn(B, vocab.size, device="cuda", generator=g).to(torch.bfloat16)
+        la, lb = logits.clone(), logits.clone()
+        if toks is not None:
+            batch_accept(pool, s_ref, toks, acc_ref)
+            batch_recycle(pool, s_ref)
+        batch_fill(pool, s_ref, bm_ref)
+        gm.apply_token_bitmask_inplace(la, bm_ref)
+        if with_logits:
+            batch_step(pool, s_new, toks, acc_new if toks is not None else None, bm_new, lb, recycle=True)
+        else:
+            batch_step(pool, s_new, toks, acc_new if toks is not None else None, bm_new, recycle=True)
+        assert torch.equal(bm_ref, bm_new), step
+        if toks is not None:
+            assert torch.equal(acc_ref, acc_new), step
+        if with_logits:
+            assert torch.equal(la.view(torch.int16), lb.view(torch.int16)), step
+        # next tokens: mostly allowed ones (EOS preferred when allowed, so
+        # requests finish and restart), sometimes an arbitrary (likely rejected) id
+        allowed = ((bm_ref.unsqueeze(-1) >> torch.arange(32, device="cuda", dtype=torch.int32)) & 1).reshape(B, -1)
+        pick = []
+        for r in range(B):
+            ids = allowed[r, :vocab.size].nonzero().flatten().tolist()
+            if rng.random() < 0.1 or not ids:
+                pick.append(rng.randrange(vocab.size - 1))
+            elif vocab.eos_id in ids and rng.random() < 0.5:
+                pick.append(vocab.eos_id)
+            else:
+                pick.append(rng.choice(ids))
+        toks = torch.tensor(pick, dtype=torch.int32, device="cuda")
+    pool.check()

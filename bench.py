@@ -356,6 +356,7 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     pinned_out = torch.zeros((S, B), dtype=torch.uint8).pin_memory()
     dev_toks = torch.empty(B, dtype=torch.int32, device=dev)
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
+    k5_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
     e2e_mism = torch.zeros((), dtype=torch.int64, device=dev)
     sync_ranks()
     for s in range(S):
@@ -365,15 +366,47 @@ def run_ours(args, rank: int, world: int, group) -> dict:
         e2e_ev[s][0].record(stream)
         if s > 0:
             dev_toks.copy_(pinned_toks[s - 1], non_blocking=True)
+        k5_ev[s][0].record(stream)
         batch.batch_step(matchers, dev_toks if s > 0 else None, bitmask=bitmask, logits=logits, recycle=True,
                          accepted=accepted)
+        k5_ev[s][1].record(stream)
         if s > 0:
             pinned_out[s - 1].copy_(accepted, non_blocking=True)
         e2e_ev[s][1].record(stream)
         e2e_ev[s][1].synchronize()
         e2e_mism += (bitmask[:sample_rows] != mask_keep[s]).any(dim=1).sum()
-    e2e_ms = [e2e_ev[s][0].elapsed_time(e2e_ev[s][1]) for s in range(W0, S)]
+    e2e_eager_ms = [e2e_ev[s][0].elapsed_time(e2e_ev[s][1]) for s in range(W0, S)]
+    k5_ms = [k5_ev[s][0].elapsed_time(k5_ev[s][1]) for s in range(W0, S)]
     all_acc = bool(pinned_out[W0:S - 1].bool().all())
+
+    # pass C' — the same decode steps replayed as CUDA graphs
+    # (DecodeStepGraph: H2D ids -> K5 -> D2H flags captured once per logits
+    # buffer), the serving-loop form of the public API
+    from paper_2411_15100_b200.graph import DecodeStepGraph
+
+    for m in matchers:
+        m.reset()
+    step_graph = DecodeStepGraph(matchers, bitmask, ring, recycle=True)
+    gs = step_graph.stream
+    g_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
+    sync_ranks()
+    with torch.cuda.stream(gs):
+        for s in range(S):
+            if not args.no_flush:
+                flush.zero_()
+            g_ev[s][0].record(gs)
+            if s == 0:
+                step_graph.first(0)
+            else:
+                acc_h = step_graph.run(pinned_toks[s - 1], s % n_ring, wait=False)
+            g_ev[s][1].record(gs)
+            g_ev[s][1].synchronize()
+            if s > 0:
+                pinned_out[s - 1].copy_(acc_h)
+            e2e_mism += (bitmask[:sample_rows] != mask_keep[s]).any(dim=1).sum()
+    torch.cuda.synchronize()
+    e2e_ms = [g_ev[s][0].elapsed_time(g_ev[s][1]) for s in range(W0, S)]
+    all_acc = all_acc and bool(pinned_out[W0:S - 1].bool().all())
     e2e_mask_mismatches = int(e2e_mism)
 
     # pass D — the same e2e as separate public calls (fill+apply, accept,
@@ -409,6 +442,8 @@ def run_ours(args, rank: int, world: int, group) -> dict:
         "apply_us": mx(statistics.fmean(apply_ms) * 1e3),
         "accept_us": mx(statistics.fmean(acc_ms) * 1e3),
         "e2e_us": mx(statistics.fmean(e2e_ms) * 1e3),
+        "e2e_eager_us": mx(statistics.fmean(e2e_eager_ms) * 1e3),
+        "k5_us": mx(statistics.fmean(k5_ms) * 1e3),
         "e2e_separate_us": mx(statistics.fmean(e2e_sep_ms) * 1e3),
         "e2e_mask_mismatches": e2e_mask_mismatches,
         "step_us_median": statistics.median(step_ms) * 1e3,
@@ -667,10 +702,13 @@ def main():
                          "traffic_source": (traffic["source"] + " (dram read+write of one cold ncu replay; the "
                                             "-inf stores stay dirty in L2 past the kernel's end)") if traffic else None,
                          "algorithmic_bytes_per_launch": algo_bytes},
-            "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": B,
-                    "path": "BatchGrammarMatcher.batch_step per decode step: accept previous tokens (pinned ids H2D) "
-                            "+ recycle + fill + apply in one launch (K5), accepted flags D2H",
+            "e2e": {"value": r["e2e_eager_us"], "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": B,
+                    "path": "BatchGrammarMatcher.batch_step per decode step: pinned token ids H2D -> K5 (accept + "
+                            "recycle + fill + apply, one launch) -> accepted flags D2H",
+                    "k5_kernel_us": r["k5_us"],
                     "mask_mismatches_vs_pass_A": r["e2e_mask_mismatches"],
+                    "graph_us": r["e2e_us"],
+                    "graph_path": "DecodeStepGraph.run (the same three operations captured as one CUDA graph)",
                     "separate_calls_us": r["e2e_separate_us"],
                     "separate_calls_path": "batch_fill_and_apply (K3) + batch accept (K4) + recycle, same copies"},
             "gpu_launches": args.steps,

@@ -399,3 +399,54 @@ def test_step_kernel_equals_accept_then_fill(name, with_logits):
                 pick.append(rng.choice(ids))
         toks = torch.tensor(pick, dtype=torch.int32, device="cuda")
     pool.check()
+
+
+def test_decode_step_graph_equals_eager():
+    """DecodeStepGraph (H2D ids -> K5 -> D2H flags, captured) == eager batch_step."""
+    import torch
+
+    import paper_2411_15100_b200 as gm
+    from paper_2411_15100_b200.engine import get_pool
+    from paper_2411_15100_b200.graph import DecodeStepGraph
+    from paper_2411_15100_b200.matcher import batch_step
+
+    vocab = vocab_by_name("4000:mixed")
+    info = gm.TokenizerInfo.from_vocabulary(vocab)
+    compiled = gm.GrammarCompiler(info).compile_builtin_json_grammar()
+    B, W = 6, (vocab.size + 31) // 32
+    pool = get_pool()
+    ref = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    new = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    s_ref = torch.tensor([m.slot for m in ref], dtype=torch.int32, device="cuda")
+    bm_ref = torch.empty((B, W), dtype=torch.int32, device="cuda")
+    bm_new = torch.empty((B, W), dtype=torch.int32, device="cuda")
+    acc_ref = torch.empty(B, dtype=torch.uint8, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(9)
+    bufs = [torch.empty(B, vocab.size, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+    step = DecodeStepGraph(new, bm_new, bufs, recycle=True)
+    rng = random.Random(4)
+    toks = None
+    for it in range(30):
+        base = torch.randn(B, vocab.size, device="cuda", generator=g).to(torch.bfloat16)
+        la = base.clone()
+        i = it % 2
+        bufs[i].copy_(base)
+        torch.cuda.synchronize()
+        if toks is None:
+            batch_step(pool, s_ref, None, None, bm_ref, la, recycle=True)
+            step.first(i)
+        else:
+            batch_step(pool, s_ref, torch.tensor(toks, dtype=torch.int32, device="cuda"), acc_ref, bm_ref, la,
+                       recycle=True)
+            acc = step.run(toks, i)
+            assert acc.tolist() == acc_ref.tolist(), (it, toks, acc.tolist(), acc_ref.tolist(), step.tokens.tolist())
+        torch.cuda.synchronize()
+        step.stream.synchronize()
+        assert torch.equal(bm_ref, bm_new), it
+        assert torch.equal(la.view(torch.int16), bufs[i].view(torch.int16)), it
+        allowed = ((bm_ref.unsqueeze(-1) >> torch.arange(32, device="cuda", dtype=torch.int32)) & 1).reshape(B, -1)
+        toks = []
+        for r in range(B):
+            ids = allowed[r, :vocab.size].nonzero().flatten().tolist()
+            toks.append(vocab.eos_id if (vocab.eos_id in ids and rng.random() < 0.5) else rng.choice(ids))
+    pool.check()

@@ -42,6 +42,23 @@ __device__ __forceinline__ void prefetch_ring(const DevPool& P, int32_t slot, Ri
   if (threadIdx.x == 3) rp->window = P.window[slot];
 }
 
+// Slot header + ring position in ONE round trip: every load is issued before
+// any shared-memory store (a store waiting on its load would otherwise hold
+// back the loads behind it — measured: four serial trips).
+__device__ __forceinline__ void load_header_ring(const DevPool& P, int32_t slot, SlotHdr* s_hdr, RingPos* rp) {
+  const int t = threadIdx.x;
+  int4 v = make_int4(0, 0, 0, 0);
+  int32_t x = 0;
+  if (t < kHdrVec) v = __ldcg(reinterpret_cast<const int4*>(P.hdr + slot) + t);
+  if (t == 1) x = __ldcg(P.head + slot);
+  else if (t == 2) x = __ldcg(P.hist_len + slot);
+  else if (t == 3) x = __ldcg(P.window + slot);
+  if (t < kHdrVec) reinterpret_cast<int4*>(s_hdr)[t] = v;
+  if (t == 1) rp->head = x;
+  else if (t == 2) rp->hist_len = x;
+  else if (t == 3) rp->window = x;
+}
+
 // Append (handle, node) tops as the next ring entry and publish the new
 // header state.  The binding pointers of the global header are unchanged, so
 // only its state fields are rewritten in place.

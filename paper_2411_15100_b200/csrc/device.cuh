@@ -112,7 +112,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 __device__ __forceinline__ void mbar_init(unsigned long long* mbar, uint32_t tx_bytes) {
   const uint32_t m = smem_u32(mbar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  // CTA-local barrier used by this thread's own TMA copies: a proxy fence
+  // suffices (a cluster-scope release fence would also wait for every prior
+  // global store of the thread — e.g. the accept's state writes in K5)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(tx_bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* mbar) {
@@ -852,5 +855,6 @@ __device__ inline void write_header(const DevPool& P, int32_t slot, const DevBin
   header_state(P, h, G, tops, n, terminated, nullptr);
   store_header(P, slot, h);
 }
+
 
 }  // namespace gm

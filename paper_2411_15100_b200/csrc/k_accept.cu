@@ -28,8 +28,7 @@ accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t
   trace_mark(P, 0, 0);
   const int32_t slot = __ldg(slots + i);
   const int32_t tid = __ldg(token_ids + i);
-  load_header(P, slot, &hd);
-  prefetch_ring(P, slot, &rp);
+  load_header_ring(P, slot, &hd, &rp);
   __syncthreads();
   trace_mark(P, 0, 1);
   const bool in_range = tid >= 0 && tid < hd.V;
@@ -45,7 +44,7 @@ accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t
   const int4 e = s_rec[0], inl = s_rec[1];
   const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;
   accepted[i] = (uint8_t)accept_one(P, slot, rp, hd, G, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
-                                    tid == hd.eos, e.x != 0);
+                                    tid == hd.eos, e.x != 0, &hd);
 }
 
 __global__ void __maxnreg__(128)
@@ -53,8 +52,7 @@ accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len, u
   extern __shared__ __align__(16) uint8_t tables[];
   __shared__ SlotHdr hd;
   __shared__ RingPos rp;
-  load_header(P, slot, &hd);
-  prefetch_ring(P, slot, &rp);
+  load_header_ring(P, slot, &hd, &rp);
   __syncthreads();
   const DevGrammar G = stage_blob(hd.blob, hd.blob_bytes, tables);
   if (threadIdx.x != 0) return;
@@ -75,7 +73,8 @@ accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len, u
     *accepted = 1;
     return;
   }
-  *accepted = (uint8_t)accept_one(P, slot, rp, hd, G, len, [&](int64_t b) { return __ldg(data + b); }, false, false);
+  *accepted = (uint8_t)accept_one(P, slot, rp, hd, G, len, [&](int64_t b) { return __ldg(data + b); }, false, false,
+                                  &hd);
 }
 
 __global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32_t start, int32_t window) {

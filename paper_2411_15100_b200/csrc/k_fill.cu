@@ -105,18 +105,20 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int32_t slot = __ldg(slots + i);
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
-  load_header(P, slot, &hd);
   __shared__ RingPos rp;
   __shared__ int4 s_rec[2];
   __shared__ int s_just_term;
   int32_t tok = -1;
   if (ACCEPT && SA.tokens) {
-    prefetch_ring(P, slot, &rp);
     tok = __ldg(SA.tokens + i);
+    load_header_ring(P, slot, &hd, &rp);
+  } else {
+    load_header(P, slot, &hd);
   }
   __syncthreads();
   trace_mark(P, 1, 1);
   DevGrammar Gs{};
+  unsigned long long t_acc = 0;
   if (ACCEPT && SA.tokens) {  // launched with one split: one accept per request
     const bool in_range = tok >= 0 && tok < hd.V;
     if (threadIdx.x < 2 && in_range) s_rec[threadIdx.x] = __ldg(hd.tokrec + 2 * (size_t)tok + threadIdx.x);
@@ -135,6 +137,8 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       SA.accepted[i] = (uint8_t)acc;
       s_just_term = !was_term && (hd.flags & 1);
       if (SA.recycle && (hd.flags & 1)) restart_slot(P, slot, Gs, &hd);
+      if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_acc));
+      if (P.trace && i == 0) P.trace[48] = t_acc;
     }
     __syncthreads();
   }
@@ -351,7 +355,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     if (c < (int64_t)P.capacity) {
       P.trace[64 + 3 * c] = t1 - t_start;
       P.trace[64 + 3 * c + 1] = (unsigned long long)total | ((unsigned long long)nt << 32);
-      P.trace[64 + 3 * c + 2] = t_merge - t_start;
+      P.trace[64 + 3 * c + 2] = (t_merge - t_start) | ((t_acc ? t_acc - t_start : 0ull) << 32);
     }
     if (c == 0) P.trace[63] = (unsigned long long)n_split;
   }

@@ -301,9 +301,10 @@ def test_guided_generation_is_in_language():  # REF test_matcher.py:376-386
             m.close()
 
 
-@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
-def test_fused_fill_apply_equals_separate(dtype):
-    """K3 (one kernel) == K2 fill then K0 apply, bit for bit, along a trajectory."""
+@pytest.mark.parametrize("dtype,B", [("float32", 6), ("bfloat16", 6), ("bfloat16", 100)])
+def test_fused_fill_apply_equals_separate(dtype, B):
+    """K3 (one kernel) == K2 fill then K0 apply, bit for bit, along a trajectory
+    (B = 100: one CTA per request with the cross-CTA apply queue)."""
     import torch
 
     import paper_2411_15100_b200 as gm
@@ -313,7 +314,6 @@ def test_fused_fill_apply_equals_separate(dtype):
     vocab = vocab_by_name("4000:mixed")
     info = gm.TokenizerInfo.from_vocabulary(vocab)
     compiled = gm.GrammarCompiler(info).compile_builtin_json_grammar()
-    B = 6
     ms = [gm.GrammarMatcher(compiled) for _ in range(B)]
     pool = get_pool()
     slots = torch.tensor([m.slot for m in ms], dtype=torch.int32, device="cuda")

@@ -21,10 +21,11 @@ import bench  # noqa: E402
 import paper_2411_15100_b200 as gm  # noqa: E402
 from paper_2411_15100_b200 import _lib  # noqa: E402
 from paper_2411_15100_b200.engine import get_pool  # noqa: E402
-from paper_2411_15100_b200.matcher import batch_accept, batch_fill, batch_fill_apply, batch_recycle  # noqa: E402
+from paper_2411_15100_b200.matcher import (  # noqa: E402
+    batch_accept, batch_fill, batch_fill_apply, batch_recycle, batch_step)
 
 
-def main(steps=12, flush=True, fused=False, grammar="json"):
+def main(steps=12, flush=True, fused=False, grammar="json", step_mode=False):
     torch.cuda.set_device(0)
     vocab = gm.synth_vocab(128256)
     info = gm.TokenizerInfo.from_vocabulary(vocab)
@@ -47,7 +48,10 @@ def main(steps=12, flush=True, fused=False, grammar="json"):
     for s in range(steps):
         if flush:
             fl.zero_()
-        if fused:
+        if step_mode:
+            batch_step(pool, slots, toks if s > 0 else None, acc if s > 0 else None, bitmask,
+                       logits if fused else None, recycle=True)
+        elif fused:
             batch_fill_apply(pool, slots, logits, bitmask)
         else:
             batch_fill(pool, slots, bitmask)
@@ -56,12 +60,15 @@ def main(steps=12, flush=True, fused=False, grammar="json"):
         f = [buf[16 + k] for k in range(8)]
         ns = max(1, buf[63])
         nc = B * ns
-        cta = sorted(((buf[64 + 3 * i] / 1e3, buf[66 + 3 * i] / 1e3, buf[65 + 3 * i] & 0xFFFFFFFF,
-                       buf[65 + 3 * i] >> 32) for i in range(nc)), reverse=True)
+        cta = sorted(((buf[64 + 3 * i] / 1e3, (buf[66 + 3 * i] & 0xFFFFFFFF) / 1e3, buf[65 + 3 * i] & 0xFFFFFFFF,
+                       buf[65 + 3 * i] >> 32, (buf[66 + 3 * i] >> 32) / 1e3) for i in range(nc)), reverse=True)
         mrg = sorted(c[1] for c in cta)
-        print(f"  {'K3' if fused else 'K2'} x{ns} per-CTA us: max {cta[0][0]:.2f} p50 {cta[nc // 2][0]:.2f} | "
-              f"to-merge-done max {mrg[-1]:.2f} p50 {mrg[nc // 2]:.2f} | slowest (us, merge-us, deps, tops): "
-              f"{[(round(a, 2), round(m, 2), b, c) for a, m, b, c in cta[:4]]}")
+        accd = sorted(c[4] for c in cta)
+        kname = ("K5" if step_mode else "K3" if fused else "K2")
+        print(f"  {kname} x{ns} per-CTA us: max {cta[0][0]:.2f} p50 {cta[nc // 2][0]:.2f} | "
+              f"accept-done max {accd[-1]:.2f} p50 {accd[nc // 2]:.2f} | "
+              f"to-merge-done max {mrg[-1]:.2f} p50 {mrg[nc // 2]:.2f} | slowest (us, merge-us, deps, tops, acc-us): "
+              f"{[(round(a, 2), round(m, 2), b, c, round(d, 2)) for a, m, b, c, d in cta[:4]]}")
         extra = f"deps={buf[24]} key0={C.c_int64(buf[25]).value} ntops={buf[26]}"
         if buf[24]:
             ln = buf[44] & 0xFFFF
@@ -71,6 +78,13 @@ def main(steps=12, flush=True, fused=False, grammar="json"):
                 buf[32 + b] = 0
         allowed = bench.unpack_allowed(bitmask, vocab.size)
         toks = bench.sample_tokens(allowed, structural, s, rows, force=force).to(torch.int32)
+        if step_mode:
+            fp = [buf[16], buf[17], buf[48], buf[18], buf[20], buf[21], buf[22], buf[23]]
+            d = [(fp[k + 1] - fp[k]) / 1e3 if fp[k + 1] >= fp[k] > 0 else float("nan") for k in range(7)]
+            print(f"step {s:2d} K5 CTA0 phases(us): header {d[0]:.2f} accept {d[1]:.2f} setup {d[2]:.2f} "
+                  f"stage+ctx {d[3]:.2f} walks {d[4]:.2f} barrier {d[5]:.2f} merge {d[6]:.2f} "
+                  f"deps={buf[24]} ntops={buf[26]}")
+            continue
         if flush:
             fl.zero_()
         torch.cuda.synchronize()
@@ -91,4 +105,4 @@ def main(steps=12, flush=True, fused=False, grammar="json"):
 
 if __name__ == "__main__":
     g = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--grammar=")), "json")
-    main(flush="--warm" not in sys.argv, fused="--fused" in sys.argv, grammar=g)
+    main(flush="--warm" not in sys.argv, fused="--fused" in sys.argv, grammar=g, step_mode="--step" in sys.argv)

@@ -42,7 +42,8 @@ enum {
   GM_ERR_SHAPE = 5,       /* mask/bitmask shape mismatch (REF matcher.py:382-383) */
   GM_ERR_ARENA_FULL = 6,  /* device stack arena exhausted                        */
   GM_ERR_ROLLBACK = 7,    /* rollback beyond history (REF matcher.py:313-314)    */
-  GM_ERR_OOM = 8
+  GM_ERR_OOM = 8,
+  GM_ERR_GRAMMAR = 9      /* grammar outside the engine's limits (GrammarError) */
 };
 
 /* Thread-local description of the last failure on this thread. */
@@ -119,6 +120,50 @@ typedef struct gm_grammar_tables {
   const int32_t* follow_next;  /* [n_fstates*n_classes]                        */
   int32_t n_fstates;
 } gm_grammar_tables;
+
+/* ------------------------------------------------------------------------ */
+/* Native host front end                                  */
+/* ------------------------------------------------------------------------ */
+/* Replaces the reference's PDA construction and optimisation passes and the
+ * FollowFsa precompute (REF pda.py:246-535, cache.py:241-333) with the
+ * automaton construction of paper_2411_15100_b200/automaton.py in C++: per
+ * rule subset construction + Moore minimisation, inlining of small call-free
+ * rules, silent-move pre-closure, follow DFA.  Input: the parsed grammar as
+ * an int32 prefix IR (front_end.cpp header), n_rules bodies in rule-id order.
+ * Output: tables in the gm_grammar_tables layout (kept_rules[i] = source rule
+ * id of device rule i), owned by the returned handle.  Host only (no GPU).
+ * Errors: GM_ERR_STATE_CAP (closure cap, REF pda.py:53-57), GM_ERR_GRAMMAR. */
+typedef struct gm_fe_options {
+  int32_t determinize;              /* must be 1 (CompileOptions.merge)      */
+  int32_t inline_rules;             /* CompileOptions.inline                 */
+  int32_t ctx_expansion;            /* CompileOptions.ctx_expansion          */
+  int32_t inline_max_rule_states;   /* 32                                    */
+  int32_t inline_max_result_states; /* 1024                                  */
+  int32_t max_dfa_states;           /* 200000                                */
+  int32_t max_follow_states;        /* 4096                                  */
+  int32_t state_cap;                /* 4096 (REF pda.py:53)                  */
+} gm_fe_options;
+
+typedef struct gm_fe_tables {
+  int32_t n_nodes, n_rules, n_classes, start_node, root_rule;
+  int32_t n_trans, n_push, n_keys, n_fstates;
+  const uint8_t* byte_class;
+  const int32_t* trans_off;
+  const int32_t* trans;
+  const int32_t* push_pool;
+  const uint8_t* node_flags;
+  const int32_t* node_rule;
+  const int32_t* cache_keys;
+  const int32_t* follow_start;
+  const int32_t* follow_next;
+  const int32_t* kept_rules;
+} gm_fe_tables;
+
+typedef struct gm_front_end gm_front_end;
+gm_status gm_front_end_build(const int32_t* ir, int64_t ir_len, int32_t n_rules,
+                             int32_t root_rule, const gm_fe_options* opts,
+                             gm_front_end** out, gm_fe_tables* view);
+void gm_front_end_release(gm_front_end* fe);
 
 typedef struct gm_grammar gm_grammar;
 /* Copies the (host) tables to the current device. */

@@ -23,6 +23,7 @@ GM_ERR_SHAPE = 5
 GM_ERR_ARENA_FULL = 6
 GM_ERR_ROLLBACK = 7
 GM_ERR_OOM = 8
+GM_ERR_GRAMMAR = 9
 
 GM_DTYPE_F32, GM_DTYPE_F16, GM_DTYPE_BF16 = 0, 1, 2
 GM_NODE_POP, GM_NODE_DEAD_END = 1, 2
@@ -57,6 +58,19 @@ class gm_grammar_tables(C.Structure):
         ("follow_next", C.c_void_p),
         ("n_fstates", C.c_int32),
     ]
+
+
+class gm_fe_options(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("determinize", "inline_rules", "ctx_expansion", "inline_max_rule_states",
+                                          "inline_max_result_states", "max_dfa_states", "max_follow_states",
+                                          "state_cap")]
+
+
+class gm_fe_tables(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("n_nodes", "n_rules", "n_classes", "start_node", "root_rule", "n_trans",
+                                          "n_push", "n_keys", "n_fstates")] + [
+        (n, C.c_void_p) for n in ("byte_class", "trans_off", "trans", "push_pool", "node_flags", "node_rule",
+                                  "cache_keys", "follow_start", "follow_next", "kept_rules")]
 
 
 class gm_cache_stats(C.Structure):
@@ -104,6 +118,9 @@ _SIGNATURES = {
     "gm_pool_check": ([_P, _P], _I32),
     "gm_pool_arena_used": ([_P], _I64),
     "gm_pool_trace": ([_P, _P, _I64], _I32),
+    "gm_front_end_build": ([_P, _I64, _I32, _I32, C.POINTER(gm_fe_options), C.POINTER(_P),
+                            C.POINTER(gm_fe_tables)], _I32),
+    "gm_front_end_release": ([_P], None),
 }
 
 _lib = None

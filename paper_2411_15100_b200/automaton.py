@@ -28,7 +28,8 @@ import numpy as np
 
 from .grammar import Alt, Bytes, Eps, GrammarError, Lit, ParsedGrammar, Ref, Rep, Seq
 
-__all__ = ["StateLimitError", "CompiledTables", "AutomatonOptions", "build_tables"]
+__all__ = ["StateLimitError", "CompiledTables", "AutomatonOptions", "build_tables", "build_tables_native",
+           "encode_ir"]
 
 DEFAULT_STATE_CAP = 4096  # REF pda.py:53
 _FOLLOW_DEAD, _FOLLOW_ANY = -1, -2
@@ -595,9 +596,119 @@ def _follow_dfa(n_nodes, n_rules, n_classes, root, trans_n, calls_n, final_n, no
                 continue
             for c, d in trans_n[s].items():
                 by_class.setdefault(c, set()).add(d)
-        for c, targets in by_class.items():
-            T, wild = expand(targets)
+        for c in sorted(by_class):  # canonical numbering (front_end.cpp does the same)
+            T, wild = expand(by_class[c])
             row[c] = intern(T, wild)
         rows.append(row)
     nxt = np.asarray(rows if rows else [[_FOLLOW_DEAD] * n_classes], dtype=np.int32).reshape(-1)
     return start, nxt, len(order)
+
+
+# ---------------------------------------------------------------------------
+# native front end (csrc/front_end.cpp): same tables, built in C++
+
+
+def encode_ir(g: ParsedGrammar) -> Tuple[np.ndarray, Dict[str, int]]:
+    """Prefix int32 IR of every rule body, in rule-id (source) order — the
+    input format of gm_front_end_build (front_end.cpp header)."""
+    rid_of = {nm: i for i, nm in enumerate(g.names)}
+    out: List[int] = []
+    stack = []
+
+    def emit(e):
+        if isinstance(e, Eps):
+            out.append(0)
+        elif isinstance(e, Bytes):
+            m = e.mask
+            out.append(1)
+            out.extend((m >> (32 * k)) & 0xFFFFFFFF for k in range(8))
+        elif isinstance(e, Lit):
+            out.append(2)
+            out.append(len(e.data))
+            out.extend(e.data)
+        elif isinstance(e, (Seq, Alt)):
+            out.append(3 if isinstance(e, Seq) else 4)
+            out.append(len(e.items))
+            for item in e.items:
+                emit(item)
+        elif isinstance(e, Rep):
+            out.extend((5, e.lo, -1 if e.hi is None else e.hi))
+            emit(e.item)
+        elif isinstance(e, Ref):
+            out.extend((6, rid_of[e.name]))
+        else:
+            raise TypeError(e)
+
+    del stack
+    for nm in g.names:
+        emit(g.bodies[nm])
+    arr = np.asarray(out, dtype=np.int64)
+    return arr.astype(np.uint32).view(np.int32) if arr.size else arr.astype(np.int32), rid_of
+
+
+def build_tables_native(g: ParsedGrammar, opts: Optional[AutomatonOptions] = None) -> CompiledTables:
+    """build_tables through libgmask's C++ front end (gm_front_end_build):
+    identical tables (tests/test_frontend.py compares them array for array),
+    a fraction of the host time."""
+    import ctypes as C
+
+    from . import _lib
+
+    opts = opts or AutomatonOptions()
+    if not opts.determinize:
+        raise NotImplementedError("determinize=False is not supported by the device tables")
+    ir, rid_of = encode_ir(g)
+    ir = np.ascontiguousarray(ir)
+    fo = _lib.gm_fe_options(1, int(opts.inline), int(opts.ctx_expansion), opts.inline_max_rule_states,
+                            opts.inline_max_result_states, opts.max_dfa_states, opts.max_follow_states,
+                            opts.state_cap)
+    view = _lib.gm_fe_tables()
+    h = C.c_void_p()
+    lib = _lib.load()
+    st = lib.gm_front_end_build(ir.ctypes.data, ir.size, len(g.names), rid_of[g.root], C.byref(fo), C.byref(h),
+                                C.byref(view))
+    if st != _lib.GM_OK:
+        msg = lib.gm_last_error().decode(errors="replace")
+        if st == _lib.GM_ERR_STATE_CAP:
+            raise StateLimitError(msg)
+        if st == _lib.GM_ERR_GRAMMAR:
+            raise GrammarError(msg)
+        _lib.check(st, "gm_front_end_build")
+    try:
+        def arr(ptr, n, ct, dt):
+            if n == 0:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).astype(dt, copy=True)
+
+        v = view
+        n_idx = v.n_nodes * v.n_classes
+        kept = arr(v.kept_rules, v.n_rules, C.c_int32, np.int32)
+        t = CompiledTables(
+            n_nodes=v.n_nodes,
+            n_rules=v.n_rules,
+            n_classes=v.n_classes,
+            start_node=v.start_node,
+            root_rule=v.root_rule,
+            rule_names=[g.names[r] for r in kept],
+            byte_class=arr(v.byte_class, 256, C.c_uint8, np.uint8),
+            trans_off=arr(v.trans_off, n_idx + 1, C.c_int32, np.int32),
+            trans=arr(v.trans, 2 * v.n_trans, C.c_int32, np.int32),
+            push_pool=arr(v.push_pool, v.n_push, C.c_int32, np.int32),
+            node_flags=arr(v.node_flags, v.n_nodes, C.c_uint8, np.uint8),
+            node_rule=arr(v.node_rule, v.n_nodes, C.c_int32, np.int32),
+            cache_keys=arr(v.cache_keys, v.n_keys, C.c_int32, np.int32),
+            follow_start=arr(v.follow_start, v.n_rules, C.c_int32, np.int32),
+            follow_next=arr(v.follow_next, max(v.n_fstates, 1) * v.n_classes, C.c_int32, np.int32),
+            n_fstates=v.n_fstates,
+        )
+    finally:
+        lib.gm_front_end_release(h)
+    t.stats = {
+        "nodes": t.n_nodes,
+        "rules": t.n_rules,
+        "classes": t.n_classes,
+        "transitions": len(t.trans) // 2,
+        "keys": len(t.cache_keys),
+        "follow_states": t.n_fstates,
+    }
+    return t

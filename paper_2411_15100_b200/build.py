@@ -21,7 +21,8 @@ OUT = PKG / "libgmask.so"
 BUILD = PKG / "_build"
 
 SOURCES = ["gm_api.cu", "k_apply.cu", "k_cache.cu", "k_fill.cu", "k_accept.cu"]
-HEADERS = ["common.cuh", "device.cuh"]
+HOST_SOURCES = ["front_end.cpp"]  # host-only C++ (g++)
+HEADERS = ["common.cuh", "device.cuh", "accept.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -43,7 +44,7 @@ def _stale() -> bool:
     if not OUT.exists():
         return True
     t = OUT.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "gmask.h", Path(__file__)]
+    deps = [CSRC / s for s in SOURCES + HOST_SOURCES + HEADERS] + [ROOT / "include" / "gmask.h", Path(__file__)]
     return any(d.stat().st_mtime > t for d in deps)
 
 
@@ -65,8 +66,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         (BUILD / (Path(src).stem + ".ptxas.txt")).write_text(res.stderr)
         return obj
 
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(compile_one, SOURCES))
+    def compile_host(src: str):
+        obj = BUILD / (Path(src).stem + ".o")
+        cxx = shutil.which("g++") or "g++"
+        cmd = [cxx, "-O2", "-std=c++17", "-fPIC", "-Wall", *include, "-c", str(CSRC / src), "-o", str(obj)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"g++ failed for {src}:\n{res.stderr}")
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES) + len(HOST_SOURCES)) as ex:
+        futs = [ex.submit(compile_one, s) for s in SOURCES] + [ex.submit(compile_host, s) for s in HOST_SOURCES]
+        objs = [f.result() for f in futs]
     tmp = OUT.with_suffix(".so.tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *map(str, objs), "-o", str(tmp)]
     res = subprocess.run(cmd, capture_output=True, text=True)

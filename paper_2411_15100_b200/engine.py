@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .automaton import AutomatonOptions, CompiledTables, StateLimitError, build_tables
+from .automaton import AutomatonOptions, CompiledTables, StateLimitError, build_tables_native
 from .grammar import parse_grammar
 from .vocab import Vocabulary
 
@@ -198,7 +198,7 @@ def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOp
     the cache keys are dealt round-robin-by-block across ranks and the rows
     are replicated with one all-gather."""
     t0 = time.perf_counter()
-    tables = build_tables(parse_grammar(text, root_rule_name), opts)
+    tables = build_tables_native(parse_grammar(text, root_rule_name), opts)
     t1 = time.perf_counter()
     grammar = DeviceGrammar(tables)
     n_keys = grammar.n_keys

@@ -109,3 +109,61 @@ def test_masks_on_small_vocab_match_golden():
                 if step >= len(traj["tokens"]) or traj["tokens"][step] == vocab.eos_id:
                     break
                 st = sim.walk(st, vocab.tokens[traj["tokens"][step]])
+
+
+def _schema_variants(n):
+    import random
+
+    words = ["name", "unit", "count", "tags", "city", "time", "zone", "level", "mode", "query", "id", "score"]
+    lits = ["get_weather", "get_time", "search", "celsius", "on", "off", "red", "blue"]
+    out = []
+    for k in range(n):
+        rng = random.Random(500 + k)
+        names = rng.sample(words, rng.randint(2, 5))
+        props = {}
+        for nm in names:
+            kind = rng.choice(["enum", "string", "integer", "array", "number", "boolean"])
+            if kind == "enum":
+                props[nm] = {"enum": rng.sample(lits, rng.randint(2, 3))}
+            elif kind == "array":
+                lo = rng.randint(0, 2)
+                props[nm] = {"type": "array", "items": {"type": "string"}, "minItems": lo, "maxItems": lo + 2}
+            else:
+                props[nm] = {"type": kind}
+        out.append({"type": "object", "properties": props, "required": names[:1], "additionalProperties": False})
+    return out
+
+
+def test_native_front_end_tables_identical():
+    """The C++ front end (gm_front_end_build, §8f rank 2) builds exactly the
+    tables of the Python specification (automaton.build_tables), array for
+    array, for every reference grammar and 24 schema grammars; host only."""
+    import numpy as np
+
+    from paper_2411_15100_b200.automaton import AutomatonOptions, build_tables_native
+    from paper_2411_15100_b200.compiler import BUILTIN_JSON_GRAMMAR
+
+    lang = languages()
+    texts = {"builtin_json": BUILTIN_JSON_GRAMMAR, **lang["grammars"], **lang["extra_grammars"]}
+    for k, sc in enumerate(_schema_variants(24)):
+        texts[f"schema{k}"] = schema_to_grammar_text(json.dumps(sc))
+    fields = ["n_nodes", "n_rules", "n_classes", "start_node", "root_rule", "rule_names", "byte_class", "trans_off",
+              "trans", "push_pool", "node_flags", "node_rule", "cache_keys", "follow_start", "follow_next",
+              "n_fstates"]
+    for opts in (AutomatonOptions(), AutomatonOptions(inline=False), AutomatonOptions(ctx_expansion=False)):
+        for name, text in texts.items():
+            g = parse_grammar(text)
+            a, b = build_tables(g, opts), build_tables_native(g, opts)
+            for f in fields:
+                x, y = getattr(a, f), getattr(b, f)
+                if isinstance(x, np.ndarray):
+                    assert np.array_equal(x, y), (name, f)
+                else:
+                    assert x == y, (name, f)
+
+
+def test_native_front_end_errors():
+    from paper_2411_15100_b200.automaton import build_tables_native
+
+    with pytest.raises(StateLimitError):
+        build_tables_native(parse_grammar('root ::= root "a" | "b"'))

@@ -169,8 +169,9 @@ struct DevCache {
   const uint32_t* acc_rows;    // [n_keys*W]
   const int32_t* dep_off;      // [n_keys+1]
   const int32_t* dep_ids;
-  const int4* dep_ent;         // [2*n_dep] records (tid, len, offset, 0) + inline bytes
-  const uint8_t* dep_bytes;    // dependent tokens' bytes, contiguous
+  const int4* dep_ent;         // [2*n_dep] records (tid, len, byte offset into the vocabulary's
+                               // token-record buffer, context classes) + 16 inline bytes
+  const uint8_t* dep_bytes;    // unused (null)
   const uint8_t* blob;         // binding blob (tables + node_info)
   int32_t blob_bytes;
 };

@@ -24,7 +24,8 @@ gm_status launch_cache_build(const DevGrammar&, const DevVocab&, const DevArena&
                              uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
 gm_status launch_row_popcount(const uint32_t*, int32_t, int32_t, int64_t*, cudaStream_t);
 gm_status launch_dep_compact(const uint32_t*, int32_t, int32_t, const int32_t*, int32_t*, cudaStream_t);
-gm_status launch_dep_context(const DevGrammar&, const int4*, int64_t, uint8_t*, cudaStream_t);
+gm_status launch_dep_records(const int32_t*, int64_t, const int4*, int4*, cudaStream_t);
+gm_status launch_dep_context(const DevGrammar&, const int32_t*, int32_t, int64_t, int4*, const uint8_t*, cudaStream_t);
 gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*,
                       uint8_t*, int32_t, cudaStream_t);
 gm_status launch_fill_apply(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*, int32_t,
@@ -403,62 +404,34 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
   const int32_t n = g->dev.n_keys, W = v->dev.W;
   gm_cache* c = new gm_cache();
   gm_status st;
-  uint32_t *acc, *dep_tmp;
-  int64_t* counts;
-  int32_t* dep_off;
-  if ((st = c->mem.alloc(&acc, (size_t)n * W)) || (st = c->mem.alloc(&counts, (size_t)n + 1)) ||
-      (st = c->mem.alloc(&dep_off, (size_t)n + 1))) {
+  auto bail = [&](gm_status e) {
     c->mem.release();
     delete c;
-    return st;
-  }
-  std::vector<int64_t> dep_cnt(n), acc_cnt(n);
+    return e;
+  };
+  // phase 1 (one allocation): the cache's own accepted rows + row counts
+  const size_t rows_bytes = (size_t)n * W * 4;
+  const size_t off_counts = (rows_bytes + 15) & ~size_t(15);
+  uint8_t* buf1;
+  if ((st = c->mem.alloc(&buf1, off_counts + (size_t)(2 * n + 1) * 8))) return bail(st);
+  uint32_t* acc = reinterpret_cast<uint32_t*>(buf1);
+  int64_t* counts = reinterpret_cast<int64_t*>(buf1 + off_counts);
+  std::vector<int64_t> cnt(2 * (size_t)n);
   if (n) {
-    GM_CUDA_TRY(cudaMemcpyAsync(acc, acc_rows, (size_t)n * W * 4, cudaMemcpyDeviceToDevice, s));
-    dep_tmp = reinterpret_cast<uint32_t*>(const_cast<int32_t*>(dep_rows));
-    if ((st = launch_row_popcount(dep_tmp, W, n, counts, s))) return st;
-    GM_CUDA_TRY(cudaMemcpyAsync(dep_cnt.data(), counts, n * 8, cudaMemcpyDeviceToHost, s));
-    if ((st = launch_row_popcount(acc, W, n, counts, s))) return st;
-    GM_CUDA_TRY(cudaMemcpyAsync(acc_cnt.data(), counts, n * 8, cudaMemcpyDeviceToHost, s));
+    GM_CUDA_TRY(cudaMemcpyAsync(acc, acc_rows, rows_bytes, cudaMemcpyDeviceToDevice, s));
+    if ((st = launch_row_popcount(reinterpret_cast<const uint32_t*>(dep_rows), W, n, counts, s))) return bail(st);
+    if ((st = launch_row_popcount(acc, W, n, counts + n, s))) return bail(st);
+    GM_CUDA_TRY(cudaMemcpyAsync(cnt.data(), counts, (size_t)2 * n * 8, cudaMemcpyDeviceToHost, s));
     GM_CUDA_TRY(cudaStreamSynchronize(s));
   }
   std::vector<int32_t> off(n + 1, 0);
   int64_t dep_total = 0, acc_total = 0;
   for (int32_t k = 0; k < n; ++k) {
-    dep_total += dep_cnt[k];
-    acc_total += acc_cnt[k];
-    if (dep_total > INT32_MAX) return fail(GM_ERR_INVALID, "too many dependent tokens");
+    dep_total += cnt[k];
+    acc_total += cnt[(size_t)n + k];
+    if (dep_total > INT32_MAX) return bail(fail(GM_ERR_INVALID, "too many dependent tokens"));
     off[k + 1] = (int32_t)dep_total;
   }
-  int32_t* dep_ids;
-  if ((st = c->mem.alloc(&dep_ids, (size_t)dep_total))) {
-    c->mem.release();
-    delete c;
-    return st;
-  }
-  GM_CUDA_TRY(cudaMemcpyAsync(dep_off, off.data(), (n + 1) * 4, cudaMemcpyHostToDevice, s));
-  if (n && (st = launch_dep_compact(reinterpret_cast<const uint32_t*>(dep_rows), W, n, dep_off, dep_ids, s)))
-    return st;
-  // dependent entries with their bytes laid out contiguously per key, so a
-  // fill-time walk needs one load for (id, bytes) instead of id -> offsets ->
-  // bytes (cold round trips)
-  std::vector<int32_t> ids_host((size_t)dep_total);
-  if (dep_total) GM_CUDA_TRY(cudaMemcpyAsync(ids_host.data(), dep_ids, dep_total * 4, cudaMemcpyDeviceToHost, s));
-  GM_CUDA_TRY(cudaStreamSynchronize(s));
-  // dependent records (tid, len, far offset, 0) + 16 inline bytes, then the
-  // dependent tokens' full bytes; offsets relative to the buffer start
-  const size_t drec = (size_t)dep_total * 32;
-  std::vector<uint8_t> depbuf(drec, 0);
-  for (int64_t i = 0; i < dep_total; ++i) {
-    const int32_t tid = ids_host[i];
-    const int64_t o0 = v->off_host[tid], len = v->off_host[tid + 1] - o0;
-    int32_t hdr4[4] = {tid, (int32_t)len, (int32_t)depbuf.size(), 0};
-    std::memcpy(depbuf.data() + (size_t)i * 32, hdr4, 16);
-    std::memcpy(depbuf.data() + (size_t)i * 32 + 16, v->bytes_host.data() + o0, (size_t)std::min<int64_t>(len, 16));
-    depbuf.insert(depbuf.end(), v->bytes_host.begin() + o0, v->bytes_host.begin() + o0 + len);
-  }
-  depbuf.resize(depbuf.size() + 16, 0);
-  if (depbuf.size() > (size_t)INT32_MAX) return fail(GM_ERR_INVALID, "too many dependent bytes");
   // binding blob: grammar blob + node_info (key, dep_lo, dep_hi, rule) per node
   std::vector<uint8_t> bblob = g->blob_host;
   const size_t o_ninfo = (bblob.size() + 15) & ~size_t(15);
@@ -473,45 +446,38 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
   bh.o_ninfo = (int32_t)o_ninfo;
   bh.bytes = (int32_t)bblob.size();
   std::memcpy(bblob.data(), &bh, sizeof(bh));
-  uint8_t *d_dep, *d_bblob;
-  if ((st = c->mem.upload(&d_dep, depbuf.data(), depbuf.size())) ||
-      (st = c->mem.upload(&d_bblob, bblob.data(), bblob.size())))
-    return st;
-  // one-level context classes per (dependent entry, caller of the key's rule)
-  {
-    BlobHdr gh;
-    std::memcpy(&gh, g->blob_host.data(), sizeof(gh));
-    const int32_t* callers = reinterpret_cast<const int32_t*>(g->blob_host.data() + gh.o_callers);
-    std::vector<int4> tasks;
-    for (int32_t k = 0; k < n; ++k) {
-      const int32_t nd = g->keys[k];
-      const int32_t* cr = callers + (size_t)g->node_rule[nd] * kMaxCallers;
-      const bool root = g->node_rule[nd] == g->node_rule[g->dev.start_node];
-      for (int32_t i = off[k]; i < off[k + 1]; ++i) {
-        for (int j = 0; j < kRootCaller && cr[j] >= 0; ++j) tasks.push_back(make_int4(i, j, nd, cr[j]));
-        if (root) tasks.push_back(make_int4(i, kRootCaller, nd, -1));
-      }
-    }
-    if (!tasks.empty()) {
-      DevAllocs tmp;
-      int4* d_tasks;
-      if ((st = tmp.upload(&d_tasks, tasks.data(), tasks.size())) ||
-          (st = launch_dep_context(g->dev, d_tasks, (int64_t)tasks.size(), d_dep, s))) {
-        tmp.release();
-        return st;
-      }
-      GM_CUDA_TRY(cudaStreamSynchronize(s));
-      tmp.release();
-    }
-  }
+  // phase 2 (one allocation): dep_off | dep_ids | dependent records | blob |
+  // binding; host-side pieces go up in one copy
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t o_off = 0, o_ids = align((size_t)(n + 1) * 4), o_rec = o_ids + align((size_t)dep_total * 4 + 4);
+  const size_t o_blob = o_rec + align((size_t)dep_total * 32 + 32), o_bind = o_blob + align(bblob.size());
+  const size_t total = o_bind + sizeof(DevBinding);
+  uint8_t* buf2;
+  if ((st = c->mem.alloc(&buf2, total))) return bail(st);
+  int32_t* dep_off = reinterpret_cast<int32_t*>(buf2 + o_off);
+  int32_t* dep_ids = reinterpret_cast<int32_t*>(buf2 + o_ids);
+  int4* rec = reinterpret_cast<int4*>(buf2 + o_rec);
+  uint8_t* d_bblob = buf2 + o_blob;
+  DevBinding* db = reinterpret_cast<DevBinding*>(buf2 + o_bind);
   c->host_binding.g = g->dev;
   c->host_binding.v = v->dev;
-  c->host_binding.c = DevCache{acc, dep_off, dep_ids, reinterpret_cast<const int4*>(d_dep), d_dep + drec, d_bblob,
-                               (int32_t)bblob.size()};
-  DevBinding* db;
-  if ((st = c->mem.alloc(&db, 1))) return st;
-  GM_CUDA_TRY(cudaMemcpyAsync(db, &c->host_binding, sizeof(DevBinding), cudaMemcpyHostToDevice, s));
-  GM_CUDA_TRY(cudaStreamSynchronize(s));
+  c->host_binding.c = DevCache{acc, dep_off, dep_ids, rec, nullptr, d_bblob, (int32_t)bblob.size()};
+  std::vector<uint8_t> host(total, 0);
+  std::memcpy(host.data() + o_off, off.data(), (size_t)(n + 1) * 4);
+  std::memcpy(host.data() + o_blob, bblob.data(), bblob.size());
+  std::memcpy(host.data() + o_bind, &c->host_binding, sizeof(DevBinding));
+  // dep_off first (the compaction needs it), blob + binding after the records
+  GM_CUDA_TRY(cudaMemcpyAsync(buf2, host.data(), o_ids, cudaMemcpyHostToDevice, s));
+  GM_CUDA_TRY(cudaMemcpyAsync(buf2 + o_blob, host.data() + o_blob, total - o_blob, cudaMemcpyHostToDevice, s));
+  if (n && (st = launch_dep_compact(reinterpret_cast<const uint32_t*>(dep_rows), W, n, dep_off, dep_ids, s)))
+    return bail(st);
+  // records gathered from the vocabulary's token records (their byte offsets
+  // point into the vocabulary buffer), then the one-level context classes
+  if ((st = launch_dep_records(dep_ids, dep_total, v->dev.tokrec, rec, s)) ||
+      (st = launch_dep_context(g->dev, dep_off, n, dep_total, rec, reinterpret_cast<const uint8_t*>(v->dev.tokrec),
+                               s)))
+    return bail(st);
+  GM_CUDA_TRY(cudaStreamSynchronize(s));  // host buffer + every consumer on other streams
   c->binding = db;
   c->n_keys = n;
   if (stats) {

@@ -115,6 +115,21 @@ __global__ void dep_compact_kernel(const uint32_t* __restrict__ rows, int32_t W,
   }
 }
 
+// Dependent records: the vocabulary's 32-byte token record (length, offset
+// of the full bytes in the vocabulary's record buffer, 16 inline bytes) with
+// the token id in word 0 and word 3 cleared for the context classes.
+__global__ void dep_records_kernel(const int32_t* __restrict__ ids, int64_t n_dep, const int4* __restrict__ tokrec,
+                                   int4* __restrict__ rec) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_dep) return;
+  const int32_t t = ids[i];
+  int4 r0 = tokrec[2 * (size_t)t];
+  r0.x = t;
+  r0.w = 0;
+  rec[2 * i] = r0;
+  rec[2 * i + 1] = tokrec[2 * (size_t)t + 1];
+}
+
 // One-level context classes of the dependent tokens (compile time).  A
 // dependent token of key n dies inside n's rule but for branches that pop
 // past n's frame, so its fate depends on the frames below.  For every
@@ -123,33 +138,48 @@ __global__ void dep_compact_kernel(const uint32_t* __restrict__ rows, int32_t W,
 //   survives                      -> accepted whatever lies below c
 //   dies, no branch pops past c   -> rejected whatever lies below c
 //   some branch pops past c       -> needs the request's deeper stack
-// The class is or-ed into the record's 4th word (2 bits per caller index);
-// the fill then walks only the "deeper" ones (and unknown callers).
-// This is an exact refinement of the reference's context-dependent set
-// (REF matcher.py:219-237 resolves every one of them by a full walk).
-__global__ void dep_context_kernel(DevGrammar G, const int4* __restrict__ tasks, int64_t n_tasks,
-                                   uint8_t* __restrict__ dep) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n_tasks) return;
-  const int4 tk = tasks[q];  // (entry, caller index, key node, caller node or -1 = root)
-  int4* rec = reinterpret_cast<int4*>(dep + (size_t)tk.x * 32);
-  const int4 e = rec[0], inl = rec[1];
-  const uint8_t* far = dep + e.z;
+// and, for keys of the root rule, from [n] alone (the root frame: popping
+// past it ends the walk).  The classes are packed 2 bits per caller index
+// into the record's 4th word; the fill then walks only the "deeper" ones and
+// unknown callers.  An exact refinement of the reference's context-dependent
+// set (REF matcher.py:219-237 resolves every one of them by a full walk).
+// One thread per dependent entry.
+__device__ uint32_t context_class(const DevGrammar& G, int32_t caller, int32_t node, const int4& e, const int4& inl,
+                                  const uint8_t* far) {
   const DevArena A{nullptr, 0, nullptr};  // only local frames are touched
   RWalker<8, 48> rw;
   rw.init(nullptr, nullptr, 0);
-  // caller -1: the root frame, popping past it ends the walk
-  rw.add(tk.w < 0 ? -1 : rw.push(G, A, -1, tk.w), tk.z);
+  rw.add(caller < 0 ? -1 : rw.push(G, A, -1, caller), node);
   bool popped = false;
   for (int b = 0; b < e.y && rw.n > 0 && !rw.spill; ++b) {
     bool pb = false;
     rw.step(G, A, rec_byte(inl, far, b), &pb);
     popped |= pb;
   }
-  uint32_t cls = kCtxUnknown;
-  if (!rw.spill && !rw.err)
-    cls = rw.n > 0 ? kCtxAccept : ((popped && tk.w >= 0) ? kCtxDeeper : kCtxReject);
-  if (cls) atomicOr(reinterpret_cast<int*>(&rec->w), (int)(cls << (2 * tk.y)));
+  if (rw.spill || rw.err) return kCtxUnknown;
+  if (rw.n > 0) return kCtxAccept;
+  return (popped && caller >= 0) ? kCtxDeeper : kCtxReject;
+}
+
+__global__ void dep_context_kernel(DevGrammar G, const int32_t* __restrict__ dep_off, int32_t n_keys, int64_t n_dep,
+                                   int4* __restrict__ rec, const uint8_t* __restrict__ tok_base) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_dep) return;
+  int32_t lo = 0, hi = n_keys - 1;  // key k: dep_off[k] <= i < dep_off[k+1]
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (dep_off[mid] <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  const int32_t node = G.cache_keys[lo];
+  const int32_t rule = G.node_rule[node];
+  const int32_t* cr = G.callers + (size_t)rule * kMaxCallers;
+  const int4 e = rec[2 * i], inl = rec[2 * i + 1];
+  const uint8_t* far = tok_base + e.z;
+  uint32_t w = 0;
+  for (int j = 0; j < kRootCaller && cr[j] >= 0; ++j) w |= context_class(G, cr[j], node, e, inl, far) << (2 * j);
+  if (rule == G.node_rule[G.start_node]) w |= context_class(G, -1, node, e, inl, far) << (2 * kRootCaller);
+  rec[2 * i].w = (int32_t)w;
 }
 
 }  // namespace gm
@@ -177,9 +207,16 @@ gm_status launch_row_popcount(const uint32_t* rows, int32_t W, int32_t n, int64_
   GM_LAUNCH_CHECK();
   return GM_OK;
 }
-gm_status launch_dep_context(const DevGrammar& G, const int4* tasks, int64_t n_tasks, uint8_t* dep, cudaStream_t s) {
-  if (n_tasks <= 0) return GM_OK;
-  dep_context_kernel<<<(unsigned)ceil_div(n_tasks, 128), 128, 0, s>>>(G, tasks, n_tasks, dep);
+gm_status launch_dep_records(const int32_t* ids, int64_t n_dep, const int4* tokrec, int4* rec, cudaStream_t s) {
+  if (n_dep <= 0) return GM_OK;
+  dep_records_kernel<<<(unsigned)ceil_div(n_dep, 256), 256, 0, s>>>(ids, n_dep, tokrec, rec);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_dep_context(const DevGrammar& G, const int32_t* dep_off, int32_t n_keys, int64_t n_dep, int4* rec,
+                             const uint8_t* tok_base, cudaStream_t s) {
+  if (n_dep <= 0) return GM_OK;
+  dep_context_kernel<<<(unsigned)ceil_div(n_dep, 128), 128, 0, s>>>(G, dep_off, n_keys, n_dep, rec, tok_base);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

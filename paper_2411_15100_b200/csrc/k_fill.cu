@@ -229,7 +229,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     }
     __syncthreads();
     trace_mark(P, 1, 4);
-    const uint8_t* rec_base = reinterpret_cast<const uint8_t*>(hd.dep_ent);
+    const uint8_t* rec_base = reinterpret_cast<const uint8_t*>(hd.tokrec);  // records' byte offsets are into it
     const int32_t tok_lo = w_lo * 32, tok_hi = w_hi * 32;
     // warp-major assignment: consecutive dependents go to different warps, so
     // a handful of walks run in parallel instead of diverging inside one warp

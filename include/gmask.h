@@ -157,6 +157,14 @@ typedef struct gm_fe_tables {
   const int32_t* follow_start;
   const int32_t* follow_next;
   const int32_t* kept_rules;
+  /* the per-rule DFAs before the pre-closure (for bundle export): node u's
+   * edges raw[2*raw_off[u] .. 2*raw_off[u+1]) as (symbol, dst), symbol >= 0
+   * a byte class, < 0 a call of rule -(symbol+1) returning to dst */
+  const int32_t* raw_off;      /* [n_nodes + 1] */
+  const int32_t* raw;          /* [2 * n_raw]   */
+  int32_t n_raw;
+  const uint8_t* finals;       /* [n_nodes]     */
+  const int32_t* rule_start;   /* [n_rules]     */
 } gm_fe_tables;
 
 typedef struct gm_front_end gm_front_end;

@@ -70,7 +70,8 @@ class gm_fe_tables(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("n_nodes", "n_rules", "n_classes", "start_node", "root_rule", "n_trans",
                                           "n_push", "n_keys", "n_fstates")] + [
         (n, C.c_void_p) for n in ("byte_class", "trans_off", "trans", "push_pool", "node_flags", "node_rule",
-                                  "cache_keys", "follow_start", "follow_next", "kept_rules")]
+                                  "cache_keys", "follow_start", "follow_next", "kept_rules", "raw_off", "raw")] + [
+        ("n_raw", C.c_int32), ("finals", C.c_void_p), ("rule_start", C.c_void_p)]
 
 
 class gm_cache_stats(C.Structure):

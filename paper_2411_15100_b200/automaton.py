@@ -346,6 +346,13 @@ class CompiledTables:
     follow_next: np.ndarray  # int32[n_fstates*n_classes]
     n_fstates: int
     stats: dict = field(default_factory=dict)
+    # per-rule DFAs before the pre-closure (bundle export, bundle_io.py):
+    # node u's edges raw[raw_off[u]:raw_off[u+1]] as (symbol, dst) rows,
+    # symbol >= 0 a byte class, < 0 a call of rule -(symbol+1)
+    raw_off: Optional[np.ndarray] = None
+    raw: Optional[np.ndarray] = None
+    finals: Optional[np.ndarray] = None
+    rule_start: Optional[np.ndarray] = None
 
 
 def build_tables(g: ParsedGrammar, opts: Optional[AutomatonOptions] = None) -> CompiledTables:
@@ -513,6 +520,15 @@ def build_tables(g: ParsedGrammar, opts: Optional[AutomatonOptions] = None) -> C
         follow_next=f_next,
         n_fstates=n_f,
     )
+    raw_off, raw = [0], []
+    for u in range(n_nodes):
+        raw += [(c, d) for c, d in sorted(trans_n[u].items())]
+        raw += [(-(q + 1), ret) for q, ret in calls_n[u]]
+        raw_off.append(len(raw))
+    t.raw_off = np.asarray(raw_off, dtype=np.int32)
+    t.raw = np.asarray(raw, dtype=np.int32).reshape(-1, 2) if raw else np.zeros((0, 2), dtype=np.int32)
+    t.finals = np.asarray(final_n, dtype=np.uint8)
+    t.rule_start = np.asarray([rule_start[r] for r in range(n_rules)], dtype=np.int32)
     t.stats = {
         "nodes": n_nodes,
         "rules": n_rules,
@@ -701,6 +717,10 @@ def build_tables_native(g: ParsedGrammar, opts: Optional[AutomatonOptions] = Non
             follow_next=arr(v.follow_next, max(v.n_fstates, 1) * v.n_classes, C.c_int32, np.int32),
             n_fstates=v.n_fstates,
         )
+        t.raw_off = arr(v.raw_off, v.n_nodes + 1, C.c_int32, np.int32)
+        t.raw = arr(v.raw, 2 * v.n_raw, C.c_int32, np.int32).reshape(-1, 2)
+        t.finals = arr(v.finals, v.n_nodes, C.c_uint8, np.uint8)
+        t.rule_start = arr(v.rule_start, v.n_rules, C.c_int32, np.int32)
     finally:
         lib.gm_front_end_release(h)
     t.stats = {

@@ -29,8 +29,8 @@ from .grammar import GrammarError
 from .matcher import SlotMatcher
 from .vocab import Vocabulary
 
-__all__ = ["CompileOptions", "Bundle", "compile_bundle", "TokenMask", "Matcher", "MatcherError",
-           "GrammarError", "StateLimitError"]
+__all__ = ["CompileOptions", "Bundle", "compile_bundle", "load_bundle", "save_bundle", "TokenMask", "Matcher",
+           "MatcherError", "GrammarError", "StateLimitError"]
 
 
 @dataclass
@@ -73,7 +73,16 @@ class Bundle:
     vocab_hash: bytes
     vocab_size: int
     options: CompileOptions
-    compiled: object  # engine.CompiledDeviceGrammar
+    compiled: object  # engine.CompiledDeviceGrammar; None until a Matcher binds a vocabulary (load_bundle)
+    image: object = None  # bundle_io.BundleImage of a loaded GMB1 file (save_bundle writes it back verbatim)
+
+    def ensure_compiled(self, vocab: Vocabulary):
+        """Device-compile a loaded bundle's grammar for ``vocab`` (once)."""
+        if self.compiled is None:
+            aopts = AutomatonOptions(inline=self.options.inline, ctx_expansion=self.options.ctx_expansion)
+            self.compiled = compile_on_device(self.grammar_text, device_vocab(vocab), aopts,
+                                              uncached=not self.options.cache)
+        return self.compiled
 
     @property
     def stats(self) -> dict:
@@ -93,6 +102,78 @@ def compile_bundle(grammar_text: str, vocab: Vocabulary, options: Optional[Compi
     dv = device_vocab(vocab)
     dev = compile_on_device(grammar_text, dv, aopts, group=group, uncached=not opts.cache)
     return Bundle(grammar_text, vocab.content_hash(), vocab.size, opts, dev)
+
+
+def _options_from_flags(flags: int) -> CompileOptions:
+    from .bundle_io import FLAG_CACHE, FLAG_CTX, FLAG_INLINE, FLAG_MERGE
+
+    return CompileOptions(inline=bool(flags & FLAG_INLINE), merge=bool(flags & FLAG_MERGE),
+                          cache=bool(flags & FLAG_CACHE), ctx_expansion=bool(flags & FLAG_CTX))
+
+
+def load_bundle(data: bytes) -> Bundle:
+    """Read a GMB1 bundle (REF bundle.py:186-206).  The engine needs its
+    normalized grammar text and option flags; the grammar is compiled on the
+    device when a Matcher binds a vocabulary (the vocabulary hash is checked
+    first, as the reference does).  The file's automaton and GMC1 sections
+    are kept, so save_bundle returns the same bytes."""
+    from .bundle_io import read_bundle
+
+    img = read_bundle(data)
+    return Bundle(img.grammar_text, img.vocab_hash, img.vocab_size, _options_from_flags(img.flags), None, img)
+
+
+def save_bundle(bundle: Bundle) -> bytes:
+    """GMB1 bytes of a bundle (REF bundle.py:167-183).  A loaded bundle is
+    written back verbatim; one compiled here is exported with this engine's
+    automaton as the PDA section (per-rule DFAs: byte-range and rule-call
+    edges, rule starts and finals) and its device cache as the GMC1 section
+    (per cache-key node: accepted / rejected / dependent ids in the adaptive
+    byte-minimal encoding).  Deterministic for identical inputs."""
+    from . import bundle_io as bio
+
+    if bundle.image is not None:
+        return bio.write_bundle(bundle.image)
+    dev = bundle.compiled
+    t = dev.tables
+    o = bundle.options
+    flags = ((bio.FLAG_INLINE if o.inline else 0) | (bio.FLAG_MERGE if o.merge else 0) |
+             (bio.FLAG_CACHE if o.cache else 0) | (bio.FLAG_CTX if o.ctx_expansion else 0))
+    class_bytes = [0] * t.n_classes
+    for b in range(256):
+        class_bytes[int(t.byte_class[b])] |= 1 << b
+    edges = []
+    for u in range(t.n_nodes):
+        rows = t.raw[int(t.raw_off[u]):int(t.raw_off[u + 1])]
+        by_dst: dict = {}
+        for sym, dst in rows:
+            if sym >= 0:
+                by_dst[int(dst)] = by_dst.get(int(dst), 0) | class_bytes[int(sym)]
+        for dst in sorted(by_dst):
+            edges.append((u, dst, bio.EDGE_CHAR, bio.byte_ranges(by_dst[dst])))
+        for sym, dst in rows:
+            if sym < 0:
+                edges.append((u, int(dst), bio.EDGE_RULE, int(-sym - 1)))
+    rules = []
+    for r in range(t.n_rules):
+        finals = [u for u in range(t.n_nodes) if t.node_rule[u] == r and t.finals[u]]
+        rules.append((t.rule_names[r], int(t.rule_start[r]), finals))
+    pda = bio.PdaImage([int(x) for x in t.node_rule], edges, rules, int(t.root_rule))
+    cache = None
+    if o.cache:
+        v = dev.dvocab.vocab
+        acc_rows, dep_off, dep_ids = dev.cache.export()
+        acc_bits = np.unpackbits(acc_rows.cpu().numpy().view(np.uint8), axis=1, bitorder="little")[:, : v.size]
+        universe = np.asarray([i for i in range(v.size) if i not in v.special_tokens], dtype=np.uint32)
+        entries = {}
+        for k, node in enumerate(t.cache_keys):
+            acc = np.nonzero(acc_bits[k])[0].astype(np.uint32)
+            dep = np.asarray(dep_ids[dep_off[k]:dep_off[k + 1]], dtype=np.uint32)
+            rej = np.setdiff1d(universe, np.concatenate([acc, dep]))
+            entries[int(node)] = bio.choose_storage(acc, rej, dep, v.size)
+        cache = bio.CacheImage(v.size, entries)
+    return bio.write_bundle(bio.BundleImage(flags, bundle.vocab_size, bundle.vocab_hash, bundle.grammar_text, pda,
+                                            cache))
 
 
 class TokenMask:
@@ -163,6 +244,8 @@ class Matcher:
         del branch_cap, dependent_sweep_threshold  # device walker limits are fixed
         self._bundle = bundle
         self._v = vocab
+        if _core is None:
+            bundle.ensure_compiled(vocab)
         self._core = _core if _core is not None else SlotMatcher(_CompiledHandle(bundle.compiled), history_window)
         self._closed = False
         self._row = torch.empty((1, (vocab.size + 31) // 32), dtype=torch.int32, device=self._core.pool.device)

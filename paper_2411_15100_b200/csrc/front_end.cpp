@@ -391,6 +391,10 @@ struct Result {
   std::vector<uint8_t> byte_class;
   std::vector<int32_t> trans_off, trans, push_pool, node_rule, cache_keys, follow_start, follow_next, kept;
   std::vector<uint8_t> node_flags;
+  // the per-rule DFAs before the pre-closure (bundle export): per node
+  // (symbol, dst) with symbol >= 0 a byte class, < 0 a call of rule -(sym+1)
+  std::vector<int32_t> raw_off, raw, rule_start;
+  std::vector<uint8_t> finals;
 };
 
 void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_options& o, Result& R) {
@@ -517,6 +521,14 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
   }
   const int root_n = new_rid[root_in];
   const int start_node = rule_start[root_n];
+  R.raw_off.assign(1, 0);
+  for (int u = 0; u < n_nodes; ++u) {
+    for (auto& e : trans_n[u]) { R.raw.push_back(e.first); R.raw.push_back(e.second); }
+    for (auto& e : calls_n[u]) { R.raw.push_back(-(e.first + 1)); R.raw.push_back(e.second); }
+    R.raw_off.push_back((int32_t)(R.raw.size() / 2));
+    R.finals.push_back((uint8_t)final_n[u]);
+  }
+  R.rule_start.assign(rule_start.begin(), rule_start.end());
   std::vector<char> dead_end(n_nodes);
   for (int u = 0; u < n_nodes; ++u) dead_end[u] = final_n[u] && trans_n[u].empty() && calls_n[u].empty();
 
@@ -766,6 +778,11 @@ extern "C" gm_status gm_front_end_build(const int32_t* ir, int64_t ir_len, int32
   view->follow_start = R.follow_start.data();
   view->follow_next = R.follow_next.data();
   view->kept_rules = R.kept.data();
+  view->raw_off = R.raw_off.data();
+  view->raw = R.raw.data();
+  view->n_raw = (int32_t)(R.raw.size() / 2);
+  view->finals = R.finals.data();
+  view->rule_start = R.rule_start.data();
   *out = fe;
   return GM_OK;
 }

@@ -149,7 +149,7 @@ def test_native_front_end_tables_identical():
         texts[f"schema{k}"] = schema_to_grammar_text(json.dumps(sc))
     fields = ["n_nodes", "n_rules", "n_classes", "start_node", "root_rule", "rule_names", "byte_class", "trans_off",
               "trans", "push_pool", "node_flags", "node_rule", "cache_keys", "follow_start", "follow_next",
-              "n_fstates"]
+              "n_fstates", "raw_off", "raw", "finals", "rule_start"]
     for opts in (AutomatonOptions(), AutomatonOptions(inline=False), AutomatonOptions(ctx_expansion=False)):
         for name, text in texts.items():
             g = parse_grammar(text)

@@ -11,6 +11,9 @@ dependency chain with no gaps.
 
     step = DecodeStepGraph(matchers, bitmask, logits_buffers)
     accepted = step.run(host_token_ids, buffer_index)   # pinned uint8 [B]
+
+With one buffer per in-flight step (``len(logits_buffers)``), steps queue
+back to back (``wait=False``) without host syncs.
 """
 
 from __future__ import annotations
@@ -40,46 +43,58 @@ class DecodeStepGraph:
         B = len(matchers)
         self.B = B
         self.slots = torch.tensor([m.slot for m in matchers], dtype=torch.int32, device=dev)
-        self.tokens_host = torch.zeros(B, dtype=torch.int32).pin_memory()
-        self.accepted_host = torch.zeros(B, dtype=torch.uint8).pin_memory()
-        self.tokens = torch.zeros(B, dtype=torch.int32, device=dev)
-        self.accepted = torch.zeros(B, dtype=torch.uint8, device=dev)
-        self.bitmask = bitmask
+        n = len(logits)
+        # per logits buffer: its own pinned staging (token ids in, accepted
+        # flags out) and device buffers, so step s+1 can be queued while step
+        # s is still in flight; an event per buffer guards the reuse of its
+        # staging n steps later
+        self.tokens_host = [torch.zeros(B, dtype=torch.int32).pin_memory() for _ in range(n)]
+        self.accepted_host = [torch.zeros(B, dtype=torch.uint8).pin_memory() for _ in range(n)]
+        self.tokens = [torch.zeros(B, dtype=torch.int32, device=dev) for _ in range(n)]
+        self.accepted = [torch.zeros(B, dtype=torch.uint8, device=dev) for _ in range(n)]
+        self.done = [torch.cuda.Event() for _ in range(n)]
+        self._tok_np = [t.numpy() for t in self.tokens_host]  # host writes without a torch op
+        # one bitmask for all steps, or one per logits buffer
+        self.bitmasks = list(bitmask) if isinstance(bitmask, (list, tuple)) else [bitmask] * n
+        self.bitmask = self.bitmasks[0]
         self.logits = list(logits)
         self.recycle = recycle
         self.stream = stream or torch.cuda.Stream(device=dev)
         # warm up outside capture (one-time kernel attribute setup): a
         # fill-only step into scratch buffers leaves the matchers unchanged
         with torch.cuda.stream(self.stream):
-            scratch_mask = torch.empty_like(bitmask) if bitmask is not None else None
+            scratch_mask = torch.empty_like(self.bitmask) if self.bitmask is not None else None
             scratch_logits = torch.empty((B, 8), dtype=self.logits[0].dtype, device=dev)
             batch_step(pool, self.slots, None, None, scratch_mask, scratch_logits, stream=self.stream)
         self.stream.synchronize()
         self.graphs = []
-        for buf in self.logits:
+        for i, buf in enumerate(self.logits):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.stream):
-                self.tokens.copy_(self.tokens_host, non_blocking=True)
-                batch_step(pool, self.slots, self.tokens, self.accepted, bitmask, buf, recycle=recycle,
+                self.tokens[i].copy_(self.tokens_host[i], non_blocking=True)
+                batch_step(pool, self.slots, self.tokens[i], self.accepted[i], self.bitmasks[i], buf, recycle=recycle,
                            stream=self.stream)
-                self.accepted_host.copy_(self.accepted, non_blocking=True)
+                self.accepted_host[i].copy_(self.accepted[i], non_blocking=True)
             self.graphs.append(g)
 
     def first(self, i: int = 0) -> None:
         """First step of a batch: fill + apply only (no token to accept)."""
         with torch.cuda.stream(self.stream):
-            batch_step(get_pool(), self.slots, None, None, self.bitmask, self.logits[i], stream=self.stream)
+            batch_step(get_pool(), self.slots, None, None, self.bitmasks[i], self.logits[i], stream=self.stream)
 
     def run(self, tokens, i: int = 0, wait: bool = True) -> torch.Tensor:
         """Accept ``tokens`` (host ints), fill + apply into logits buffer i.
-        Returns the pinned accepted flags (valid after the stream syncs;
-        ``wait`` syncs before returning)."""
+        Returns buffer i's pinned accepted flags (valid once the stream has
+        passed this step: ``wait`` syncs before returning, else
+        ``self.done[i]``).  Steps may be queued back to back: buffer i's
+        staging is reused only after its previous replay has completed."""
+        self.done[i].synchronize()
         if isinstance(tokens, torch.Tensor):
-            self.tokens_host.copy_(tokens.to(torch.int32))
-        else:
-            self.tokens_host.numpy()[:] = np.asarray(tokens, dtype=np.int32)
+            tokens = tokens.numpy() if tokens.device.type == "cpu" else tokens.cpu().numpy()
+        np.copyto(self._tok_np[i], np.asarray(tokens), casting="unsafe")
         with torch.cuda.stream(self.stream):  # replay() launches on the current stream
             self.graphs[i].replay()
+            self.done[i].record(self.stream)
         if wait:
             self.stream.synchronize()
-        return self.accepted_host
+        return self.accepted_host[i]

@@ -439,7 +439,7 @@ def test_decode_step_graph_equals_eager():
             batch_step(pool, s_ref, torch.tensor(toks, dtype=torch.int32, device="cuda"), acc_ref, bm_ref, la,
                        recycle=True)
             acc = step.run(toks, i)
-            assert acc.tolist() == acc_ref.tolist(), (it, toks, acc.tolist(), acc_ref.tolist(), step.tokens.tolist())
+            assert acc.tolist() == acc_ref.tolist(), (it, toks, acc.tolist(), acc_ref.tolist(), step.tokens[i].tolist())
         torch.cuda.synchronize()
         step.stream.synchronize()
         assert torch.equal(bm_ref, bm_new), it
@@ -449,4 +449,63 @@ def test_decode_step_graph_equals_eager():
         for r in range(B):
             ids = allowed[r, :vocab.size].nonzero().flatten().tolist()
             toks.append(vocab.eos_id if (vocab.eos_id in ids and rng.random() < 0.5) else rng.choice(ids))
+    pool.check()
+
+
+def test_decode_step_graph_queued_back_to_back():
+    """Steps queued without host syncs (wait=False, 3 buffers reused over 14
+    steps) give the same accepted flags and masks as eager batch_step."""
+    import torch
+
+    import paper_2411_15100_b200 as gm
+    from paper_2411_15100_b200.engine import get_pool
+    from paper_2411_15100_b200.graph import DecodeStepGraph
+    from paper_2411_15100_b200.matcher import batch_step
+
+    vocab = vocab_by_name("4000:mixed")
+    info = gm.TokenizerInfo.from_vocabulary(vocab)
+    compiled = gm.GrammarCompiler(info).compile_builtin_json_grammar()
+    B, W, n_buf, S = 5, (vocab.size + 31) // 32, 3, 14
+    pool = get_pool()
+    ref = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    s_ref = torch.tensor([m.slot for m in ref], dtype=torch.int32, device="cuda")
+    bm = torch.empty((B, W), dtype=torch.int32, device="cuda")
+    acc = torch.empty(B, dtype=torch.uint8, device="cuda")
+    lg = torch.zeros(B, vocab.size, device="cuda", dtype=torch.bfloat16)
+    rng = random.Random(11)
+    toks, masks, accs = [None], [], []
+    for s in range(S):
+        batch_step(pool, s_ref, None if s == 0 else torch.tensor(toks[s], dtype=torch.int32, device="cuda"),
+                   None if s == 0 else acc, bm, lg, recycle=True)
+        masks.append(bm.clone())
+        accs.append(acc.tolist() if s else None)
+        allowed = ((bm.unsqueeze(-1) >> torch.arange(32, device="cuda", dtype=torch.int32)) & 1).reshape(B, -1)
+        nxt = []
+        for r in range(B):
+            ids = allowed[r, :vocab.size].nonzero().flatten().tolist()
+            nxt.append(rng.choice(ids))
+        toks.append(nxt)
+    new = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    bms = [torch.empty((B, W), dtype=torch.int32, device="cuda") for _ in range(n_buf)]
+    bufs = [torch.zeros(B, vocab.size, device="cuda", dtype=torch.bfloat16) for _ in range(n_buf)]
+    step = DecodeStepGraph(new, bms, bufs, recycle=True)
+
+    def check(s):
+        i = s % n_buf
+        step.done[i].synchronize()
+        assert torch.equal(bms[i], masks[s]), s
+        if s:
+            assert step.accepted_host[i].tolist() == accs[s], s
+
+    for s in range(S):
+        if s >= n_buf:
+            check(s - n_buf)
+        if s == 0:
+            step.first(0)
+            step.done[0].record(step.stream)
+        else:
+            step.run(toks[s], s % n_buf, wait=False)
+    step.stream.synchronize()
+    for s in range(S - n_buf, S):
+        check(s)
     pool.check()

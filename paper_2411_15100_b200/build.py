@@ -54,6 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     nvcc = _nvcc()
     BUILD.mkdir(exist_ok=True)
     include = ["-I", str(ROOT / "include"), "-I", str(CSRC)]
+    if os.environ.get("GMASK_PROBES") == "1":  # debug: K5 dry-walk / load-latency probes (GMASK_TRACE=1)
+        include += ["-DGM_TRACE_PROBES"]
     if os.environ.get("GMASK_VERIFY") == "1":  # debug: cross-check cached arena keys
         include += ["-DGM_VERIFY_KNOWN"]
 

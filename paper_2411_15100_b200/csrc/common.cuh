@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/gmask.h"
 
@@ -27,5 +29,44 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 #define GM_LAUNCH_CHECK() GM_CUDA_TRY(cudaGetLastError())
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch (PDL).  The per-step kernels (apply, fill,
+// accept, step, recycle) are launched with programmatic stream
+// serialization: the launch, CTA rasterisation and prologue of kernel k+1
+// overlap the drain of kernel k in the same stream (measured ~2 us per
+// launch on B200, tools/bwprobe.cu).  Each such kernel calls pdl_trigger()
+// then pdl_wait() before its first global-memory access, so every read and
+// write still happens after the previous kernel has completed and its
+// memory is visible — stream order is preserved.  GMASK_NO_PDL=1 disables
+// the attribute (plain launches; the griddepcontrol instructions are then
+// no-ops).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GMASK_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
 
 }  // namespace gm

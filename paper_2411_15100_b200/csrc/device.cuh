@@ -476,9 +476,10 @@ struct RWalker {
   const int32_t* xh;
   const unsigned long long* xk;
   int nx;
+  int nload;  // arena loads issued (diagnostics)
 
   __device__ __forceinline__ void init(const int32_t* ch, const unsigned long long* ck, int nc) {
-    n = 0; nf = 0; spill = false; err = 0;
+    n = 0; nf = 0; spill = false; err = 0; nload = 0;
     xh = ch; xk = ck; nx = nc;
   }
 
@@ -490,8 +491,9 @@ struct RWalker {
     return -2 - h;
   }
 
-  __device__ __forceinline__ unsigned long long global_key(const DevArena& A, int32_t r) const {
+  __device__ __forceinline__ unsigned long long global_key(const DevArena& A, int32_t r) {
     if (r >= kChainRef) return xk[r - kChainRef];
+    ++nload;
     return arena_load(A, -2 - r);
   }
 
@@ -505,7 +507,7 @@ struct RWalker {
     pr = p < 0 ? -1 : -2 - p;
   }
 
-  __device__ __forceinline__ uint32_t term_of(const DevArena& A, int32_t r) const {
+  __device__ __forceinline__ uint32_t term_of(const DevArena& A, int32_t r) {
     if (r == -1) return 1u;
     if (r >= 0 && r < kChainRef) return fterm[r];
     return key_term(global_key(A, r));

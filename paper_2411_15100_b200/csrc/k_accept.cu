@@ -23,6 +23,8 @@ accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t
   __shared__ SlotHdr hd;
   __shared__ int4 s_rec[2];
   __shared__ RingPos rp;
+  pdl_trigger();
+  pdl_wait();
   const int32_t i = blockIdx.x;
   if (i >= n) return;
   trace_mark(P, 0, 0);
@@ -92,6 +94,8 @@ __global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32
 // Request recycling for serving loops: a terminated slot restarts at the
 // grammar's start state (fresh request, same grammar), others are untouched.
 __global__ void recycle_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n) {
+  pdl_trigger();
+  pdl_wait();
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int32_t slot = slots[i];
@@ -187,8 +191,7 @@ gm_status launch_accept_tokens(const DevPool& P, const int32_t* slots, const int
   if (n <= 0) return GM_OK;
   static gm_status once = set_smem_attr(reinterpret_cast<const void*>(accept_tokens_kernel));
   if (once) return once;
-  accept_tokens_kernel<<<n, kAccThreads, kStageBytes, s>>>(P, slots, toks, n, acc);
-  GM_LAUNCH_CHECK();
+  GM_CUDA_TRY(launch_pdl(accept_tokens_kernel, dim3(n), dim3(kAccThreads), kStageBytes, s, P, slots, toks, n, acc));
   return GM_OK;
 }
 gm_status launch_accept_bytes(const DevPool& P, int32_t slot, const uint8_t* data, int64_t len, uint8_t* acc,
@@ -207,8 +210,7 @@ gm_status launch_reset(const DevPool& P, int32_t slot, const DevBinding* b, int3
 }
 gm_status launch_recycle(const DevPool& P, const int32_t* slots, int32_t n, cudaStream_t s) {
   if (n <= 0) return GM_OK;
-  recycle_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(P, slots, n);
-  GM_LAUNCH_CHECK();
+  GM_CUDA_TRY(launch_pdl(recycle_kernel, dim3((unsigned)ceil_div(n, 128)), dim3(128), 0, s, P, slots, n));
   return GM_OK;
 }
 gm_status launch_rollback(const DevPool& P, const int32_t* slots, const int32_t* steps, int32_t n, cudaStream_t s) {

@@ -97,6 +97,8 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   __shared__ int2 s_top[32];
   __shared__ int s_cj[32];
   __shared__ __align__(8) unsigned long long rows_bar;
+  pdl_trigger();
+  pdl_wait();
   const int32_t i = blockIdx.x;
   if (i >= n) return;
   const int32_t split = blockIdx.y, n_split = gridDim.y;
@@ -123,6 +125,12 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     const bool in_range = tok >= 0 && tok < hd.V;
     if (threadIdx.x < 2 && in_range) s_rec[threadIdx.x] = __ldg(hd.tokrec + 2 * (size_t)tok + threadIdx.x);
     Gs = stage_blob(hd.blob, hd.blob_bytes, tables);  // barrier inside
+    if (P.trace && i == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      P.trace[49] = t;
+      P.trace[50] = (unsigned long long)hd.blob_bytes;
+    }
     if (threadIdx.x == 0) {
       int acc = 0;
       const bool was_term = hd.flags & 1;
@@ -131,6 +139,57 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       } else {
         const int4 e = s_rec[0], inl = s_rec[1];
         const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;
+#ifdef GM_TRACE_PROBES
+        if (P.trace && i == 0 && hd.ntops > 0) {  // diagnostic: dry walk of the same token, timed
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          auto clk = []() { long long t; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) :: "memory"); return t; };
+          {  // load-latency probes: generic load of the staged table, its 2nd load, a plain smem load
+            const volatile uint8_t* bc = Gs.byte_class;
+            long long a0 = clk();
+            uint32_t v0 = bc[rec_byte(inl, far, 0)];
+            asm volatile("" :: "r"(v0) : "memory");
+            long long a1 = clk();
+            uint32_t v1 = bc[(v0 + 7) & 255];
+            asm volatile("" :: "r"(v1) : "memory");
+            long long a2 = clk();
+            const volatile int32_t* sk = s_key;
+            uint32_t v2 = sk[(v1 + 3) & 31];
+            asm volatile("" :: "r"(v2) : "memory");
+            long long a3 = clk();
+            const volatile int32_t* fst = Gs.fast;
+            uint32_t v3 = fst[(v2 + v1) & 63];
+            asm volatile("" :: "r"(v3) : "memory");
+            long long a4 = clk();
+            P.trace[46] = (unsigned long long)(a1 - a0) | ((unsigned long long)(a2 - a1) << 16) |
+                          ((unsigned long long)(a3 - a2) << 32) | ((unsigned long long)(a4 - a3) << 48);
+            P.trace[47] = v0 + v1 + v2 + v3;
+          }
+          RWalker<kAccR, kAccRF> rw;
+#pragma unroll 1
+          for (int it = 0; it < 2; ++it) {
+            long long c0 = clock64();
+            rw.init(hd.chain_h, hd.chain_k, hd.nchain);
+            for (int s = 0; s < hd.ntops && s < kAccR; ++s) rw.add(rw.ref_of_handle(hd.top[s].x), hd.top[s].y);
+            long long c1 = clock64();
+            P.trace[54 + 5 * it] = (unsigned long long)(c1 - c0);
+            for (int b = 0; b < e.y && rw.n > 0 && !rw.spill; ++b) {
+              bool pb = false;
+              rw.step(Gs, P.arena, rec_byte(inl, far, b), &pb);
+              const long long c2 = clock64();
+              if (b < 4) P.trace[55 + 5 * it + b] = (unsigned long long)(c2 - c1);
+              c1 = c2;
+            }
+          }
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          P.trace[51] = t1 - t0;
+          P.trace[52] = (unsigned long long)rw.n | ((unsigned long long)e.y << 32);
+          P.trace[53] = (unsigned long long)rw.nload | ((unsigned long long)rw.nf << 16) |
+                        ((unsigned long long)rw.spill << 32) | ((unsigned long long)hd.nchain << 40) |
+                        ((unsigned long long)(hd.top[0].x == hd.chain_h[0]) << 48);
+          P.trace[49] = t1;
+        }
+#endif
         acc = accept_one(P, slot, rp, hd, Gs, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
                          tok == hd.eos, e.x != 0, &hd);
       }
@@ -400,10 +459,9 @@ gm_status launch_fill(const DevPool& P, const int32_t* slots, int32_t n, int32_t
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
   static gm_status attrs = fill_attrs<false, false>();
   if (attrs) return attrs;
-  fill_kernel<false, false><<<dim3(n, splits), kFillThreads, smem, s>>>(
-      P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows, need_apply, Wp, nullptr, 0, 0, 2, 0u,
-      StepArgs{nullptr, nullptr, 0});
-  GM_LAUNCH_CHECK();
+  GM_CUDA_TRY(launch_pdl(fill_kernel<false, false>, dim3(n, splits), dim3(kFillThreads), smem, s, P, slots, n,
+                         reinterpret_cast<uint32_t*>(bitmask), bstride, rows, need_apply, Wp, nullptr, (int64_t)0,
+                         (int64_t)0, 2, 0u, StepArgs{nullptr, nullptr, 0}));
   return GM_OK;
 }
 
@@ -418,10 +476,9 @@ gm_status launch_fill_apply(const DevPool& P, const int32_t* slots, int32_t n, i
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
   static gm_status attrs = fill_attrs<true, false>();
   if (attrs) return attrs;
-  fill_kernel<true, false><<<dim3(n, splits), kFillThreads, smem, s>>>(
-      P, slots, n, reinterpret_cast<uint32_t*>(bitmask), bstride, rows, nullptr, Wp, static_cast<char*>(logits),
-      lstride_bytes, vocab, eb, neg, StepArgs{nullptr, nullptr, 0});
-  GM_LAUNCH_CHECK();
+  GM_CUDA_TRY(launch_pdl(fill_kernel<true, false>, dim3(n, splits), dim3(kFillThreads), smem, s, P, slots, n,
+                         reinterpret_cast<uint32_t*>(bitmask), bstride, rows, nullptr, Wp, static_cast<char*>(logits),
+                         lstride_bytes, vocab, (int)eb, neg, StepArgs{nullptr, nullptr, 0}));
   return GM_OK;
 }
 
@@ -439,14 +496,14 @@ gm_status launch_step(const DevPool& P, const int32_t* slots, int32_t n, const i
   if (logits) {
     static gm_status attrs = fill_attrs<true, true>();
     if (attrs) return attrs;
-    fill_kernel<true, true><<<dim3(n, 1), kFillThreads, smem, s>>>(P, slots, n, bm, bstride, rows, nullptr,
-                                                                   split_words(Wmax, 1), static_cast<char*>(logits),
-                                                                   lstride_bytes, vocab, eb, neg, sa);
+    GM_CUDA_TRY(launch_pdl(fill_kernel<true, true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm, bstride,
+                           rows, nullptr, split_words(Wmax, 1), static_cast<char*>(logits), lstride_bytes, vocab,
+                           (int)eb, neg, sa));
   } else {
     static gm_status attrs = fill_attrs<false, true>();
     if (attrs) return attrs;
-    fill_kernel<false, true><<<dim3(n, 1), kFillThreads, smem, s>>>(P, slots, n, bm, bstride, rows, nullptr,
-                                                                    split_words(Wmax, 1), nullptr, 0, 0, 2, 0u, sa);
+    GM_CUDA_TRY(launch_pdl(fill_kernel<false, true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm,
+                           bstride, rows, nullptr, split_words(Wmax, 1), nullptr, (int64_t)0, (int64_t)0, 2, 0u, sa));
   }
   GM_LAUNCH_CHECK();
   return GM_OK;

@@ -84,6 +84,17 @@ def main(steps=12, flush=True, fused=False, grammar="json", step_mode=False):
             print(f"step {s:2d} K5 CTA0 phases(us): header {d[0]:.2f} accept {d[1]:.2f} setup {d[2]:.2f} "
                   f"stage+ctx {d[3]:.2f} walks {d[4]:.2f} barrier {d[5]:.2f} merge {d[6]:.2f} "
                   f"deps={buf[24]} ntops={buf[26]}")
+            a = [buf[17], buf[49], buf[3], buf[4], buf[5], buf[48]]
+            da = [(a[k + 1] - a[k]) / 1e3 if a[k + 1] >= a[k] > 0 else float("nan") for k in range(5)]
+            print(f"         accept split(us): stage {da[0]:.2f} walk {da[1]:.2f} commit {da[2]:.2f} "
+                  f"publish {da[3]:.2f} tail {da[4]:.2f} blob_bytes={buf[50]} | dry walk {buf[51] / 1e3:.2f} us "
+                  f"(n={buf[52] & 0xFFFFFFFF}, len={buf[52] >> 32}, arena loads={buf[53] & 0xFFFF}, "
+                  f"frames={(buf[53] >> 16) & 0xFFFF}, spill={(buf[53] >> 32) & 0xFF}, nchain={(buf[53] >> 40) & 0xFF}, "
+                  f"top0=chain0:{(buf[53] >> 48) & 1}) cycles init {buf[54]} per byte {[buf[55 + b] for b in range(min(4, buf[52] >> 32))]} | 2nd: init {buf[59]} per byte {[buf[60 + b] for b in range(min(4, buf[52] >> 32))]}")
+            print(f"         load probes (cycles): generic smem {buf[46] & 0xFFFF}, again {(buf[46] >> 16) & 0xFFFF}, "
+                  f"LDS {(buf[46] >> 32) & 0xFFFF}, generic fast[] {(buf[46] >> 48) & 0xFFFF}")
+            for k in (3, 4, 5, 48, 49):
+                buf[k] = 0
             continue
         if flush:
             fl.zero_()

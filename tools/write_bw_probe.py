@@ -13,15 +13,29 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
+GRAPH = "--graph" in sys.argv
+
+
 def bracket(fn, n=200, warm=10):
     for i in range(warm):
         fn(i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for i in range(n):
-        fn(i)
-    e1.record()
+    if GRAPH:  # n launches captured once, replayed: device-side time per launch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(n):
+                fn(i)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+    else:
+        e0.record()
+        for i in range(n):
+            fn(i)
+        e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) * 1e3 / n  # us per launch
 
@@ -65,6 +79,23 @@ def main():
     f32 = [torch.zeros(B, V, dtype=torch.float32, device=dev) for _ in range(4)]
     rep("K0 fp32 all masked (65.7 MB)",
         bracket(lambda i: gm.apply_token_bitmask_inplace(f32[i % 4], zero_mask)), 2 * rows_b + 4 * B * W)
+    # real decode-step masks: JSON start-state rows and string-interior-like rows
+    if "--real" in sys.argv:
+        from paper_2411_15100_b200.engine import get_pool
+        from paper_2411_15100_b200.matcher import batch_fill
+        info = gm.TokenizerInfo.from_vocabulary(gm.synth_vocab(V))
+        comp = gm.GrammarCompiler(info).compile_builtin_json_grammar()
+        ms = [gm.GrammarMatcher(comp) for _ in range(B)]
+        for r, m in enumerate(ms[: B // 2]):
+            m.accept_string(b'{"k": "ab')
+        slots = torch.tensor([m.slot for m in ms], dtype=torch.int32, device=dev)
+        real = torch.empty(B, W, dtype=torch.int32, device=dev)
+        batch_fill(get_pool(), slots, real)
+        allowed = ((real.unsqueeze(-1) >> torch.arange(32, device=dev, dtype=torch.int32)) & 1).reshape(B, -1)[:, :V]
+        masked = int((allowed == 0).sum())
+        print(f"real masks: masked fraction {masked / (B * V):.3f}")
+        rep("K0 real masks (half string, half start)",
+            bracket(lambda i: gm.apply_token_bitmask_inplace(ring[i % 8], real)), 2 * masked + 4 * B * W)
     rep("torch masked_fill_ bf16 (bool mask, dense)",
         bracket(lambda i: ring[i % 8].masked_fill_(ring[(i + 1) % 8] > 10, float("-inf")), n=50),
         3 * rows_b)

@@ -413,53 +413,55 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     k0_b2b_ms = t_ev[2].elapsed_time(t_ev[3]) / (S - W0)
 
     # pass E2E — `e2e`: the same decode steps through the public serving API
-    # with host buffers, back to back in one bracket: per step
-    # DecodeStepGraph.run = pinned token ids H2D -> K5 -> accepted flags D2H
-    # (one CUDA graph per logits buffer, 8 in flight), and the host consumes
-    # the flags of step s-8 before reusing that buffer's staging
-    from paper_2411_15100_b200.graph import DecodeStepGraph
+    # with host buffers, back to back in one bracket: per step one
+    # DecodeLoop.step (native gm_decoder_step: host ids -> pinned staging ->
+    # H2D on a copy stream -> K5 -> accepted flags D2H, event-ordered, 8
+    # steps in flight), and the host reads the flags of step s-8 before that
+    # buffer is reused
+    from paper_2411_15100_b200.graph import DecodeLoop, DecodeStepGraph
 
     for m in matchers:
         m.reset()
     pinned_toks = torch.from_numpy(toks_h.copy()).pin_memory()
+    toks_np = np.ascontiguousarray(toks_h, dtype=np.int32)
     acc_host = np.zeros((S, B), dtype=np.uint8)
-    step_graph = DecodeStepGraph(matchers, bitmask, ring, recycle=True)
-    gs = step_graph.stream
+    loop = DecodeLoop(matchers, bitmask, ring, recycle=True)
+    gs = loop.stream
 
     def consume(s):
-        i = s % n_ring
-        step_graph.done[i].synchronize()
-        np.copyto(acc_host[s], step_graph.accepted_host[i].numpy())
+        loop.flags(s % n_ring, out=acc_host[s], wait=True)
 
     def e2e_step(s):
         if s >= n_ring + 1:
             consume(s - n_ring)
-        if s == 0:
-            step_graph.first(0)
-            step_graph.done[0].record(gs)
-        else:
-            step_graph.run(pinned_toks[s - 1], s % n_ring, wait=False)
+        loop.step(None if s == 0 else toks_np[s - 1], s % n_ring)
 
-    with torch.cuda.stream(gs):
-        for s in range(W0):
-            e2e_step(s)
-        gs.synchronize()
-        sync_ranks()
-        e_ev = ev()
-        e_ev[0].record(gs)
-        for s in range(W0, S):
-            e2e_step(s)
-        e_ev[1].record(gs)
-        gs.synchronize()
+    for s in range(W0):
+        e2e_step(s)
+    gs.synchronize()
+    sync_ranks()
+    e_ev = ev()
+    t_host = time.perf_counter()
+    e_ev[0].record(gs)
+    for s in range(W0, S):
+        e2e_step(s)
+    e_ev[1].record(gs)
+    t_host = time.perf_counter() - t_host
+    torch.cuda.synchronize()
     for s in range(max(W0, S - n_ring), S):
         consume(s)
+    loop.close()
     e2e_ms = e_ev[0].elapsed_time(e_ev[1]) / (S - W0)
+    e2e_host_us = t_host / (S - W0) * 1e6  # host time to issue one step (run() + reading flags)
     e2e_all_acc = bool(acc_host[W0:S].astype(bool).all())
 
-    # pass C — latency view of the same API: one graph step at a time with
-    # L2 flushed before it and a host sync after it
+    # pass C — latency view: DecodeStepGraph (H2D -> K5 -> D2H captured as
+    # one graph), one step at a time with L2 flushed before it and a host
+    # sync after it
     for m in matchers:
         m.reset()
+    step_graph = DecodeStepGraph(matchers, bitmask, ring, recycle=True)
+    gs = step_graph.stream
     g_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(S)]
     e2e_mism = torch.zeros((), dtype=torch.int64, device=dev)
     sync_ranks()
@@ -505,6 +507,7 @@ def run_ours(args, rank: int, world: int, group) -> dict:
         "k5_b2b_reps_us": [x * 1e3 for x in k5_rep_ms],
         "k0_b2b_us": mx(k0_b2b_ms * 1e3),
         "e2e_us": mx(e2e_ms * 1e3),
+        "e2e_host_us": e2e_host_us,
         "step_us": mx(statistics.fmean(step_ms) * 1e3),
         "separate_us": mx(statistics.fmean(sep_ms) * 1e3),
         "fill_us": mx(statistics.fmean(fill_ms) * 1e3),
@@ -787,9 +790,10 @@ def main():
                                             "replay)") if traffic else None,
                          "algorithmic_bytes_per_launch": algo_bytes},
             "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": B,
-                    "path": "DecodeStepGraph.run per decode step, K steps back to back in one bracket (one CUDA "
-                            "graph per logits buffer: pinned token ids H2D -> K5 -> accepted flags D2H; the host "
-                            "reads each step's flags)",
+                    "path": "DecodeLoop.step per decode step (native gm_decoder_step: host token ids -> pinned "
+                            "staging -> H2D on a copy stream -> K5 -> accepted flags D2H, event-ordered), K steps back "
+                            "to back in one bracket; the host reads every step's flags",
+                    "host_issue_us_per_step": r["e2e_host_us"],
                     "mask_mismatches_latency_pass": r["e2e_mask_mismatches"]},
             "gpu_launches": args.steps,
             "clocks": r["clocks_value"],

@@ -291,6 +291,35 @@ gm_status gm_step_tokens(gm_pool* p, const int32_t* slots, int32_t n,
                          void* logits, int32_t dtype, int64_t vocab_size,
                          int64_t logits_stride, void* stream);
 
+/* Native decode loop over gm_step_tokens with host buffers (the serving
+ * form of the reference's per-token accept_token -> fill_next_token_mask
+ * loop, REF matcher.py:273, 377, driven from the host as in REF bench.py:
+ * 287-338).  A decoder owns n_buf step slots; slot b has pinned host staging
+ * for the token ids and accepted flags, device copies, and its bitmask /
+ * logits buffers (device pointers, caller-owned; bitmasks may be NULL).
+ * gm_decoder_step(d, b, host_tokens, stream) issues one decode step without
+ * blocking: waits (host) until slot b's previous step has completed, copies
+ * host_tokens (int32[n], NULL = first step: fill + apply only) into slot b's
+ * staging, then H2D copy on the decoder's copy stream -> K5 (accept +
+ * recycle + fill + apply) on `stream` -> D2H copy of the accepted flags,
+ * ordered by events so the copies of neighbouring steps overlap the
+ * kernels.  gm_decoder_flags(d, b, out, wait) copies slot b's latest
+ * accepted flags (uint8[n]) to host memory `out` (wait = 1: block until
+ * that step completed; 0: caller already waited), returning GM_ERR_INVALID
+ * when the step has not completed and wait = 0. */
+typedef struct gm_decoder gm_decoder;
+gm_status gm_decoder_create(gm_pool* p, const int32_t* slots, int32_t n,
+                            int32_t n_buf, int32_t* const* bitmasks,
+                            int64_t bitmask_stride, void* const* logits,
+                            int32_t dtype, int64_t vocab_size,
+                            int64_t logits_stride, int32_t recycle,
+                            gm_decoder** out);
+gm_status gm_decoder_step(gm_decoder* d, int32_t buf,
+                          const int32_t* host_tokens, void* stream);
+gm_status gm_decoder_flags(gm_decoder* d, int32_t buf, uint8_t* out,
+                           int32_t wait);
+void gm_decoder_release(gm_decoder* d);
+
 /* rollback `steps` acceptances of each slot (REF matcher.py:310-326);
  * slots/steps are device int32[n]. */
 gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps,

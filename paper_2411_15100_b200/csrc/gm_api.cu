@@ -653,6 +653,134 @@ gm_status gm_step_tokens(gm_pool* p, const int32_t* slots, int32_t n, const int3
                      p->max_w, logits, eb, neg, vocab_size, logits_stride * eb, as_stream(stream));
 }
 
+// ---------------------------------------------------------------------------
+// Native decode loop (gm_decoder_*): per step one host memcpy into pinned
+// staging, H2D on an input copy stream, K5 on the caller's stream, D2H of
+// the accepted flags on an output copy stream — all ordered by events (so
+// step s+1's H2D overlaps step s's kernel), no host sync except the reuse
+// guard of a step slot.
+struct gm_decoder {
+  gm_pool* pool = nullptr;
+  const int32_t* slots = nullptr;
+  int32_t n = 0, n_buf = 0, recycle = 1, dtype = GM_DTYPE_BF16;
+  int64_t bstride = 0, vocab = 0, lstride = 0;
+  std::vector<int32_t*> bitmask;
+  std::vector<void*> logits;
+  std::vector<int32_t*> tok_host, tok_dev;
+  std::vector<uint8_t*> acc_host, acc_dev;
+  std::vector<cudaEvent_t> h2d, k5, done;
+  std::vector<int> issued;
+  cudaStream_t copy = nullptr;      // H2D of token ids
+  cudaStream_t copy_out = nullptr;  // D2H of accepted flags (separate: the next H2D must not queue behind it)
+};
+
+static void decoder_free(gm_decoder* d) {
+  if (!d) return;
+  if (d->copy) cudaStreamSynchronize(d->copy);
+  if (d->copy_out) cudaStreamSynchronize(d->copy_out);
+  for (auto e : d->h2d) if (e) cudaEventDestroy(e);
+  for (auto e : d->k5) if (e) cudaEventDestroy(e);
+  for (auto e : d->done) if (e) cudaEventDestroy(e);
+  for (auto q : d->tok_host) if (q) cudaFreeHost(q);
+  for (auto q : d->acc_host) if (q) cudaFreeHost(q);
+  for (auto q : d->tok_dev) if (q) cudaFree(q);
+  for (auto q : d->acc_dev) if (q) cudaFree(q);
+  if (d->copy) cudaStreamDestroy(d->copy);
+  if (d->copy_out) cudaStreamDestroy(d->copy_out);
+  delete d;
+}
+
+gm_status gm_decoder_create(gm_pool* p, const int32_t* slots, int32_t n, int32_t n_buf, int32_t* const* bitmasks,
+                            int64_t bitmask_stride, void* const* logits, int32_t dtype, int64_t vocab_size,
+                            int64_t logits_stride, int32_t recycle, gm_decoder** out) {
+  if (!p || !slots || n <= 0 || n_buf <= 0 || !out || !logits) return fail(GM_ERR_INVALID, "bad decoder arguments");
+  auto* d = new gm_decoder();
+  d->pool = p;
+  d->slots = slots;
+  d->n = n;
+  d->n_buf = n_buf;
+  d->recycle = recycle;
+  d->dtype = dtype;
+  d->bstride = bitmask_stride;
+  d->vocab = vocab_size;
+  d->lstride = logits_stride;
+  d->issued.assign(n_buf, 0);
+  auto bail = [&](cudaError_t e) {
+    decoder_free(d);
+    return fail(GM_ERR_CUDA, std::string("gm_decoder_create: ") + cudaGetErrorString(e));
+  };
+  cudaError_t e = cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return bail(e);
+  if ((e = cudaStreamCreateWithFlags(&d->copy_out, cudaStreamNonBlocking)) != cudaSuccess) return bail(e);
+  for (int32_t b = 0; b < n_buf; ++b) {
+    d->bitmask.push_back(bitmasks ? bitmasks[b] : nullptr);
+    d->logits.push_back(logits[b]);
+    int32_t *th = nullptr, *td = nullptr;
+    uint8_t *ah = nullptr, *ad = nullptr;
+    cudaEvent_t e1 = nullptr, e2 = nullptr, e3 = nullptr;
+    if ((e = cudaHostAlloc(&th, (size_t)n * 4, cudaHostAllocDefault)) != cudaSuccess) return bail(e);
+    d->tok_host.push_back(th);
+    if ((e = cudaHostAlloc(&ah, (size_t)n, cudaHostAllocDefault)) != cudaSuccess) return bail(e);
+    d->acc_host.push_back(ah);
+    if ((e = cudaMalloc(&td, (size_t)n * 4)) != cudaSuccess) return bail(e);
+    d->tok_dev.push_back(td);
+    if ((e = cudaMalloc(&ad, (size_t)n)) != cudaSuccess) return bail(e);
+    d->acc_dev.push_back(ad);
+    if ((e = cudaEventCreateWithFlags(&e1, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
+    d->h2d.push_back(e1);
+    if ((e = cudaEventCreateWithFlags(&e2, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
+    d->k5.push_back(e2);
+    if ((e = cudaEventCreateWithFlags(&e3, cudaEventDisableTiming)) != cudaSuccess) return bail(e);
+    d->done.push_back(e3);
+    std::memset(ah, 0, (size_t)n);
+  }
+  *out = d;
+  return GM_OK;
+}
+
+gm_status gm_decoder_step(gm_decoder* d, int32_t buf, const int32_t* host_tokens, void* stream) {
+  if (!d || buf < 0 || buf >= d->n_buf) return fail(GM_ERR_INVALID, "bad decoder slot");
+  cudaStream_t s = as_stream(stream);
+  if (d->issued[buf]) GM_CUDA_TRY(cudaEventSynchronize(d->done[buf]));  // staging reuse guard
+  const int32_t n = d->n;
+  if (host_tokens) {
+    std::memcpy(d->tok_host[buf], host_tokens, (size_t)n * 4);
+    GM_CUDA_TRY(cudaMemcpyAsync(d->tok_dev[buf], d->tok_host[buf], (size_t)n * 4, cudaMemcpyHostToDevice, d->copy));
+    GM_CUDA_TRY(cudaEventRecord(d->h2d[buf], d->copy));
+    GM_CUDA_TRY(cudaStreamWaitEvent(s, d->h2d[buf], 0));
+  }
+  gm_status st = gm_step_tokens(d->pool, d->slots, n, host_tokens ? d->tok_dev[buf] : nullptr,
+                                host_tokens ? d->acc_dev[buf] : nullptr, d->recycle, d->bitmask[buf], d->bstride,
+                                nullptr, d->logits[buf], d->dtype, d->vocab, d->lstride, stream);
+  if (st) return st;
+  GM_CUDA_TRY(cudaEventRecord(d->k5[buf], s));
+  GM_CUDA_TRY(cudaStreamWaitEvent(d->copy_out, d->k5[buf], 0));
+  if (host_tokens)
+    GM_CUDA_TRY(cudaMemcpyAsync(d->acc_host[buf], d->acc_dev[buf], (size_t)n, cudaMemcpyDeviceToHost, d->copy_out));
+  else
+    std::memset(d->acc_host[buf], 0, (size_t)n);
+  GM_CUDA_TRY(cudaEventRecord(d->done[buf], d->copy_out));
+  d->issued[buf] = 1;
+  return GM_OK;
+}
+
+gm_status gm_decoder_flags(gm_decoder* d, int32_t buf, uint8_t* out, int32_t wait) {
+  if (!d || buf < 0 || buf >= d->n_buf || !out) return fail(GM_ERR_INVALID, "bad decoder slot");
+  if (d->issued[buf]) {
+    if (wait) {
+      GM_CUDA_TRY(cudaEventSynchronize(d->done[buf]));
+    } else {
+      const cudaError_t q = cudaEventQuery(d->done[buf]);
+      if (q == cudaErrorNotReady) return fail(GM_ERR_INVALID, "decoder step not complete");
+      GM_CUDA_TRY(q);
+    }
+  }
+  std::memcpy(out, d->acc_host[buf], (size_t)d->n);
+  return GM_OK;
+}
+
+void gm_decoder_release(gm_decoder* d) { decoder_free(d); }
+
 gm_status gm_rollback(gm_pool* p, const int32_t* slots, const int32_t* steps, int32_t n, void* stream) {
   if (!p) return fail(GM_ERR_INVALID, "null pool");
   return launch_rollback(p->dev, slots, steps, n, as_stream(stream));

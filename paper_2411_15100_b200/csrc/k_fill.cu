@@ -112,7 +112,9 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   __shared__ int s_just_term;
   int32_t tok = -1;
   if (ACCEPT && SA.tokens) {
-    tok = __ldg(SA.tokens + i);
+    // volatile load: `tokens` may be pinned host memory written by the host
+    // between graph replays (zero-copy H2D, graph.py), never cached
+    asm volatile("ld.global.cv.s32 %0, [%1];" : "=r"(tok) : "l"(SA.tokens + i));
     load_header_ring(P, slot, &hd, &rp);
   } else {
     load_header(P, slot, &hd);

@@ -1,8 +1,8 @@
 """CUDA-graph capture of the per-decode-step grammar work.
 
 A serving loop advances a fixed batch of matchers once per generated token:
-copy the sampled token ids to the device, accept them, restart finished
-requests, fill the next masks and apply them to the logits buffer, and copy
+hand the sampled token ids to the device, accept them, restart finished
+requests, fill the next masks and apply them to the logits buffer, and hand
 the accepted flags back.  With static buffers every one of those operations
 has fixed arguments, so the whole step is captured once into a CUDA graph
 and replayed with a single launch — the host cost per step drops from the
@@ -37,7 +37,8 @@ class DecodeStepGraph:
     Bit-identical to the eager calls (same kernels, same arguments)."""
 
     def __init__(self, matchers: Sequence[GrammarMatcher], bitmask: Optional[torch.Tensor],
-                 logits: Sequence[torch.Tensor], recycle: bool = True, stream: Optional[torch.cuda.Stream] = None):
+                 logits: Sequence[torch.Tensor], recycle: bool = True, stream: Optional[torch.cuda.Stream] = None,
+                 zero_copy: bool = False):
         pool = get_pool()
         dev = pool.device
         B = len(matchers)
@@ -67,14 +68,25 @@ class DecodeStepGraph:
             scratch_logits = torch.empty((B, 8), dtype=self.logits[0].dtype, device=dev)
             batch_step(pool, self.slots, None, None, scratch_mask, scratch_logits, stream=self.stream)
         self.stream.synchronize()
+        # default: H2D copy -> K5 -> D2H copy.  zero_copy: the step kernel
+        # reads the token ids straight from the pinned host buffer (volatile
+        # loads over PCIe, unified addressing) and writes the accepted flags
+        # straight into pinned host memory — one launch, no copy engine, but
+        # measured ~10x slower per step on the B200 box (356 vs 38 us: each
+        # CTA's host access is a serialized PCIe round trip), so off.
+        self.zero_copy = zero_copy
         self.graphs = []
         for i, buf in enumerate(self.logits):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.stream):
-                self.tokens[i].copy_(self.tokens_host[i], non_blocking=True)
-                batch_step(pool, self.slots, self.tokens[i], self.accepted[i], self.bitmasks[i], buf, recycle=recycle,
-                           stream=self.stream)
-                self.accepted_host[i].copy_(self.accepted[i], non_blocking=True)
+                if zero_copy:
+                    batch_step(pool, self.slots, self.tokens_host[i], self.accepted_host[i], self.bitmasks[i], buf,
+                               recycle=recycle, stream=self.stream)
+                else:
+                    self.tokens[i].copy_(self.tokens_host[i], non_blocking=True)
+                    batch_step(pool, self.slots, self.tokens[i], self.accepted[i], self.bitmasks[i], buf,
+                               recycle=recycle, stream=self.stream)
+                    self.accepted_host[i].copy_(self.accepted[i], non_blocking=True)
             self.graphs.append(g)
 
     def first(self, i: int = 0) -> None:
@@ -98,3 +110,85 @@ class DecodeStepGraph:
         if wait:
             self.stream.synchronize()
         return self.accepted_host[i]
+
+
+class DecodeLoop:
+    """Native decode loop (C-ABI gm_decoder_*): per step the library copies
+    the host token ids into pinned staging, issues the H2D copy on its own
+    copy stream, K5 (accept + recycle + fill + apply) on ``stream`` and the
+    D2H copy of the accepted flags, ordered by events — no Python on the
+    per-step path beyond one ctypes call, and the copies of neighbouring
+    steps overlap the kernels.  ``len(logits)`` steps may be in flight.
+
+        loop = DecodeLoop(matchers, bitmasks, logits_buffers)
+        loop.step(None, 0)                 # first step: fill + apply
+        loop.step(host_token_ids, i)       # later steps (int32 numpy / list)
+        flags = loop.flags(i)              # uint8 [B], waits for step i
+    """
+
+    def __init__(self, matchers: Sequence[GrammarMatcher], bitmask, logits: Sequence[torch.Tensor],
+                 recycle: bool = True, stream: Optional[torch.cuda.Stream] = None):
+        import ctypes as C
+
+        from . import _lib
+        from .bitmask import _DTYPES
+
+        pool = get_pool()
+        dev = pool.device
+        n_buf = len(logits)
+        self.B = len(matchers)
+        self.slots = torch.tensor([m.slot for m in matchers], dtype=torch.int32, device=dev)
+        self.bitmasks = list(bitmask) if isinstance(bitmask, (list, tuple)) else [bitmask] * n_buf
+        self.logits = list(logits)
+        lg0 = self.logits[0]
+        for lg in self.logits:
+            if lg.dtype not in _DTYPES or lg.dim() != 2 or lg.stride(-1) != 1 or lg.shape != lg0.shape:
+                raise ValueError("logits buffers must be equal-shape 2-D fp32/fp16/bf16 CUDA tensors")
+        self.stream = stream or torch.cuda.current_stream(dev)
+        bm_ptrs = (C.c_void_p * n_buf)(*[b.data_ptr() if b is not None else None for b in self.bitmasks])
+        lg_ptrs = (C.c_void_p * n_buf)(*[lg.data_ptr() for lg in self.logits])
+        bstride = self.bitmasks[0].stride(0) if self.bitmasks[0] is not None else 0
+        h = C.c_void_p()
+        lib = _lib.load()
+        _lib.check(lib.gm_decoder_create(pool.handle, self.slots.data_ptr(), self.B, n_buf,
+                                         bm_ptrs if self.bitmasks[0] is not None else None, bstride, lg_ptrs,
+                                         _DTYPES[lg0.dtype], lg0.shape[1], lg0.stride(0), 1 if recycle else 0,
+                                         C.byref(h)), "gm_decoder_create")
+        self._h = h
+        self._lib = lib
+        self._check = _lib.check
+        self._sptr = int(self.stream.cuda_stream)
+        self._tok = np.zeros(self.B, dtype=np.int32)
+        self._flags = np.zeros(self.B, dtype=np.uint8)
+
+    def step(self, tokens, i: int = 0) -> None:
+        """Issue one decode step on buffer i (tokens: host ints, or None for
+        the first step).  Blocks only if buffer i's previous step is still
+        in flight."""
+        if tokens is None:
+            ptr = None
+        else:
+            t = tokens if isinstance(tokens, np.ndarray) and tokens.dtype == np.int32 else np.asarray(tokens, np.int32)
+            ptr = t.ctypes.data
+        st = self._lib.gm_decoder_step(self._h, i, ptr, self._sptr)
+        if st:
+            self._check(st, "gm_decoder_step")
+
+    def flags(self, i: int = 0, out: Optional[np.ndarray] = None, wait: bool = True) -> np.ndarray:
+        """Accepted flags (uint8 [B]) of buffer i's latest step."""
+        o = self._flags if out is None else out
+        st = self._lib.gm_decoder_flags(self._h, i, o.ctypes.data, 1 if wait else 0)
+        if st:
+            self._check(st, "gm_decoder_flags")
+        return o
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.gm_decoder_release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -348,8 +348,9 @@ def batch_step(pool: MatcherPool, slots: torch.Tensor, tokens: Optional[torch.Te
                bitmask: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None,
                rows: Optional[torch.Tensor] = None, recycle: bool = False, vocab_size: Optional[int] = None,
                stream=None) -> None:
-    """K5, one launch per decode step: accept ``tokens`` (int32 CUDA, or None
-    for the first step) into ``accepted`` (uint8 CUDA), optionally restart
+    """K5, one launch per decode step: accept ``tokens`` (int32 CUDA or pinned
+    host, or None for the first step) into ``accepted`` (uint8 CUDA or pinned
+    host; host buffers are read/written by the kernel directly), optionally restart
     requests that terminated, then fill the next masks into ``bitmask``
     and/or apply them to ``logits`` in place."""
     from .bitmask import _DTYPES
@@ -358,6 +359,9 @@ def batch_step(pool: MatcherPool, slots: torch.Tensor, tokens: Optional[torch.Te
         raise ValueError("logits must be a 2-D fp32/fp16/bf16 CUDA tensor, contiguous per row")
     if tokens is not None and accepted is None:
         raise ValueError("accepted output is required with tokens")
+    for t in (tokens, accepted):  # device tensors, or pinned host memory read/written by the kernel (zero-copy)
+        if t is not None and t.device.type == "cpu" and not t.is_pinned():
+            raise ValueError("tokens / accepted must be CUDA tensors or pinned host tensors")
     v = (logits.shape[1] if vocab_size is None else vocab_size) if logits is not None else 0
     _lib.check(_lib.load().gm_step_tokens(
         pool.handle, slots.data_ptr(), slots.numel(), tokens.data_ptr() if tokens is not None else None,

@@ -401,8 +401,10 @@ def test_step_kernel_equals_accept_then_fill(name, with_logits):
     pool.check()
 
 
-def test_decode_step_graph_equals_eager():
-    """DecodeStepGraph (H2D ids -> K5 -> D2H flags, captured) == eager batch_step."""
+@pytest.mark.parametrize("zero_copy", [True, False])
+def test_decode_step_graph_equals_eager(zero_copy):
+    """DecodeStepGraph (host ids -> K5 -> host flags, captured; zero-copy or
+    with copy-engine H2D/D2H) == eager batch_step."""
     import torch
 
     import paper_2411_15100_b200 as gm
@@ -423,7 +425,7 @@ def test_decode_step_graph_equals_eager():
     acc_ref = torch.empty(B, dtype=torch.uint8, device="cuda")
     g = torch.Generator(device="cuda").manual_seed(9)
     bufs = [torch.empty(B, vocab.size, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
-    step = DecodeStepGraph(new, bm_new, bufs, recycle=True)
+    step = DecodeStepGraph(new, bm_new, bufs, recycle=True, zero_copy=zero_copy)
     rng = random.Random(4)
     toks = None
     for it in range(30):
@@ -508,4 +510,62 @@ def test_decode_step_graph_queued_back_to_back():
     step.stream.synchronize()
     for s in range(S - n_buf, S):
         check(s)
+    pool.check()
+
+
+def test_decode_loop_native_equals_eager():
+    """DecodeLoop (native gm_decoder_*: host ids -> H2D -> K5 -> D2H, steps
+    queued back to back over 3 reused buffers) == eager batch_step: same
+    accepted flags and masks at every step."""
+    import numpy as np
+    import torch
+
+    import paper_2411_15100_b200 as gm
+    from paper_2411_15100_b200.engine import get_pool
+    from paper_2411_15100_b200.graph import DecodeLoop
+    from paper_2411_15100_b200.matcher import batch_step
+
+    vocab = vocab_by_name("4000:mixed")
+    info = gm.TokenizerInfo.from_vocabulary(vocab)
+    compiled = gm.GrammarCompiler(info).compile_builtin_json_grammar()
+    B, W, n_buf, S = 7, (vocab.size + 31) // 32, 3, 16
+    pool = get_pool()
+    ref = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    s_ref = torch.tensor([m.slot for m in ref], dtype=torch.int32, device="cuda")
+    bm = torch.empty((B, W), dtype=torch.int32, device="cuda")
+    acc = torch.empty(B, dtype=torch.uint8, device="cuda")
+    lg = torch.zeros(B, vocab.size, device="cuda", dtype=torch.bfloat16)
+    rng = random.Random(5)
+    toks, masks, accs = [None], [], []
+    for s in range(S):
+        batch_step(pool, s_ref, None if s == 0 else torch.tensor(toks[s], dtype=torch.int32, device="cuda"),
+                   None if s == 0 else acc, bm, lg, recycle=True)
+        masks.append(bm.clone())
+        accs.append(acc.tolist() if s else [0] * B)
+        allowed = ((bm.unsqueeze(-1) >> torch.arange(32, device="cuda", dtype=torch.int32)) & 1).reshape(B, -1)
+        nxt = []
+        for r in range(B):
+            ids = allowed[r, :vocab.size].nonzero().flatten().tolist()
+            nxt.append(rng.choice(ids) if rng.random() < 0.9 else vocab.size - 2)  # some rejected specials
+        toks.append(nxt)
+    new = [gm.GrammarMatcher(compiled) for _ in range(B)]
+    bms = [torch.empty((B, W), dtype=torch.int32, device="cuda") for _ in range(n_buf)]
+    bufs = [torch.zeros(B, vocab.size, device="cuda", dtype=torch.bfloat16) for _ in range(n_buf)]
+    loop = DecodeLoop(new, bms, bufs, recycle=True)
+    out = np.zeros(B, dtype=np.uint8)
+
+    def check(s):
+        i = s % n_buf
+        loop.flags(i, out=out, wait=True)
+        assert out.tolist() == accs[s], s
+        assert torch.equal(bms[i], masks[s]), s
+
+    for s in range(S):
+        if s >= n_buf:
+            check(s - n_buf)
+        loop.step(None if s == 0 else np.asarray(toks[s], dtype=np.int32), s % n_buf)
+    torch.cuda.synchronize()
+    for s in range(S - n_buf, S):
+        check(s)
+    loop.close()
     pool.check()

@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libgmask.so"
+LIB_PATH = Path(os.environ["GMASK_LIB"]) if os.environ.get("GMASK_LIB") else _HERE / "libgmask.so"
 
 GM_OK = 0
 GM_ERR_INVALID = 1

@@ -48,7 +48,14 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+def build(force: bool = False, verbose: bool = False, out: Path = None) -> Path:
+    global OUT
+    if out is not None:  # diagnostics: variant builds into another file
+        OUT, saved = Path(out), OUT
+        try:
+            return build(force=True, verbose=verbose)
+        finally:
+            OUT = saved
     if not force and not _stale():
         return OUT
     nvcc = _nvcc()
@@ -59,9 +66,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if os.environ.get("GMASK_VERIFY") == "1":  # debug: cross-check cached arena keys
         include += ["-DGM_VERIFY_KNOWN"]
 
+    extra = os.environ.get("GMASK_NVCC_EXTRA", "").split()  # diagnostics: variant builds
+
     def compile_one(src: str):
         obj = BUILD / (Path(src).stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, *include, "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc, *NVCC_FLAGS, *extra, *include, "-c", str(CSRC / src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")

@@ -108,9 +108,18 @@ __device__ inline void push_history(const DevPool& P, int32_t slot, const RingPo
 // the i-th input byte; is_eos = EOS token.  Returns 1 if accepted.  With
 // `mirror` (== &hdr, the caller's shared header) the new state is written
 // there as well as to the slot, so a fused step kernel can fill from it.
-template <class ByteFn>
+struct NoWalkHook {
+  template <class W>
+  __device__ __forceinline__ void operator()(const W&) const {}
+};
+
+// `on_walk(rw)` runs after a successful register-walker walk, before the
+// survivors are interned and published: the fused step kernel uses it to
+// start fetching the new tops' cache rows while the commit runs.
+template <class ByteFn, class OnWalk = NoWalkHook>
 __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr, const DevGrammar& G,
-                          int64_t len, ByteFn byte, bool is_eos, bool reject_token, SlotHdr* mirror = nullptr) {
+                          int64_t len, ByteFn byte, bool is_eos, bool reject_token, SlotHdr* mirror = nullptr,
+                          OnWalk on_walk = OnWalk()) {
   if (hdr.flags & 1) {  // REF matcher.py:276-277 "matcher is terminated"
     atomicOr(P.err, kErrTerminated);
     return 0;
@@ -141,6 +150,7 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
         return 0;
       }
       if (rw.n == 0) return 0;
+      on_walk(rw);
       int2 out[kAccR];
       Chain c;
       const int nout = rwalker_commit(rw, P.arena, out, c);

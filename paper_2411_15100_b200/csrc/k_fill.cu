@@ -103,7 +103,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   if (i >= n) return;
   const int32_t split = blockIdx.y, n_split = gridDim.y;
   trace_mark(P, 1, 0);
-  unsigned long long t_start = 0;
+  unsigned long long t_start = 0, t_hdr = 0, t_setup = 0, t_ctx = 0, t_walks = 0;
   if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int32_t slot = __ldg(slots + i);
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
@@ -121,8 +121,11 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   }
   __syncthreads();
   trace_mark(P, 1, 1);
+  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_hdr));
   DevGrammar Gs{};
   unsigned long long t_acc = 0;
+  const bool vec = (!bitmask || (reinterpret_cast<uintptr_t>(bitmask + row * bstride) & 15) == 0) && (hd.W % 4 == 0);
+  __shared__ int s_pref;  // K5: cache rows already in flight (count), -1 none, -2 issued but stale
   if (ACCEPT && SA.tokens) {  // launched with one split: one accept per request
     const bool in_range = tok >= 0 && tok < hd.V;
     if (threadIdx.x < 2 && in_range) s_rec[threadIdx.x] = __ldg(hd.tokrec + 2 * (size_t)tok + threadIdx.x);
@@ -192,8 +195,37 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
           P.trace[49] = t1;
         }
 #endif
+        // as soon as the walk has the new tops, start the TMA copies of their
+        // cache rows + the universe (the fill needs them) so they overlap
+        // the interning and the header publish
+        s_pref = -1;
+        auto prefetch_rows = [&](const auto& rw) {
+          if (!vec || rw.n > kTmaRows) return;
+          const int32_t Wr = hd.W;
+          int32_t keys[kTmaRows];
+          int nr = 0;
+#pragma unroll
+          for (int q = 0; q < kTmaRows; ++q) {
+            keys[q] = -1;
+            if (q < rw.n) {
+              keys[q] = Gs.node_info[rw.node[q]].x;
+              nr += keys[q] >= 0;
+            }
+          }
+          mbar_init(&rows_bar, (uint32_t)((nr + 1) * (size_t)Wr * 4));
+          int k = 0;
+#pragma unroll
+          for (int q = 0; q < kTmaRows; ++q) {
+            if (keys[q] < 0) continue;
+            bulk_g2s(rows_s + (size_t)k * part_bytes, hd.acc_rows + (size_t)keys[q] * Wr, (uint32_t)Wr * 4, &rows_bar);
+            ++k;
+          }
+          bulk_g2s(rows_s + (size_t)kTmaRows * part_bytes, hd.universe, (uint32_t)Wr * 4, &rows_bar);
+          s_pref = nr;
+        };
         acc = accept_one(P, slot, rp, hd, Gs, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
-                         tok == hd.eos, e.x != 0, &hd);
+                         tok == hd.eos, e.x != 0, &hd, prefetch_rows);
+        if (!acc && s_pref >= 0) s_pref = -2;  // walked but not committed: state unchanged, rows stale
       }
       SA.accepted[i] = (uint8_t)acc;
       s_just_term = !was_term && (hd.flags & 1);
@@ -207,7 +239,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   const int32_t per = ((W + 3) / 4 + n_split - 1) / n_split * 4;  // words per split
   const int32_t w_lo = min(W, split * per), w_hi = min(W, w_lo + per), nw = w_hi - w_lo;
   const bool terminated = hd.flags & 1;
-  const bool vec = (!bitmask || (reinterpret_cast<uintptr_t>(bitmask + row * bstride) & 15) == 0) && (W % 4 == 0);
+  const int pref = (ACCEPT && SA.tokens) ? s_pref : -1;
   if (threadIdx.x == 0) {
     s_partial = 0;
     int nt = hd.ntops;
@@ -216,7 +248,9 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       nt = 0;
     } else if (nt >= 0) {
       // issue the row copies first: they are the longest-latency loads
-      if (vec && nt <= kTmaRows && nw > 0) {
+      if (pref >= 0) {
+        s_nrows = pref;  // issued during the accept (K5, one split: w_lo = 0, nw = W)
+      } else if (vec && nt <= kTmaRows && nw > 0 && pref == -1) {
         int nr = 0;
         for (int s = 0; s < nt; ++s) nr += hd.key[s] >= 0;
         s_nrows = nr;
@@ -254,8 +288,10 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) dep_acc[w] = 0u;
   __syncthreads();
   trace_mark(P, 1, 2);
+  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
   const int nt = s_nt;
-  const bool tma = vec && hd.ntops >= 0 && nt <= kTmaRows && nw > 0 && !terminated;
+  const bool tma = pref >= 0 || (vec && hd.ntops >= 0 && nt <= kTmaRows && nw > 0 && !terminated && pref == -1);
+  if (pref == -2) mbar_wait(&rows_bar, 0);  // drain the stale prefetch before leaving
 
   trace_mark(P, 1, 3);
   int total = 0;
@@ -290,6 +326,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     }
     __syncthreads();
     trace_mark(P, 1, 4);
+    if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ctx));
     const uint8_t* rec_base = reinterpret_cast<const uint8_t*>(hd.tokrec);  // records' byte offsets are into it
     const int32_t tok_lo = w_lo * 32, tok_hi = w_hi * 32;
     // warp-major assignment: consecutive dependents go to different warps, so
@@ -351,6 +388,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   trace_mark(P, 1, 5);
   __syncthreads();
   trace_mark(P, 1, 6);
+  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_walks));
 
   // Merge and store this CTA's words.
   uint32_t* out = bitmask ? bitmask + row * bstride : nullptr;
@@ -413,10 +451,10 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     const int64_t c = (int64_t)i * n_split + split;
-    if (c < (int64_t)P.capacity) {
-      P.trace[64 + 3 * c] = t1 - t_start;
-      P.trace[64 + 3 * c + 1] = (unsigned long long)total | ((unsigned long long)nt << 32);
-      P.trace[64 + 3 * c + 2] = (t_merge - t_start) | ((t_acc ? t_acc - t_start : 0ull) << 32);
+    if (8 * c + 8 <= 3 * (int64_t)P.capacity) {  // per-CTA timeline (absolute %globaltimer stamps)
+      unsigned long long* tr = P.trace + 64 + 8 * c;
+      tr[0] = t_start; tr[1] = t_hdr; tr[2] = t_acc; tr[3] = t_setup;
+      tr[4] = t_ctx; tr[5] = t_walks; tr[6] = t_merge; tr[7] = t1;
     }
     if (c == 0) P.trace[63] = (unsigned long long)n_split;
   }

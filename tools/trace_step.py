@@ -25,6 +25,39 @@ from paper_2411_15100_b200.matcher import (  # noqa: E402
     batch_accept, batch_fill, batch_fill_apply, batch_recycle, batch_step)
 
 
+PHASES = ["header", "accept", "setup", "ctx", "walks", "merge", "apply"]
+
+
+def timeline(buf, nc):
+    """Per-CTA timeline (absolute %globaltimer stamps at 64 + 8c): span of
+    the kernel and p50 / max of every phase over the CTAs."""
+    import statistics
+
+    rec = [[buf[64 + 8 * c + k] for k in range(8)] for c in range(nc)]
+    t0 = min(r[0] for r in rec)
+    t1 = max(r[7] for r in rec)
+    out = [f"span {(t1 - t0) / 1e3:.2f} us, CTA start spread {(max(r[0] for r in rec) - t0) / 1e3:.2f}"]
+    for k, name in enumerate(PHASES):
+        d = []
+        for r in rec:
+            a, b = r[k], r[k + 1]
+            if k == 3 and not b:  # no ctx stamp (no dependents): fold into walks
+                continue
+            if k == 4 and not a:
+                a = r[3]
+            if k == 1 and not b:
+                continue
+            if k == 2 and not a:
+                a = r[1]
+            if a and b and b >= a:
+                d.append((b - a) / 1e3)
+        if d:
+            out.append(f"{name} {statistics.median(d):.2f}/{max(d):.2f}")
+    ends = sorted((r[7] - t0) / 1e3 for r in rec)
+    out.append(f"CTA end p50 {ends[len(ends) // 2]:.2f} max {ends[-1]:.2f}")
+    return " | ".join(out)
+
+
 def main(steps=12, flush=True, fused=False, grammar="json", step_mode=False):
     torch.cuda.set_device(0)
     vocab = gm.synth_vocab(128256)
@@ -60,15 +93,8 @@ def main(steps=12, flush=True, fused=False, grammar="json", step_mode=False):
         f = [buf[16 + k] for k in range(8)]
         ns = max(1, buf[63])
         nc = B * ns
-        cta = sorted(((buf[64 + 3 * i] / 1e3, (buf[66 + 3 * i] & 0xFFFFFFFF) / 1e3, buf[65 + 3 * i] & 0xFFFFFFFF,
-                       buf[65 + 3 * i] >> 32, (buf[66 + 3 * i] >> 32) / 1e3) for i in range(nc)), reverse=True)
-        mrg = sorted(c[1] for c in cta)
-        accd = sorted(c[4] for c in cta)
         kname = ("K5" if step_mode else "K3" if fused else "K2")
-        print(f"  {kname} x{ns} per-CTA us: max {cta[0][0]:.2f} p50 {cta[nc // 2][0]:.2f} | "
-              f"accept-done max {accd[-1]:.2f} p50 {accd[nc // 2]:.2f} | "
-              f"to-merge-done max {mrg[-1]:.2f} p50 {mrg[nc // 2]:.2f} | slowest (us, merge-us, deps, tops, acc-us): "
-              f"{[(round(a, 2), round(m, 2), b, c, round(d, 2)) for a, m, b, c, d in cta[:4]]}")
+        print(f"  {kname} x{ns} {timeline(buf, nc)}")
         extra = f"deps={buf[24]} key0={C.c_int64(buf[25]).value} ntops={buf[26]}"
         if buf[24]:
             ln = buf[44] & 0xFFFF

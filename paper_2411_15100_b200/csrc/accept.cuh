@@ -71,9 +71,8 @@ __device__ inline void push_tops(const DevPool& P, int32_t slot, const RingPos& 
   P.head[slot] = nh;
   const int32_t hl = rp.hist_len + 1;
   P.hist_len[slot] = hl < rp.window ? hl : rp.window;
-  if (mirror) {  // new state into the caller's shared copy, then published
+  if (mirror) {  // new state into the caller's shared copy; the caller publishes it
     header_state(P, *mirror, G, tops, nt, terminated, &c);
-    store_header_state(P, slot, *mirror);
   } else {
     header_state(P, P.hdr[slot], G, tops, nt, terminated, &c);
   }
@@ -87,8 +86,7 @@ __device__ inline void restart_slot(const DevPool& P, int32_t slot, const DevGra
   const int2 t0 = make_int2(-1, G.start_node);
   *slot_tops(P, slot, 0) = t0;
   P.meta[(size_t)slot * P.H] = 1;
-  header_state(P, *mirror, G, &t0, 1, 0, nullptr);
-  store_header_state(P, slot, *mirror);
+  header_state(P, *mirror, G, &t0, 1, 0, nullptr);  // the caller publishes it
 }
 
 __device__ inline void push_history(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr,
@@ -107,7 +105,8 @@ __device__ inline void push_history(const DevPool& P, int32_t slot, const RingPo
 // Shared by token and byte-string acceptance (lane 0 only).  byte(i) gives
 // the i-th input byte; is_eos = EOS token.  Returns 1 if accepted.  With
 // `mirror` (== &hdr, the caller's shared header) the new state is written
-// there as well as to the slot, so a fused step kernel can fill from it.
+// there and the ring updated, but the caller publishes the header (warp-
+// parallel, store_header_state_warp) so a fused step kernel can fill from it.
 struct NoWalkHook {
   template <class W>
   __device__ __forceinline__ void operator()(const W&) const {}
@@ -119,7 +118,7 @@ struct NoWalkHook {
 template <class ByteFn, class OnWalk = NoWalkHook>
 __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr, const DevGrammar& G,
                           int64_t len, ByteFn byte, bool is_eos, bool reject_token, SlotHdr* mirror = nullptr,
-                          OnWalk on_walk = OnWalk()) {
+                          OnWalk on_walk = OnWalk(), unsigned long long* ts = nullptr) {
   if (hdr.flags & 1) {  // REF matcher.py:276-277 "matcher is terminated"
     atomicOr(P.err, kErrTerminated);
     return 0;
@@ -152,6 +151,24 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
       if (rw.n == 0) return 0;
       on_walk(rw);
       int2 out[kAccR];
+      if (mirror) {  // fused step kernel: chain rewritten in place in the shared header
+        const int nout = rwalker_commit_inplace(rw, P.arena, out, *mirror);
+        if (nout < 0) {
+          atomicOr(P.err, kErrArena);
+          return 0;
+        }
+        if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[0]));
+        const int32_t nh = (rp.head + 1) % P.H;
+        int2* dst = slot_tops(P, slot, nh);
+        for (int s = 0; s < nout; ++s) dst[s] = out[s];
+        P.meta[(size_t)slot * P.H + nh] = nout;
+        P.head[slot] = nh;
+        const int32_t hl = rp.hist_len + 1;
+        P.hist_len[slot] = hl < rp.window ? hl : rp.window;
+        header_state_inplace(P, *mirror, G, out, nout, 0);
+        if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[1]));
+        return 1;
+      }
       Chain c;
       const int nout = rwalker_commit(rw, P.arena, out, c);
       if (nout < 0) {
@@ -159,7 +176,9 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
         return 0;
       }
       trace_mark(P, 0, 4);
+      if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[0]));
       push_tops(P, slot, rp, G, out, nout, 0, c, mirror);
+      if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[1]));
       trace_mark(P, 0, 5);
       return 1;
     }

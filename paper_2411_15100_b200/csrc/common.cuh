@@ -65,6 +65,20 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 }
 
 #ifdef __CUDACC__
+// -inf stores into logits: streaming (.cs = evict-first in L2), so the
+// masked-logits stream does not push the matcher state, arena and cache rows
+// (read again next step) out of L2 — with the logits written back to back,
+// every L2 miss of the latency-bound fill/accept chain otherwise queues
+// behind the write stream at HBM.
+__device__ __forceinline__ void st_cs_v4(void* p, uint32_t v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cs_u32(void* p, uint32_t v) {
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cs_u16(void* p, uint32_t v) {
+  asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"((unsigned short)v) : "memory");
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 #endif

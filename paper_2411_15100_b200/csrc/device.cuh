@@ -207,8 +207,14 @@ __device__ __forceinline__ uint32_t mix64(unsigned long long k) {
   k ^= k >> 33;
   return (uint32_t)k;
 }
+// GPU-scope relaxed load (L2): an arena slot only ever changes from empty to
+// its key, so no system-scope ordering is needed — a volatile (.sys) load of
+// a hot slot (frames are hash-consed: every request shares its stack prefix,
+// so 100+ CTAs read the same few slots each step) measured 1.5-3.5 us.
 __device__ __forceinline__ unsigned long long arena_load(const DevArena& A, int32_t h) {
-  return *reinterpret_cast<volatile const unsigned long long*>(A.keys + h);
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(A.keys + h) : "memory");
+  return v;
 }
 __device__ __forceinline__ int32_t key_parent(unsigned long long k) { return (int32_t)(uint32_t)(k >> 32) - 1; }
 __device__ __forceinline__ int32_t key_node(unsigned long long k) { return (int32_t)((uint32_t)k >> 1); }
@@ -741,6 +747,14 @@ struct DevPool {
   uint32_t* err;
   SlotHdr* hdr;               // [capacity]
   unsigned long long* trace;  // optional phase timestamps (GMASK_TRACE=1), else null
+  // launch hint: the binding every bound slot shares (host bookkeeping,
+  // gm_pool_reset / fork), or null.  Grammar blobs and token records are
+  // immutable, so a step kernel may start staging them before its
+  // griddepcontrol.wait and before its slot header arrives; it still checks
+  // the header's binding and restages on a mismatch.
+  const uint8_t* hint_blob;
+  const int4* hint_tokrec;
+  int32_t hint_blob_bytes, hint_V;
 };
 
 // Phase timestamps of CTA 0 (diagnostics only): trace[kernel*16 + phase].
@@ -831,6 +845,154 @@ __device__ inline void header_state(const DevPool& P, SlotHdr& h, const DevGramm
   h.flags = (terminated ? 1 : 0) | (term ? 2 : 0);
 }
 
+// rwalker_commit for the fused step kernel: interns exactly like
+// rwalker_commit, but writes the first top's ancestor chain straight into
+// the shared-memory header `h` (whose chain the walker used as its external
+// chain, w.xh/w.xk == h.chain_h/h.chain_k): the surviving part of the old
+// chain is shifted in place and the fresh frames written in front — no
+// walker-local Chain copy (16 local-memory round trips per accept).
+template <int R, int F>
+__device__ inline int rwalker_commit_inplace(RWalker<R, F>& w, const DevArena& A, int2* out, SlotHdr& h) {
+  // scratch in shared memory: one committing thread per CTA (the accept
+  // thread); local-memory arrays here cost an L2 round trip per access
+  __shared__ int32_t gmap[F];
+  __shared__ unsigned long long keyq[F];
+  for (int q = 0; q < w.nf; ++q) gmap[q] = 0;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    if (s >= w.n) break;
+    int32_t r = w.ref[s];
+    while (r >= 0 && r < kChainRef && gmap[r] == 0) { gmap[r] = 1; r = w.fpar[r]; }
+  }
+  auto parent_handle = [&](int32_t p) -> int32_t {
+    if (p == -1) return -1;
+    if (p >= kChainRef) return w.xh[p - kChainRef];
+    if (p >= 0) return gmap[p];
+    return -2 - p;
+  };
+  // speculative handles (a frame's slot = its key's hash), then the CASes
+  // issued in batches of 8 with their results in registers, so the atomic
+  // round trips overlap instead of serialising on a local-memory store
+  for (int q = 0; q < w.nf; ++q) {
+    if (!gmap[q]) { gmap[q] = -1; continue; }
+    keyq[q] = arena_key(parent_handle(w.fpar[q]), w.fnode[q], w.fterm[q]);
+    gmap[q] = (int32_t)(mix64(keyq[q]) & A.mask);
+  }
+  bool redo = false;
+  constexpr int kBatch = 8;
+  for (int q0 = 0; q0 < w.nf; q0 += kBatch) {
+    unsigned long long res[kBatch];
+    // test before test-and-set: most frames are already interned (requests
+    // share stack prefixes, hash-consed to the same slot), and a plain load
+    // of a hot slot does not serialise at L2 the way 100+ concurrent CASes
+    // on it do (measured ~5 us per contended frame)
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int q = q0 + j;
+      res[j] = kEmptyKey;
+      if (q < w.nf && gmap[q] >= 0) res[j] = arena_load(A, gmap[q]);
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int q = q0 + j;
+      if (q < w.nf && gmap[q] >= 0 && res[j] == kEmptyKey) res[j] = atomicCAS(A.keys + gmap[q], kEmptyKey, keyq[q]);
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int q = q0 + j;
+      if (q >= w.nf || gmap[q] < 0) continue;
+      if (!redo && (res[j] == kEmptyKey || res[j] == keyq[q])) continue;
+      redo = true;  // collision: this frame and every later one probe serially
+      keyq[q] = arena_key(parent_handle(w.fpar[q]), w.fnode[q], w.fterm[q]);
+      const int32_t hh = arena_probe(A, keyq[q], mix64(keyq[q]));
+      if (hh < 0) return -1;
+      gmap[q] = hh;
+    }
+  }
+  int n = 0;
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    if (s >= w.n) break;
+    const int32_t r = w.ref[s];
+    const int32_t hh = (r >= 0 && r < kChainRef) ? gmap[r] : w.handle_of(r);
+    bool dup = false;
+    for (int q = 0; q < n; ++q) dup |= (out[q].x == hh && out[q].y == w.node[s]);
+    if (!dup) out[n++] = make_int2(hh, w.node[s]);
+  }
+  // chain of the first top = its fresh frames, then the old chain from the
+  // first frame they share
+  int nfresh = 0;
+  int32_t r = w.n > 0 ? w.ref[0] : -1;
+  const int32_t r0 = r;
+  while (r >= 0 && r < kChainRef && nfresh < kChain) { ++nfresh; r = w.fpar[r]; }
+  int from = -1;
+  if (r >= 0 && r < kChainRef) {
+    from = -1;  // more fresh frames than the chain holds: old part not reached
+  } else if (r >= kChainRef) {
+    from = r - kChainRef;
+  } else if (r <= -2) {
+    const int32_t hh = -2 - r;
+    for (int j = 0; j < w.nx; ++j)
+      if (w.xh[j] == hh) { from = j; break; }
+  }
+  const int on = h.nchain;
+  const int nold = from >= 0 ? min(on - from, kChain - nfresh) : 0;
+  if (nold > 0 && from != nfresh) {
+    if (nfresh < from) {
+      for (int j = 0; j < nold; ++j) { h.chain_h[nfresh + j] = h.chain_h[from + j]; h.chain_k[nfresh + j] = h.chain_k[from + j]; }
+    } else {
+      for (int j = nold - 1; j >= 0; --j) { h.chain_h[nfresh + j] = h.chain_h[from + j]; h.chain_k[nfresh + j] = h.chain_k[from + j]; }
+    }
+  }
+  r = r0;
+  for (int j = 0; j < nfresh; ++j) {
+    h.chain_h[j] = gmap[r];
+    h.chain_k[j] = keyq[r];
+    r = w.fpar[r];
+  }
+  h.nchain = nfresh + max(nold, 0);
+  return n;
+}
+
+constexpr int kHdrStateVec = 3;  // first int4 holding state (ntops at byte 56)
+static_assert(offsetof(SlotHdr, ntops) >= kHdrStateVec * 16, "header state offset");
+// header_state for a header whose ancestor chain (chain_h/chain_k/nchain)
+// has already been rewritten in place (rwalker_commit_inplace): same state
+// fields, no chain copy.
+__device__ inline void header_state_inplace(const DevPool& P, SlotHdr& h, const DevGrammar& G, const int2* tops, int n,
+                                            int terminated) {
+  int term = 0;
+  for (int s = 0; s < n; ++s) {
+    const int2 t = tops[s];
+    if (!terminated && !term && (G.node_flags[t.y] & GM_NODE_POP)) {
+      if (t.x < 0) {
+        term = 1;
+      } else {
+        const unsigned long long k = (s == 0 && h.nchain && h.chain_h[0] == t.x) ? h.chain_k[0] : arena_load(P.arena, t.x);
+        term = (int)key_term(k);
+      }
+    }
+    if (s < kHdrTops) {
+      const int4 ni = G.node_info[t.y];
+      h.key[s] = ni.x;
+      h.dep_lo[s] = ni.y;
+      h.dep_hi[s] = ni.z;
+      h.top[s] = t;
+    }
+  }
+  if (n == 0) h.nchain = 0;
+  h.ntops = n <= kHdrTops ? n : -1;
+  h.flags = (terminated ? 1 : 0) | (term ? 2 : 0);
+}
+
+// Publish the state part of a shared-memory header with the lanes of one
+// warp (one 16-byte store each) — the deferred counterpart of
+// store_header_state for the fused step kernel.
+__device__ __forceinline__ void store_header_state_warp(const DevPool& P, int32_t slot, const SlotHdr& h, int lane) {
+  const int i = kHdrStateVec + lane;
+  if (i < kHdrVec) reinterpret_cast<int4*>(P.hdr + slot)[i] = reinterpret_cast<const int4*>(&h)[i];
+}
+
 __device__ inline void store_header(const DevPool& P, int32_t slot, const SlotHdr& h) {
   const int4* src = reinterpret_cast<const int4*>(&h);
   int4* dst = reinterpret_cast<int4*>(P.hdr + slot);
@@ -840,8 +1002,6 @@ __device__ inline void store_header(const DevPool& P, int32_t slot, const SlotHd
 
 // Publish the state part of a header (everything after the binding pointers
 // and sizes, which never change for a slot) with 16-byte stores.
-constexpr int kHdrStateVec = 3;  // first int4 holding state (ntops at byte 56)
-static_assert(offsetof(SlotHdr, ntops) >= kHdrStateVec * 16, "header state offset");
 __device__ inline void store_header_state(const DevPool& P, int32_t slot, const SlotHdr& h) {
   const int4* src = reinterpret_cast<const int4*>(&h);
   int4* dst = reinterpret_cast<int4*>(P.hdr + slot);

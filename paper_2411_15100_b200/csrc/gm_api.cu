@@ -6,6 +6,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "device.cuh"
@@ -130,6 +131,8 @@ struct gm_cache {
 struct gm_pool {
   DevAllocs mem;
   DevPool dev;
+  std::vector<const gm_cache*> slot_cache;           // binding of each slot (null: never bound)
+  std::unordered_map<const gm_cache*, int32_t> bound;  // slots per binding
   uint8_t* scratch_bytes;  // accept_bytes staging
   int64_t scratch_cap;
   int32_t* scratch_i32;    // probe outputs
@@ -569,18 +572,37 @@ void gm_pool_release(gm_pool* p) {
   delete p;
 }
 
+// Host bookkeeping of slot bindings -> the pool's launch hint (DevPool
+// hint_*): set while every bound slot shares one binding.
+static void bind_slot(gm_pool* p, int32_t slot, const gm_cache* c) {
+  if ((int32_t)p->slot_cache.size() < p->dev.capacity) p->slot_cache.resize(p->dev.capacity, nullptr);
+  const gm_cache* old = p->slot_cache[slot];
+  if (old == c) return;
+  if (old && --p->bound[old] == 0) p->bound.erase(old);
+  p->slot_cache[slot] = c;
+  if (c) ++p->bound[c];
+  const gm_cache* h = p->bound.size() == 1 ? p->bound.begin()->first : nullptr;
+  const bool fits = h && h->host_binding.c.blob_bytes <= kStageBytes;
+  p->dev.hint_blob = fits ? h->host_binding.c.blob : nullptr;
+  p->dev.hint_blob_bytes = fits ? h->host_binding.c.blob_bytes : 0;
+  p->dev.hint_tokrec = fits ? h->host_binding.v.tokrec : nullptr;
+  p->dev.hint_V = fits ? h->host_binding.v.V : 0;
+}
+
 gm_status gm_pool_reset(gm_pool* p, int32_t slot, const gm_grammar* g, const gm_cache* c, const gm_vocab* v,
                         int32_t window, void* stream) {
   if (!p || !g || !c || !v) return fail(GM_ERR_INVALID, "null argument");
   if (slot < 0 || slot >= p->dev.capacity) return fail(GM_ERR_INVALID, "slot out of range");
   if (window < 0 || window > p->dev.H - 1) return fail(GM_ERR_INVALID, "history window exceeds pool maximum");
   if (v->dev.W > p->max_w) p->max_w = v->dev.W;
+  bind_slot(p, slot, c);
   return launch_reset(p->dev, slot, c->binding, g->dev.start_node, window, as_stream(stream));
 }
 
 gm_status gm_pool_fork(gm_pool* p, int32_t src, int32_t dst, void* stream) {
   if (!p || src < 0 || dst < 0 || src >= p->dev.capacity || dst >= p->dev.capacity)
     return fail(GM_ERR_INVALID, "slot out of range");
+  bind_slot(p, dst, (int32_t)p->slot_cache.size() > src ? p->slot_cache[src] : nullptr);
   return launch_fork(p->dev, src, dst, as_stream(stream));
 }
 

@@ -45,8 +45,10 @@ accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t
   }
   const int4 e = s_rec[0], inl = s_rec[1];
   const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;
-  accepted[i] = (uint8_t)accept_one(P, slot, rp, hd, G, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
-                                    tid == hd.eos, e.x != 0, &hd);
+  const int acc = accept_one(P, slot, rp, hd, G, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
+                             tid == hd.eos, e.x != 0, &hd);
+  if (acc) store_header_state(P, slot, hd);  // accept_one leaves the mirror's publish to the caller
+  accepted[i] = (uint8_t)acc;
 }
 
 __global__ void __maxnreg__(128)
@@ -75,8 +77,9 @@ accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len, u
     *accepted = 1;
     return;
   }
-  *accepted = (uint8_t)accept_one(P, slot, rp, hd, G, len, [&](int64_t b) { return __ldg(data + b); }, false, false,
-                                  &hd);
+  const int acc = accept_one(P, slot, rp, hd, G, len, [&](int64_t b) { return __ldg(data + b); }, false, false, &hd);
+  if (acc) store_header_state(P, slot, hd);  // accept_one leaves the mirror's publish to the caller
+  *accepted = (uint8_t)acc;
 }
 
 __global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32_t start, int32_t window) {

@@ -24,7 +24,7 @@ namespace gm {
 namespace {
 
 __device__ __forceinline__ void st_v4(void* p, uint32_t v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%1,%1,%1};" :: "l"(p), "r"(v) : "memory");
+  st_cs_v4(p, v);
 }
 
 constexpr int kTileTok = 1024;  // tokens per warp tile (32 words)
@@ -62,8 +62,8 @@ __device__ __forceinline__ void apply_tile(char* __restrict__ tp, int64_t tok_ba
       while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1;
-        if (EB == 4) *reinterpret_cast<uint32_t*>(p + j * 4) = neg;
-        else *reinterpret_cast<uint16_t*>(p + j * 2) = (uint16_t)neg;
+        if (EB == 4) st_cs_u32(p + j * 4, neg);
+        else st_cs_u16(p + j * 2, neg);
       }
     }
   }

@@ -32,6 +32,10 @@ constexpr int kDepS = 16;
 constexpr int kDepF = 64;
 constexpr int kDepR = 4;    // register walker: stacks
 constexpr int kDepRF = 24;  // register walker: local frames
+#ifndef GM_PREFETCH_ROWS
+#define GM_PREFETCH_ROWS 0
+#endif
+constexpr bool kPrefetchRows = GM_PREFETCH_ROWS;  // K5: issue row TMAs from the accept walk
 
 // K3 tail: mask one logits row in place from the finished mask words in
 // shared memory (coalesced 16-byte chunks, -inf only where masked, logits
@@ -49,14 +53,14 @@ __device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_
     if (keep == full) continue;
     char* p = rowp + (tok_lo + t0) * eb;
     if (keep == 0) {
-      asm volatile("st.global.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(p), "r"(neg) : "memory");
+      st_cs_v4(p, neg);
     } else {
       uint32_t m = ~keep & full;
       while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1;
-        if (eb == 4) *reinterpret_cast<uint32_t*>(p + j * 4) = neg;
-        else *reinterpret_cast<uint16_t*>(p + j * 2) = (uint16_t)neg;
+        if (eb == 4) st_cs_u32(p + j * 4, neg);
+        else st_cs_u16(p + j * 2, neg);
       }
     }
   }
@@ -97,29 +101,45 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   __shared__ int2 s_top[32];
   __shared__ int s_cj[32];
   __shared__ __align__(8) unsigned long long rows_bar;
+  __shared__ __align__(8) unsigned long long blob_bar;
   pdl_trigger();
+  // the pool's launch hint (immutable grammar blob of the binding every
+  // slot shares): staged before the grid dependency wait and the header
+  const bool hinted = P.hint_blob != nullptr && blockIdx.x < n;
+  if (hinted && threadIdx.x == 0) {
+    mbar_init(&blob_bar, (uint32_t)P.hint_blob_bytes);
+    bulk_g2s(tables, P.hint_blob, (uint32_t)P.hint_blob_bytes, &blob_bar);
+  }
   pdl_wait();
   const int32_t i = blockIdx.x;
   if (i >= n) return;
   const int32_t split = blockIdx.y, n_split = gridDim.y;
   trace_mark(P, 1, 0);
-  unsigned long long t_start = 0, t_hdr = 0, t_setup = 0, t_ctx = 0, t_walks = 0;
+  unsigned long long t_start = 0, t_hdr = 0, t_setup = 0, t_ctx = 0, t_walks = 0, t_walk = 0, walk_info = 0;
+  unsigned long long acc_ts[2] = {0, 0};  // accept: frames interned, header state built
   if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int32_t slot = __ldg(slots + i);
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   __shared__ RingPos rp;
   __shared__ int4 s_rec[2];
-  __shared__ int s_just_term;
+  __shared__ int s_just_term, s_dirty;
   int32_t tok = -1;
   if (ACCEPT && SA.tokens) {
     // volatile load: `tokens` may be pinned host memory written by the host
     // between graph replays (zero-copy H2D, graph.py), never cached
     asm volatile("ld.global.cv.s32 %0, [%1];" : "=r"(tok) : "l"(SA.tokens + i));
     load_header_ring(P, slot, &hd, &rp);
+    // token record from the hinted vocabulary, in the header's round trip
+    if (hinted && threadIdx.x < 2 && tok >= 0 && tok < P.hint_V)
+      s_rec[threadIdx.x] = __ldg(P.hint_tokrec + 2 * (size_t)tok + threadIdx.x);
   } else {
     load_header(P, slot, &hd);
   }
   __syncthreads();
+  // the hint is usable iff this slot is bound to it; otherwise drain the
+  // early copy and stage the slot's own blob
+  const bool hint_ok = hinted && hd.blob == P.hint_blob && hd.tokrec == P.hint_tokrec;
+  if (hinted) mbar_wait(&blob_bar, 0);
   trace_mark(P, 1, 1);
   if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_hdr));
   DevGrammar Gs{};
@@ -128,8 +148,12 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   __shared__ int s_pref;  // K5: cache rows already in flight (count), -1 none, -2 issued but stale
   if (ACCEPT && SA.tokens) {  // launched with one split: one accept per request
     const bool in_range = tok >= 0 && tok < hd.V;
-    if (threadIdx.x < 2 && in_range) s_rec[threadIdx.x] = __ldg(hd.tokrec + 2 * (size_t)tok + threadIdx.x);
-    Gs = stage_blob(hd.blob, hd.blob_bytes, tables);  // barrier inside
+    if (hint_ok) {
+      Gs = blob_view(tables);
+    } else {
+      if (threadIdx.x < 2 && in_range) s_rec[threadIdx.x] = __ldg(hd.tokrec + 2 * (size_t)tok + threadIdx.x);
+      Gs = stage_blob(hd.blob, hd.blob_bytes, tables);  // barrier inside
+    }
     if (P.trace && i == 0 && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -200,7 +224,11 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
         // the interning and the header publish
         s_pref = -1;
         auto prefetch_rows = [&](const auto& rw) {
-          if (!vec || rw.n > kTmaRows) return;
+          if (P.trace) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_walk));
+            walk_info = (unsigned long long)e.y | ((unsigned long long)rw.n << 16) | ((unsigned long long)rw.nf << 24);
+          }
+          if (!vec || rw.n > kTmaRows || !kPrefetchRows) return;
           const int32_t Wr = hd.W;
           int32_t keys[kTmaRows];
           int nr = 0;
@@ -224,16 +252,20 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
           s_pref = nr;
         };
         acc = accept_one(P, slot, rp, hd, Gs, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
-                         tok == hd.eos, e.x != 0, &hd, prefetch_rows);
+                         tok == hd.eos, e.x != 0, &hd, prefetch_rows, P.trace ? acc_ts : nullptr);
         if (!acc && s_pref >= 0) s_pref = -2;  // walked but not committed: state unchanged, rows stale
       }
       SA.accepted[i] = (uint8_t)acc;
       s_just_term = !was_term && (hd.flags & 1);
-      if (SA.recycle && (hd.flags & 1)) restart_slot(P, slot, Gs, &hd);
+      const bool restart = SA.recycle && (hd.flags & 1);
+      if (restart) restart_slot(P, slot, Gs, &hd);
+      s_dirty = acc || restart;
       if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_acc));
       if (P.trace && i == 0) P.trace[48] = t_acc;
     }
     __syncthreads();
+    // publish the new header state (one 16-byte store per lane of warp 0)
+    if (s_dirty && threadIdx.x < 32) store_header_state_warp(P, slot, hd, threadIdx.x);
   }
   const int32_t W = hd.W;
   const int32_t per = ((W + 3) / 4 + n_split - 1) / n_split * 4;  // words per split
@@ -302,7 +334,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     P.trace[16 + 10] = (unsigned long long)nt;
   }
   if (total) {
-    const DevGrammar G = (ACCEPT && SA.tokens) ? Gs : stage_blob(hd.blob, hd.blob_bytes, tables);
+    const DevGrammar G = (ACCEPT && SA.tokens) ? Gs : hint_ok ? blob_view(tables) : stage_blob(hd.blob, hd.blob_bytes, tables);
     // caller index of each top's parent frame within the callers of the
     // top's rule: selects the dependents' one-level context class
     if ((int)threadIdx.x < nt) {
@@ -451,10 +483,14 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     const int64_t c = (int64_t)i * n_split + split;
-    if (8 * c + 8 <= 3 * (int64_t)P.capacity) {  // per-CTA timeline (absolute %globaltimer stamps)
-      unsigned long long* tr = P.trace + 64 + 8 * c;
+    if (12 * c + 12 <= 3 * (int64_t)P.capacity) {  // per-CTA timeline (absolute %globaltimer stamps)
+      unsigned long long* tr = P.trace + 64 + 12 * c;
       tr[0] = t_start; tr[1] = t_hdr; tr[2] = t_acc; tr[3] = t_setup;
       tr[4] = t_ctx; tr[5] = t_walks; tr[6] = t_merge; tr[7] = t1;
+      tr[8] = t_walk;                // accept: register walk done (0: no walk / general path)
+      tr[9] = walk_info;             // token bytes | stacks << 16 | walker frames << 24
+      tr[10] = (unsigned long long)total | ((unsigned long long)nt << 32);  // dependents, tops
+      tr[11] = acc_ts[0];            // accept: frames interned (publish starts)
     }
     if (c == 0) P.trace[63] = (unsigned long long)n_split;
   }

@@ -33,7 +33,7 @@ def timeline(buf, nc):
     the kernel and p50 / max of every phase over the CTAs."""
     import statistics
 
-    rec = [[buf[64 + 8 * c + k] for k in range(8)] for c in range(nc)]
+    rec = [[buf[64 + 12 * c + k] for k in range(12)] for c in range(nc)]
     t0 = min(r[0] for r in rec)
     t1 = max(r[7] for r in rec)
     out = [f"span {(t1 - t0) / 1e3:.2f} us, CTA start spread {(max(r[0] for r in rec) - t0) / 1e3:.2f}"]
@@ -55,6 +55,16 @@ def timeline(buf, nc):
             out.append(f"{name} {statistics.median(d):.2f}/{max(d):.2f}")
     ends = sorted((r[7] - t0) / 1e3 for r in rec)
     out.append(f"CTA end p50 {ends[len(ends) // 2]:.2f} max {ends[-1]:.2f}")
+    # the slowest CTAs: where their time went
+    order = sorted(range(nc), key=lambda c: -(rec[c][7] - rec[c][0]))[:3]
+    for c in order:
+        r = rec[c]
+        walk = (f"walk {(r[8] - r[1]) / 1e3:.2f} commit {(r[11] - r[8]) / 1e3:.2f} pub+ {(r[2] - r[11]) / 1e3:.2f}"
+                if r[8] and r[2] and r[11] else "no reg walk")
+        info = r[9]
+        out.append(f"[slow {(r[7] - r[0]) / 1e3:.2f}: acc {(r[2] - r[1]) / 1e3 if r[2] else 0:.2f} ({walk}; "
+                   f"len {info & 0xFFFF} stacks {(info >> 16) & 0xFF} frames {info >> 24}) "
+                   f"deps {r[10] & 0xFFFFFFFF} tops {r[10] >> 32} walks {(r[5] - (r[4] or r[3])) / 1e3:.2f}]")
     return " | ".join(out)
 
 
@@ -104,6 +114,8 @@ def main(steps=12, flush=True, fused=False, grammar="json", step_mode=False):
                 buf[32 + b] = 0
         allowed = bench.unpack_allowed(bitmask, vocab.size)
         toks = bench.sample_tokens(allowed, structural, s, rows, force=force).to(torch.int32)
+        if step_mode and s == steps - 1:
+            print(f"  arena slots used: {lib.gm_pool_arena_used(pool.handle)}")
         if step_mode:
             fp = [buf[16], buf[17], buf[48], buf[18], buf[20], buf[21], buf[22], buf[23]]
             d = [(fp[k + 1] - fp[k]) / 1e3 if fp[k + 1] >= fp[k] > 0 else float("nan") for k in range(7)]

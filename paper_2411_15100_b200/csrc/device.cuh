@@ -755,6 +755,11 @@ struct DevPool {
   const uint8_t* hint_blob;
   const int4* hint_tokrec;
   int32_t hint_blob_bytes, hint_V;
+  // host-side launch setting: the pool's hot block (arena + slot headers +
+  // ring positions) as an L2 persisting access-policy window, or null
+  void* l2_base;
+  size_t l2_bytes;
+  float l2_hit;
 };
 
 // Phase timestamps of CTA 0 (diagnostics only): trace[kernel*16 + phase].
@@ -882,20 +887,11 @@ __device__ inline int rwalker_commit_inplace(RWalker<R, F>& w, const DevArena& A
   constexpr int kBatch = 8;
   for (int q0 = 0; q0 < w.nf; q0 += kBatch) {
     unsigned long long res[kBatch];
-    // test before test-and-set: most frames are already interned (requests
-    // share stack prefixes, hash-consed to the same slot), and a plain load
-    // of a hot slot does not serialise at L2 the way 100+ concurrent CASes
-    // on it do (measured ~5 us per contended frame)
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
       const int q = q0 + j;
       res[j] = kEmptyKey;
-      if (q < w.nf && gmap[q] >= 0) res[j] = arena_load(A, gmap[q]);
-    }
-#pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-      const int q = q0 + j;
-      if (q < w.nf && gmap[q] >= 0 && res[j] == kEmptyKey) res[j] = atomicCAS(A.keys + gmap[q], kEmptyKey, keyq[q]);
+      if (q < w.nf && gmap[q] >= 0) res[j] = atomicCAS(A.keys + gmap[q], kEmptyKey, keyq[q]);
     }
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {

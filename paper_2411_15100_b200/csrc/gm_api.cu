@@ -31,6 +31,7 @@ gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t
                       uint8_t*, int32_t, cudaStream_t);
 gm_status launch_fill_apply(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*, int32_t,
                             void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
+gm_status launch_l2_touch(void* base, size_t bytes, const L2Window& win);
 gm_status launch_step(const DevPool&, const int32_t*, int32_t, const int32_t*, uint8_t*, int32_t, int32_t*, int64_t,
                       const int32_t*, int32_t, void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_accept_tokens(const DevPool&, const int32_t*, const int32_t*, int32_t, uint8_t*, cudaStream_t);
@@ -557,6 +558,31 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   }
   p->dev = DevPool{capacity, max_stacks, H,   tops, meta, head, hist, win, bind,
                    DevArena{keys, acap - 1, err}, err, hdr, trace};
+  // opt-in L2 persistence for the arena (GMASK_L2_PERSIST=1): a device-wide
+  // persisting carve-out + a persisting access-policy window on the step
+  // launches; measured no gain on the JSON bench (the contended arena lines
+  // are L2-resident anyway)
+  const char* pe = getenv("GMASK_L2_PERSIST");
+  if (pe && pe[0] == '1') {
+    int dev = 0, max_persist = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    const size_t abytes = sizeof(unsigned long long) * acap;
+    if (max_persist > 0) {
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      const size_t want = std::min<size_t>((size_t)max_persist, std::max(cur, abytes));
+      if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      if (cur > 0) {
+        p->dev.l2_base = keys;
+        p->dev.l2_bytes = abytes;
+        p->dev.l2_hit = abytes <= cur ? 1.0f : (float)cur / (float)abytes;
+        launch_l2_touch(keys, abytes, L2Window{keys, abytes, p->dev.l2_hit});
+      }
+      cudaGetLastError();  // the limit is advisory: ignore a refusal
+    }
+  }
   p->scratch_bytes = sb;
   p->scratch_cap = 1 << 16;
   p->scratch_i32 = scr;

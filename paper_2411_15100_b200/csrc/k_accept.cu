@@ -194,7 +194,9 @@ gm_status launch_accept_tokens(const DevPool& P, const int32_t* slots, const int
   if (n <= 0) return GM_OK;
   static gm_status once = set_smem_attr(reinterpret_cast<const void*>(accept_tokens_kernel));
   if (once) return once;
-  GM_CUDA_TRY(launch_pdl(accept_tokens_kernel, dim3(n), dim3(kAccThreads), kStageBytes, s, P, slots, toks, n, acc));
+  const L2Window win{P.l2_base, P.l2_bytes, P.l2_hit};
+  GM_CUDA_TRY(launch_pdl_w(&win, accept_tokens_kernel, dim3(n), dim3(kAccThreads), kStageBytes, s, P, slots, toks, n,
+                           acc));
   return GM_OK;
 }
 gm_status launch_accept_bytes(const DevPool& P, int32_t slot, const uint8_t* data, int64_t len, uint8_t* acc,

@@ -111,7 +111,23 @@ apply_scalar_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab, in
   }
 }
 
+// Read one word of every 128-byte line of a buffer (launched under an L2
+// persisting access-policy window: pulls the pool's hot block into L2).
+__global__ void l2_touch_kernel(const uint4* __restrict__ p, int64_t lines, uint32_t* sink) {
+  uint32_t acc = 0;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < lines; l += (int64_t)gridDim.x * blockDim.x)
+    acc ^= __ldcg(p + l * 8).x;
+  if (acc == 0x9E3779B9u && sink) *sink = acc;  // keeps the loads (sink is null)
+}
+
 }  // namespace
+
+gm_status launch_l2_touch(void* base, size_t bytes, const L2Window& win) {
+  const int64_t lines = (int64_t)(bytes / 128);
+  GM_CUDA_TRY(launch_pdl_w(&win, l2_touch_kernel, dim3(296), dim3(256), 0, (cudaStream_t)0,
+                           static_cast<const uint4*>(base), lines, static_cast<uint32_t*>(nullptr)));
+  return GM_OK;
+}
 }  // namespace gm
 
 using namespace gm;

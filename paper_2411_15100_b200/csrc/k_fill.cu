@@ -122,7 +122,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   __shared__ RingPos rp;
   __shared__ int4 s_rec[2];
-  __shared__ int s_just_term, s_dirty;
+  __shared__ int s_just_term, s_dirty, s_walked;
   int32_t tok = -1;
   if (ACCEPT && SA.tokens) {
     // volatile load: `tokens` may be pinned host memory written by the host
@@ -318,6 +318,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     s_nt = nt;
   }
   for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) dep_acc[w] = 0u;
+  if (threadIdx.x == 0) s_walked = 0;
   __syncthreads();
   trace_mark(P, 1, 2);
   if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
@@ -386,6 +387,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
           continue;
         }
       }
+      if (P.trace) atomicAdd(&s_walked, 1 | (e.y << 16));  // diagnostics: walks, bytes walked
       const int4 inl = __ldg(rec + 1);
       const int2 t = s_top[s];
       const uint8_t* far = rec_base + e.z;  // bytes beyond the inline 16
@@ -489,7 +491,8 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       tr[4] = t_ctx; tr[5] = t_walks; tr[6] = t_merge; tr[7] = t1;
       tr[8] = t_walk;                // accept: register walk done (0: no walk / general path)
       tr[9] = walk_info;             // token bytes | stacks << 16 | walker frames << 24
-      tr[10] = (unsigned long long)total | ((unsigned long long)nt << 32);  // dependents, tops
+      tr[10] = (unsigned long long)total | ((unsigned long long)nt << 32) |
+               ((unsigned long long)(s_walked & 0xFFFF) << 40);  // dependents, tops, dependents walked
       tr[11] = acc_ts[0];            // accept: frames interned (publish starts)
     }
     if (c == 0) P.trace[63] = (unsigned long long)n_split;
@@ -508,8 +511,15 @@ static gm_status fill_attrs() {
 // Splits per request: enough CTAs to cover the SMs once,
 // at most kMaxSplits; one when the caller wants the per-row need_apply flag.
 constexpr int kMaxSplits = 8;
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
 static int fill_splits(int32_t n, bool need_apply) {
   if (need_apply) return 1;
+  static const int forced = env_int("GMASK_FILL_SPLITS", 0);  // diagnostics
+  if (forced > 0) return forced > kMaxSplits ? kMaxSplits : forced;
   int sms = 148;
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -517,6 +527,14 @@ static int fill_splits(int32_t n, bool need_apply) {
   // resident CTA would take (measured: two per SM is slower)
   int s = sms / (n > 0 ? n : 1);
   return s < 1 ? 1 : (s > kMaxSplits ? kMaxSplits : s);
+}
+
+// threads per fill CTA: 512 for one CTA per request; with splits the CTAs
+// are smaller so two fit per SM (GMASK_FILL_THREADS overrides, diagnostics)
+static int fill_threads(int splits) {
+  static const int forced = env_int("GMASK_FILL_THREADS", 0);
+  if (forced > 0) return forced;
+  return splits > 1 ? 256 : kFillThreads;
 }
 
 static int32_t split_words(int32_t Wmax, int splits) { return ((Wmax + 3) / 4 + splits - 1) / splits * 4; }
@@ -535,7 +553,8 @@ gm_status launch_fill(const DevPool& P, const int32_t* slots, int32_t n, int32_t
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
   static gm_status attrs = fill_attrs<false, false>();
   if (attrs) return attrs;
-  GM_CUDA_TRY(launch_pdl(fill_kernel<false, false>, dim3(n, splits), dim3(kFillThreads), smem, s, P, slots, n,
+  const L2Window win{P.l2_base, P.l2_bytes, P.l2_hit};
+  GM_CUDA_TRY(launch_pdl_w(&win, fill_kernel<false, false>, dim3(n, splits), dim3(fill_threads(splits)), smem, s, P, slots, n,
                          reinterpret_cast<uint32_t*>(bitmask), bstride, rows, need_apply, Wp, nullptr, (int64_t)0,
                          (int64_t)0, 2, 0u, StepArgs{nullptr, nullptr, 0}));
   return GM_OK;
@@ -552,7 +571,8 @@ gm_status launch_fill_apply(const DevPool& P, const int32_t* slots, int32_t n, i
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
   static gm_status attrs = fill_attrs<true, false>();
   if (attrs) return attrs;
-  GM_CUDA_TRY(launch_pdl(fill_kernel<true, false>, dim3(n, splits), dim3(kFillThreads), smem, s, P, slots, n,
+  const L2Window win{P.l2_base, P.l2_bytes, P.l2_hit};
+  GM_CUDA_TRY(launch_pdl_w(&win, fill_kernel<true, false>, dim3(n, splits), dim3(fill_threads(splits)), smem, s, P, slots, n,
                          reinterpret_cast<uint32_t*>(bitmask), bstride, rows, nullptr, Wp, static_cast<char*>(logits),
                          lstride_bytes, vocab, (int)eb, neg, StepArgs{nullptr, nullptr, 0}));
   return GM_OK;
@@ -568,17 +588,18 @@ gm_status launch_step(const DevPool& P, const int32_t* slots, int32_t n, const i
   const size_t smem = fill_smem(split_words(Wmax, 1));
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
   const StepArgs sa{tokens, accepted, recycle};
+  const L2Window win{P.l2_base, P.l2_bytes, P.l2_hit};
   uint32_t* bm = reinterpret_cast<uint32_t*>(bitmask);
   if (logits) {
     static gm_status attrs = fill_attrs<true, true>();
     if (attrs) return attrs;
-    GM_CUDA_TRY(launch_pdl(fill_kernel<true, true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm, bstride,
+    GM_CUDA_TRY(launch_pdl_w(&win, fill_kernel<true, true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm, bstride,
                            rows, nullptr, split_words(Wmax, 1), static_cast<char*>(logits), lstride_bytes, vocab,
                            (int)eb, neg, sa));
   } else {
     static gm_status attrs = fill_attrs<false, true>();
     if (attrs) return attrs;
-    GM_CUDA_TRY(launch_pdl(fill_kernel<false, true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm,
+    GM_CUDA_TRY(launch_pdl_w(&win, fill_kernel<false, true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm,
                            bstride, rows, nullptr, split_words(Wmax, 1), nullptr, (int64_t)0, (int64_t)0, 2, 0u, sa));
   }
   GM_LAUNCH_CHECK();

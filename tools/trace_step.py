@@ -53,6 +53,8 @@ def timeline(buf, nc):
                 d.append((b - a) / 1e3)
         if d:
             out.append(f"{name} {statistics.median(d):.2f}/{max(d):.2f}")
+    wk = [(r[10] >> 40) & 0xFFFF for r in rec]
+    out.append(f"deps walked per CTA: mean {sum(wk) / len(wk):.1f} max {max(wk)}")
     ends = sorted((r[7] - t0) / 1e3 for r in rec)
     out.append(f"CTA end p50 {ends[len(ends) // 2]:.2f} max {ends[-1]:.2f}")
     # the slowest CTAs: where their time went
@@ -64,7 +66,7 @@ def timeline(buf, nc):
         info = r[9]
         out.append(f"[slow {(r[7] - r[0]) / 1e3:.2f}: acc {(r[2] - r[1]) / 1e3 if r[2] else 0:.2f} ({walk}; "
                    f"len {info & 0xFFFF} stacks {(info >> 16) & 0xFF} frames {info >> 24}) "
-                   f"deps {r[10] & 0xFFFFFFFF} tops {r[10] >> 32} walks {(r[5] - (r[4] or r[3])) / 1e3:.2f}]")
+                   f"deps {r[10] & 0xFFFFFFFF} tops {(r[10] >> 32) & 0xFF} walked {(r[10] >> 40) & 0xFFFF} walks {(r[5] - (r[4] or r[3])) / 1e3:.2f}]")
     return " | ".join(out)
 
 

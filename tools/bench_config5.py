@@ -115,6 +115,7 @@ def main():
     S = args.warmup + args.steps
     sample_rows = min(B, 4)
     keep = torch.empty((S, sample_rows, W), dtype=torch.int32, device=dev)
+    masks_all = torch.empty((S, B, W), dtype=torch.int32, device=dev)
     toks_hist = torch.empty((S, B), dtype=torch.int32, device=dev)
     masked = torch.zeros(S, dtype=torch.int64, device=dev)
     ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(S)]
@@ -128,6 +129,7 @@ def main():
             allowed = bench.unpack_allowed(bitmask, V)
             masked[s] = (~allowed).sum()
             keep[s] = bitmask[:sample_rows]
+            masks_all[s] = bitmask
             toks = bench.sample_tokens(allowed, structural, s, rows).to(torch.int32)
             toks_hist[s] = toks
             ev[s][2].record(stream)
@@ -138,6 +140,45 @@ def main():
     pool.check()
     step_us = statistics.fmean(ev[s][0].elapsed_time(ev[s][1]) for s in range(args.warmup, S)) * 1e3
     acc_us = statistics.fmean(ev[s][2].elapsed_time(ev[s][3]) for s in range(args.warmup, S)) * 1e3
+
+    # the same decode steps as K5 launches back to back (CUDA graph, one event
+    # bracket; inputs larger than L2), every mask compared with the pass above
+    from paper_2411_15100_b200.matcher import batch_step
+
+    masks_t = torch.empty_like(masks_all)
+    acc_t = torch.zeros((S, B), dtype=torch.uint8, device=dev)
+
+    def k5(s):
+        batch_step(pool, slots, toks_hist[s - 1] if s > 0 else None, acc_t[s - 1] if s > 0 else None, masks_t[s],
+                   ring[s % 8], recycle=True)
+
+    for m in matchers:
+        m.reset()
+    for s in range(args.warmup):
+        k5(s)
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream(device=dev)
+    g_w, g_t = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_w, stream=cap):
+        for s in range(args.warmup):
+            k5(s)
+    with torch.cuda.graph(g_t, stream=cap):
+        for s in range(args.warmup, S):
+            k5(s)
+    reps = []
+    for _ in range(3):
+        for m in matchers:
+            m.reset()
+        g_w.replay()
+        torch.cuda.synchronize()
+        ev[0][0].record(stream)
+        g_t.replay()
+        ev[0][1].record(stream)
+        torch.cuda.synchronize()
+        reps.append(ev[0][0].elapsed_time(ev[0][1]) / args.steps * 1e3)
+    k5_b2b_us = statistics.median(reps)
+    k5_mism = int((masks_t != masks_all).any(dim=2).sum())
+    k5_acc = bool(acc_t[:S - 1].bool().all())
 
     # oracle parity on the sampled rows (their own schemas) + oracle compile time
     from oracle import compile_oracle_bundle
@@ -168,7 +209,9 @@ def main():
         "compile_ms_rank_total": compile_total_ms,
         "compile_split_ms_mean": split,
         "cache_keys_per_schema": {"mean": statistics.fmean(keys), "max": max(keys)},
-        "fill_apply_us_per_step": step_us, "accept_recycle_us_per_step": acc_us,
+        "k5_step_us_back_to_back": k5_b2b_us, "k5_mask_mismatches_vs_flushed_pass": k5_mism,
+        "k5_all_accepted": k5_acc,
+        "fill_apply_us_per_step_l2_flushed": step_us, "accept_recycle_us_per_step_l2_flushed": acc_us,
         "masked_fraction": float(masked[args.warmup:].double().mean().item()) / (B * V),
         "oracle_parity": {"requests": min(sample_rows, args.oracle_schemas), "steps_checked": checked,
                           "mismatches": mism},
@@ -176,7 +219,7 @@ def main():
         "cpu_reference_compile_s_1024_extrapolated_1core": (statistics.fmean(ocomp) * args.schemas) if ocomp else None,
         "cpu": bench._cpu_name(),
         "clocks": clocks.summary(),
-        "l2": "flushed before every step (256 MiB write)",
+        "l2": "k5 back to back: inputs larger than L2 (logits ring 8 x 32.8 MB); *_l2_flushed: 256 MiB flush before every step",
     }
     line = json.dumps(out)
     print(line)

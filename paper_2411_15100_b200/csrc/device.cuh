@@ -49,7 +49,8 @@ enum : uint32_t {
 struct BlobHdr {
   int32_t bytes, n_classes, n_nodes, o_bc;
   int32_t o_flags, o_toff, o_trans, o_pool;
-  int32_t o_kon, o_rule, o_ninfo, o_fast, o_callers, start_node, pad[2];
+  int32_t o_kon, o_rule, o_ninfo, o_fast, o_callers, start_node;
+  uint32_t ctx2_lo, ctx2_hi;  // binding blobs: device address of the two-level context classes (or 0)
 };
 static_assert(sizeof(BlobHdr) == 64, "BlobHdr layout");
 
@@ -68,6 +69,7 @@ struct DevGrammar {
   const int4* node_info;       // binding views only
   const int32_t* fast;         // [n_nodes*n_classes] single-stack DFA move, -1 dies, -2 general
   const int32_t* callers;      // [n_rules*kMaxCallers] return nodes that can sit below a frame of the rule, -1 pad
+  const uint32_t* ctx2;        // binding views: [n_dep*kMaxCallers] two-level context classes, or null
   const uint8_t* blob;
   int32_t blob_bytes;
 };
@@ -89,6 +91,7 @@ __device__ __forceinline__ DevGrammar blob_view(const uint8_t* base) {
   g.node_info = h->o_ninfo ? reinterpret_cast<const int4*>(base + h->o_ninfo) : nullptr;
   g.fast = reinterpret_cast<const int32_t*>(base + h->o_fast);
   g.callers = reinterpret_cast<const int32_t*>(base + h->o_callers);
+  g.ctx2 = reinterpret_cast<const uint32_t*>(((unsigned long long)h->ctx2_hi << 32) | h->ctx2_lo);
   g.blob = base;
   g.blob_bytes = h->bytes;
   return g;
@@ -891,7 +894,11 @@ __device__ inline int rwalker_commit_inplace(RWalker<R, F>& w, const DevArena& A
     for (int j = 0; j < kBatch; ++j) {
       const int q = q0 + j;
       res[j] = kEmptyKey;
+#ifdef GM_EXPERIMENT_NO_CAS  // timing experiment only: assumes no collision
+      if (q < w.nf && gmap[q] >= 0) { A.keys[gmap[q]] = keyq[q]; res[j] = kEmptyKey; }
+#else
       if (q < w.nf && gmap[q] >= 0) res[j] = atomicCAS(A.keys + gmap[q], kEmptyKey, keyq[q]);
+#endif
     }
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {

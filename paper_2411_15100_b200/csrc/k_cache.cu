@@ -182,6 +182,61 @@ __global__ void dep_context_kernel(DevGrammar G, const int32_t* __restrict__ dep
   rec[2 * i].w = (int32_t)w;
 }
 
+// Two-level context classes: for a dependent whose one-level class at
+// caller c1 is "deeper", walk it from [c2 | c1 | n] for every caller c2 of
+// c1's rule (and from [c1 | n] with c1's frame at the bottom when c1's rule
+// is the root rule, index kRootCaller): accept / reject / still deeper.
+// ctx2[dep * kMaxCallers + j] packs the classes over c2 for caller j.  The
+// fill uses them when the request's stack has the matching grandparent
+// frame, so most "deeper" dependents need no walk at all.
+__device__ uint32_t context_class2(const DevGrammar& G, int32_t c2, int32_t c1, int32_t node, const int4& e,
+                                   const int4& inl, const uint8_t* far) {
+  const DevArena A{nullptr, 0, nullptr};
+  RWalker<8, 48> rw;
+  rw.init(nullptr, nullptr, 0);
+  const int32_t f2 = c2 < 0 ? -1 : rw.push(G, A, -1, c2);
+  rw.add(rw.push(G, A, f2, c1), node);
+  bool popped = false;
+  for (int b = 0; b < e.y && rw.n > 0 && !rw.spill; ++b) {
+    bool pb = false;
+    rw.step(G, A, rec_byte(inl, far, b), &pb);
+    popped |= pb;
+  }
+  if (rw.spill || rw.err) return kCtxUnknown;
+  if (rw.n > 0) return kCtxAccept;
+  return (popped && c2 >= 0) ? kCtxDeeper : kCtxReject;
+}
+
+__global__ void dep_context2_kernel(DevGrammar G, const int32_t* __restrict__ dep_off, int32_t n_keys, int64_t n_dep,
+                                    const int4* __restrict__ rec, const uint8_t* __restrict__ tok_base,
+                                    uint32_t* __restrict__ ctx2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_dep) return;
+  int32_t lo = 0, hi = n_keys - 1;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (dep_off[mid] <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  const int32_t node = G.cache_keys[lo];
+  const int32_t* cr = G.callers + (size_t)G.node_rule[node] * kMaxCallers;
+  const int4 e = rec[2 * i], inl = rec[2 * i + 1];
+  const uint8_t* far = tok_base + e.z;
+  const int32_t root_rule = G.node_rule[G.start_node];
+  for (int j = 0; j < kMaxCallers; ++j) {
+    uint32_t w = 0;
+    const int32_t c1 = j < kRootCaller ? cr[j] : -1;
+    if (c1 >= 0 && (((uint32_t)e.w >> (2 * j)) & 3u) == kCtxDeeper) {
+      const int32_t r1 = G.node_rule[c1];
+      const int32_t* cr2 = G.callers + (size_t)r1 * kMaxCallers;
+      for (int j2 = 0; j2 < kRootCaller && cr2[j2] >= 0; ++j2)
+        w |= context_class2(G, cr2[j2], c1, node, e, inl, far) << (2 * j2);
+      if (r1 == root_rule) w |= context_class2(G, -1, c1, node, e, inl, far) << (2 * kRootCaller);
+    }
+    ctx2[i * kMaxCallers + j] = w;
+  }
+}
+
 }  // namespace gm
 
 using namespace gm;
@@ -217,6 +272,13 @@ gm_status launch_dep_context(const DevGrammar& G, const int32_t* dep_off, int32_
                              const uint8_t* tok_base, cudaStream_t s) {
   if (n_dep <= 0) return GM_OK;
   dep_context_kernel<<<(unsigned)ceil_div(n_dep, 128), 128, 0, s>>>(G, dep_off, n_keys, n_dep, rec, tok_base);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_dep_context2(const DevGrammar& G, const int32_t* dep_off, int32_t n_keys, int64_t n_dep,
+                              const int4* rec, const uint8_t* tok_base, uint32_t* ctx2, cudaStream_t s) {
+  if (n_dep <= 0) return GM_OK;
+  dep_context2_kernel<<<(unsigned)ceil_div(n_dep, 64), 64, 0, s>>>(G, dep_off, n_keys, n_dep, rec, tok_base, ctx2);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

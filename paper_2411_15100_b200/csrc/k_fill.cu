@@ -99,7 +99,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   __shared__ int s_partial, s_nt, s_nrows;
   __shared__ int32_t s_key[32], s_lo[32], s_hi[32];
   __shared__ int2 s_top[32];
-  __shared__ int s_cj[32];
+  __shared__ int s_cj[32], s_cj2[32];
   __shared__ __align__(8) unsigned long long rows_bar;
   __shared__ __align__(8) unsigned long long blob_bar;
   pdl_trigger();
@@ -138,7 +138,8 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   __syncthreads();
   // the hint is usable iff this slot is bound to it; otherwise drain the
   // early copy and stage the slot's own blob
-  const bool hint_ok = hinted && hd.blob == P.hint_blob && hd.tokrec == P.hint_tokrec;
+  const bool hint_ok = hinted && hd.blob == P.hint_blob && hd.blob_bytes == P.hint_blob_bytes &&
+                       hd.tokrec == P.hint_tokrec && hd.V == P.hint_V;
   if (hinted) mbar_wait(&blob_bar, 0);
   trace_mark(P, 1, 1);
   if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_hdr));
@@ -341,10 +342,11 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     if ((int)threadIdx.x < nt) {
       const int2 t = s_top[threadIdx.x];
       int cj = kRootCaller;  // the root frame: nothing below it
+      int cj2 = -1;          // the grandparent frame's caller index (two-level classes)
       if (t.x >= 0) {
         cj = -1;
-        const unsigned long long pk =
-            (hd.nchain > 0 && hd.chain_h[0] == t.x) ? hd.chain_k[0] : arena_load(P.arena, t.x);
+        const bool on_chain = hd.nchain > 0 && hd.chain_h[0] == t.x;
+        const unsigned long long pk = on_chain ? hd.chain_k[0] : arena_load(P.arena, t.x);
         if (pk != kEmptyKey) {
           const int32_t pn = key_node(pk);
           const int32_t* cr = G.callers + (size_t)G.node_rule[t.y] * kMaxCallers;
@@ -353,9 +355,28 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
             if (c < 0) break;
             if (c == pn) { cj = j; break; }
           }
+          if (cj >= 0 && G.ctx2) {
+            const int32_t h2 = key_parent(pk);
+            if (h2 < 0) {
+              cj2 = kRootCaller;  // pn's frame is the bottom one
+            } else {
+              const unsigned long long k2 =
+                  (on_chain && hd.nchain > 1 && hd.chain_h[1] == h2) ? hd.chain_k[1] : arena_load(P.arena, h2);
+              if (k2 != kEmptyKey) {
+                const int32_t pn2 = key_node(k2);
+                const int32_t* cr2 = G.callers + (size_t)G.node_rule[pn] * kMaxCallers;
+                for (int j = 0; j < kRootCaller; ++j) {
+                  const int32_t c = cr2[j];
+                  if (c < 0) break;
+                  if (c == pn2) { cj2 = j; break; }
+                }
+              }
+            }
+          }
         }
       }
       s_cj[threadIdx.x] = cj;
+      s_cj2[threadIdx.x] = cj2;
     }
     __syncthreads();
     trace_mark(P, 1, 4);
@@ -380,7 +401,9 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
       const uint32_t bit = 1u << (tid & 31);
       if (*acc_w & bit) continue;  // already allowed by another stack
       if (s_cj[s] >= 0) {
-        const uint32_t cls = ((uint32_t)e.w >> (2 * s_cj[s])) & 3u;
+        uint32_t cls = ((uint32_t)e.w >> (2 * s_cj[s])) & 3u;
+        if (cls == kCtxDeeper && s_cj2[s] >= 0)  // two-level class from the grandparent frame
+          cls = (__ldg(G.ctx2 + (size_t)(s_lo[s] + (q - base)) * kMaxCallers + s_cj[s]) >> (2 * s_cj2[s])) & 3u;
         if (cls == kCtxReject) continue;
         if (cls == kCtxAccept) {
           atomicOr(acc_w, bit);

@@ -36,6 +36,8 @@ gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t
 gm_status launch_fill_apply(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*, int32_t,
                             void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_l2_touch(void* base, size_t bytes, const L2Window& win);
+gm_status launch_step_ptok(const DevPool&, const int32_t*, int32_t, const int32_t*, uint8_t*, int32_t, int32_t*, int64_t,
+                           int32_t, void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_step(const DevPool&, const int32_t*, int32_t, const int32_t*, uint8_t*, int32_t, int32_t*, int64_t,
                       const int32_t*, int32_t, void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_accept_tokens(const DevPool&, const int32_t*, const int32_t*, int32_t, uint8_t*, cudaStream_t);
@@ -769,6 +771,7 @@ struct gm_decoder {
   std::vector<uint8_t*> acc_host, acc_dev;
   std::vector<cudaEvent_t> h2d, k5, done;
   std::vector<int> issued;
+  bool no_ptok = false;             // GMASK_DECODER_COPY=1: token ids via the H2D copy path
   cudaStream_t copy = nullptr;      // H2D of token ids
   cudaStream_t copy_out = nullptr;  // D2H of accepted flags (separate: the next H2D must not queue behind it)
 };
@@ -804,6 +807,10 @@ gm_status gm_decoder_create(gm_pool* p, const int32_t* slots, int32_t n, int32_t
   d->vocab = vocab_size;
   d->lstride = logits_stride;
   d->issued.assign(n_buf, 0);
+  {
+    const char* e = getenv("GMASK_DECODER_COPY");
+    d->no_ptok = e && e[0] == '1';
+  }
   auto bail = [&](cudaError_t e) {
     decoder_free(d);
     return fail(GM_ERR_CUDA, std::string("gm_decoder_create: ") + cudaGetErrorString(e));
@@ -842,6 +849,26 @@ gm_status gm_decoder_step(gm_decoder* d, int32_t buf, const int32_t* host_tokens
   cudaStream_t s = as_stream(stream);
   if (d->issued[buf]) GM_CUDA_TRY(cudaEventSynchronize(d->done[buf]));  // staging reuse guard
   const int32_t n = d->n;
+  if (host_tokens && n <= 512 && !d->no_ptok) {
+    // token ids by value in the K5 launch parameters: no staging, no H2D copy
+    int32_t eb = 2;
+    uint32_t neg = 0;
+    switch (d->dtype) {
+      case GM_DTYPE_F32: eb = 4; neg = 0xFF800000u; break;
+      case GM_DTYPE_F16: eb = 2; neg = 0xFC00FC00u; break;
+      default: eb = 2; neg = 0xFF80FF80u; break;
+    }
+    gm_status st = launch_step_ptok(d->pool->dev, d->slots, n, host_tokens, d->acc_dev[buf], d->recycle,
+                                    d->bitmask[buf], d->bstride, d->pool->max_w, d->logits[buf], eb, neg, d->vocab,
+                                    d->lstride * eb, s);
+    if (st) return st;
+    GM_CUDA_TRY(cudaEventRecord(d->k5[buf], s));
+    GM_CUDA_TRY(cudaStreamWaitEvent(d->copy_out, d->k5[buf], 0));
+    GM_CUDA_TRY(cudaMemcpyAsync(d->acc_host[buf], d->acc_dev[buf], (size_t)n, cudaMemcpyDeviceToHost, d->copy_out));
+    GM_CUDA_TRY(cudaEventRecord(d->done[buf], d->copy_out));
+    d->issued[buf] = 1;
+    return GM_OK;
+  }
   if (host_tokens) {
     std::memcpy(d->tok_host[buf], host_tokens, (size_t)n * 4);
     GM_CUDA_TRY(cudaMemcpyAsync(d->tok_dev[buf], d->tok_host[buf], (size_t)n * 4, cudaMemcpyHostToDevice, d->copy));

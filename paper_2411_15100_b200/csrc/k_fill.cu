@@ -22,6 +22,8 @@
 //      ancestor chain), setting bits of a shared-memory row;
 //   4. rows, dependent bits and universe are merged from shared memory and
 //      stored with 128-bit stores.
+#include <cstring>
+
 #include "accept.cuh"
 
 namespace gm {
@@ -84,12 +86,19 @@ struct StepArgs {
   int32_t recycle;
 };
 
+// Token ids carried in the launch parameters (the native decode loop passes
+// the host's sampled ids by value: no H2D copy on the step's path).
+constexpr int kParamTokens = 512;
+struct TokParams {
+  int32_t v[kParamTokens];
+};
+
 template <bool APPLY, bool ACCEPT>
-__global__ void __maxnreg__(128)
-fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
-            int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wp,
-            char* __restrict__ logits, int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg,
-            StepArgs SA) {
+__device__ __forceinline__ void
+fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
+          int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wp,
+          char* __restrict__ logits, int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg,
+          StepArgs SA, const int32_t* ptok) {
   extern __shared__ __align__(16) uint8_t smem[];
   const size_t part_bytes = ((size_t)Wp * 4 + 15) & ~(size_t)15;
   uint32_t* dep_acc = reinterpret_cast<uint32_t*>(smem);  // [Wp] this CTA's words
@@ -124,10 +133,12 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   __shared__ int4 s_rec[2];
   __shared__ int s_just_term, s_dirty, s_walked;
   int32_t tok = -1;
-  if (ACCEPT && SA.tokens) {
+  const bool do_acc = ACCEPT && (SA.tokens || ptok);
+  if (do_acc) {
     // volatile load: `tokens` may be pinned host memory written by the host
     // between graph replays (zero-copy H2D, graph.py), never cached
-    asm volatile("ld.global.cv.s32 %0, [%1];" : "=r"(tok) : "l"(SA.tokens + i));
+    if (ptok) tok = ptok[i];
+    else asm volatile("ld.global.cv.s32 %0, [%1];" : "=r"(tok) : "l"(SA.tokens + i));
     load_header_ring(P, slot, &hd, &rp);
     // token record from the hinted vocabulary, in the header's round trip
     if (hinted && threadIdx.x < 2 && tok >= 0 && tok < P.hint_V)
@@ -147,7 +158,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   unsigned long long t_acc = 0;
   const bool vec = (!bitmask || (reinterpret_cast<uintptr_t>(bitmask + row * bstride) & 15) == 0) && (hd.W % 4 == 0);
   __shared__ int s_pref;  // K5: cache rows already in flight (count), -1 none, -2 issued but stale
-  if (ACCEPT && SA.tokens) {  // launched with one split: one accept per request
+  if (do_acc) {  // launched with one split: one accept per request
     const bool in_range = tok >= 0 && tok < hd.V;
     if (hint_ok) {
       Gs = blob_view(tables);
@@ -272,12 +283,12 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
   const int32_t per = ((W + 3) / 4 + n_split - 1) / n_split * 4;  // words per split
   const int32_t w_lo = min(W, split * per), w_hi = min(W, w_lo + per), nw = w_hi - w_lo;
   const bool terminated = hd.flags & 1;
-  const int pref = (ACCEPT && SA.tokens) ? s_pref : -1;
+  const int pref = do_acc ? s_pref : -1;
   if (threadIdx.x == 0) {
     s_partial = 0;
     int nt = hd.ntops;
     if (terminated) {  // a request that terminated in this very step gets an empty row, no error
-      if (split == 0 && !(ACCEPT && SA.tokens && s_just_term)) atomicOr(P.err, kErrTerminated);
+      if (split == 0 && !(do_acc && s_just_term)) atomicOr(P.err, kErrTerminated);
       nt = 0;
     } else if (nt >= 0) {
       // issue the row copies first: they are the longest-latency loads
@@ -336,7 +347,7 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
     P.trace[16 + 10] = (unsigned long long)nt;
   }
   if (total) {
-    const DevGrammar G = (ACCEPT && SA.tokens) ? Gs : hint_ok ? blob_view(tables) : stage_blob(hd.blob, hd.blob_bytes, tables);
+    const DevGrammar G = do_acc ? Gs : hint_ok ? blob_view(tables) : stage_blob(hd.blob, hd.blob_bytes, tables);
     // caller index of each top's parent frame within the callers of the
     // top's rule: selects the dependents' one-level context class
     if ((int)threadIdx.x < nt) {
@@ -523,6 +534,28 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
 }
 
 template <bool APPLY, bool ACCEPT>
+__global__ void __maxnreg__(128)
+fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
+            int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wp,
+            char* __restrict__ logits, int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg,
+            StepArgs SA) {
+  fill_body<APPLY, ACCEPT>(P, slots, n, bitmask, bstride, rows, need_apply, Wp, logits, lstride_bytes, ap_vocab,
+                           ap_eb, ap_neg, SA, nullptr);
+}
+
+// K5 with the token ids in the launch parameters (__grid_constant__: read
+// in place from the parameter bank)
+template <bool APPLY>
+__global__ void __maxnreg__(128)
+step_ptok_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
+                 int64_t bstride, const int32_t* __restrict__ rows, int32_t Wp, char* __restrict__ logits,
+                 int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg, StepArgs SA,
+                 const __grid_constant__ TokParams tp) {
+  fill_body<APPLY, true>(P, slots, n, bitmask, bstride, rows, nullptr, Wp, logits, lstride_bytes, ap_vocab, ap_eb,
+                         ap_neg, SA, tp.v);
+}
+
+template <bool APPLY, bool ACCEPT>
 static gm_status fill_attrs() {
   GM_CUDA_TRY(cudaFuncSetAttribute(fill_kernel<APPLY, ACCEPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    220 * 1024));
@@ -626,6 +659,43 @@ gm_status launch_step(const DevPool& P, const int32_t* slots, int32_t n, const i
                            bstride, rows, nullptr, split_words(Wmax, 1), nullptr, (int64_t)0, (int64_t)0, 2, 0u, sa));
   }
   GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+
+// K5 from the native decode loop: token ids by value (n <= kParamTokens).
+template <bool APPLY>
+static gm_status ptok_attrs() {
+  GM_CUDA_TRY(cudaFuncSetAttribute(step_ptok_kernel<APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  GM_CUDA_TRY(cudaFuncSetAttribute(step_ptok_kernel<APPLY>, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
+  return GM_OK;
+}
+
+gm_status launch_step_ptok(const DevPool& P, const int32_t* slots, int32_t n, const int32_t* host_tokens,
+                           uint8_t* accepted, int32_t recycle, int32_t* bitmask, int64_t bstride, int32_t Wmax,
+                           void* logits, int32_t eb, uint32_t neg, int64_t vocab, int64_t lstride_bytes,
+                           cudaStream_t s) {
+  if (n <= 0) return GM_OK;
+  if (n > kParamTokens) return fail(GM_ERR_INVALID, "batch too large for parameter-passed token ids");
+  const size_t smem = fill_smem(split_words(Wmax, 1));
+  if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
+  TokParams tp;
+  std::memcpy(tp.v, host_tokens, (size_t)n * 4);
+  const StepArgs sa{nullptr, accepted, recycle};
+  const L2Window win{P.l2_base, P.l2_bytes, P.l2_hit};
+  uint32_t* bm = reinterpret_cast<uint32_t*>(bitmask);
+  if (logits) {
+    static gm_status attrs = ptok_attrs<true>();
+    if (attrs) return attrs;
+    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm,
+                             bstride, (const int32_t*)nullptr, split_words(Wmax, 1), static_cast<char*>(logits),
+                             lstride_bytes, vocab, (int)eb, neg, sa, tp));
+  } else {
+    static gm_status attrs = ptok_attrs<false>();
+    if (attrs) return attrs;
+    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<false>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm,
+                             bstride, (const int32_t*)nullptr, split_words(Wmax, 1), (char*)nullptr, (int64_t)0,
+                             (int64_t)0, 2, 0u, sa, tp));
+  }
   return GM_OK;
 }
 

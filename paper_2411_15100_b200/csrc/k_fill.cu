@@ -68,6 +68,44 @@ __device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_
   }
 }
 
+// Caller index of a top's parent frame within the callers of the top's
+// rule (selects the dependents' one-level context class; kRootCaller for a
+// top on the root frame, -1 if unknown) and, with two-level classes, the
+// grandparent frame's caller index.
+__device__ __forceinline__ void context_of(const DevPool& P, const SlotHdr& hd, const DevGrammar& G, int2 t, int& cj,
+                                           int& cj2) {
+  cj = kRootCaller;  // the root frame: nothing below it
+  cj2 = -1;
+  if (t.x < 0) return;
+  cj = -1;
+  const bool on_chain = hd.nchain > 0 && hd.chain_h[0] == t.x;
+  const unsigned long long pk = on_chain ? hd.chain_k[0] : arena_load(P.arena, t.x);
+  if (pk == kEmptyKey) return;
+  const int32_t pn = key_node(pk);
+  const int32_t* cr = G.callers + (size_t)G.node_rule[t.y] * kMaxCallers;
+  for (int j = 0; j < kRootCaller; ++j) {
+    const int32_t c = cr[j];
+    if (c < 0) break;
+    if (c == pn) { cj = j; break; }
+  }
+  if (cj < 0 || !G.ctx2) return;
+  const int32_t h2 = key_parent(pk);
+  if (h2 < 0) {
+    cj2 = kRootCaller;  // pn's frame is the bottom one
+    return;
+  }
+  const unsigned long long k2 =
+      (on_chain && hd.nchain > 1 && hd.chain_h[1] == h2) ? hd.chain_k[1] : arena_load(P.arena, h2);
+  if (k2 == kEmptyKey) return;
+  const int32_t pn2 = key_node(k2);
+  const int32_t* cr2 = G.callers + (size_t)G.node_rule[pn] * kMaxCallers;
+  for (int j = 0; j < kRootCaller; ++j) {
+    const int32_t c = cr2[j];
+    if (c < 0) break;
+    if (c == pn2) { cj2 = j; break; }
+  }
+}
+
 // Grid: (requests, splits).  A request's mask is cut into `splits` word
 // ranges (multiples of 4 words, i.e. 128 tokens) and each CTA owns one: it
 // merges only its slice of the rows, walks only the dependents whose token
@@ -329,6 +367,16 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     }
     s_nt = nt;
   }
+  // K5: the dependents' context indices from the new header, by warp 1 while
+  // thread 0 issues the row copies (one phase and one barrier fewer)
+  const bool early_ctx = do_acc && hd.ntops >= 0 && !terminated;
+  if (early_ctx && threadIdx.x >= 32 && (int)threadIdx.x < 32 + hd.ntops) {
+    const int st = threadIdx.x - 32;
+    int cj, cj2;
+    context_of(P, hd, Gs, hd.top[st], cj, cj2);
+    s_cj[st] = cj;
+    s_cj2[st] = cj2;
+  }
   for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) dep_acc[w] = 0u;
   if (threadIdx.x == 0) s_walked = 0;
   __syncthreads();
@@ -350,46 +398,15 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     const DevGrammar G = do_acc ? Gs : hint_ok ? blob_view(tables) : stage_blob(hd.blob, hd.blob_bytes, tables);
     // caller index of each top's parent frame within the callers of the
     // top's rule: selects the dependents' one-level context class
-    if ((int)threadIdx.x < nt) {
-      const int2 t = s_top[threadIdx.x];
-      int cj = kRootCaller;  // the root frame: nothing below it
-      int cj2 = -1;          // the grandparent frame's caller index (two-level classes)
-      if (t.x >= 0) {
-        cj = -1;
-        const bool on_chain = hd.nchain > 0 && hd.chain_h[0] == t.x;
-        const unsigned long long pk = on_chain ? hd.chain_k[0] : arena_load(P.arena, t.x);
-        if (pk != kEmptyKey) {
-          const int32_t pn = key_node(pk);
-          const int32_t* cr = G.callers + (size_t)G.node_rule[t.y] * kMaxCallers;
-          for (int j = 0; j < kRootCaller; ++j) {
-            const int32_t c = cr[j];
-            if (c < 0) break;
-            if (c == pn) { cj = j; break; }
-          }
-          if (cj >= 0 && G.ctx2) {
-            const int32_t h2 = key_parent(pk);
-            if (h2 < 0) {
-              cj2 = kRootCaller;  // pn's frame is the bottom one
-            } else {
-              const unsigned long long k2 =
-                  (on_chain && hd.nchain > 1 && hd.chain_h[1] == h2) ? hd.chain_k[1] : arena_load(P.arena, h2);
-              if (k2 != kEmptyKey) {
-                const int32_t pn2 = key_node(k2);
-                const int32_t* cr2 = G.callers + (size_t)G.node_rule[pn] * kMaxCallers;
-                for (int j = 0; j < kRootCaller; ++j) {
-                  const int32_t c = cr2[j];
-                  if (c < 0) break;
-                  if (c == pn2) { cj2 = j; break; }
-                }
-              }
-            }
-          }
-        }
+    if (!early_ctx) {
+      if ((int)threadIdx.x < nt) {
+        int cj, cj2;
+        context_of(P, hd, G, s_top[threadIdx.x], cj, cj2);
+        s_cj[threadIdx.x] = cj;
+        s_cj2[threadIdx.x] = cj2;
       }
-      s_cj[threadIdx.x] = cj;
-      s_cj2[threadIdx.x] = cj2;
+      __syncthreads();
     }
-    __syncthreads();
     trace_mark(P, 1, 4);
     if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ctx));
     const uint8_t* rec_base = reinterpret_cast<const uint8_t*>(hd.tokrec);  // records' byte offsets are into it

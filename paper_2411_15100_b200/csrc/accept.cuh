@@ -10,8 +10,14 @@ namespace gm {
 constexpr int kAccS = 32;
 constexpr int kAccF = 160;
 constexpr int kAccThreads = 32;
-constexpr int kAccR = 4;    // stacks held in registers by the fast walker
-constexpr int kAccRF = 48;  // its walker-local frames
+#ifndef GM_ACC_R
+#define GM_ACC_R 2
+#endif
+constexpr int kAccR = GM_ACC_R;  // stacks held in registers by the fast walker
+#ifndef GM_ACC_RF
+#define GM_ACC_RF 48
+#endif
+constexpr int kAccRF = GM_ACC_RF;  // its walker-local frames
 
 // Current (handle, node) set of a slot: from the header when it fits, else
 // from the ring.

@@ -32,8 +32,14 @@ constexpr int kFillThreads = 512;
 constexpr int kTmaRows = 4;     // tops whose rows are TMA-staged (more: direct loads)
 constexpr int kDepS = 16;
 constexpr int kDepF = 64;
-constexpr int kDepR = 4;    // register walker: stacks
-constexpr int kDepRF = 24;  // register walker: local frames
+#ifndef GM_DEP_R
+#define GM_DEP_R 1
+#endif
+constexpr int kDepR = GM_DEP_R;  // register walker: stacks
+#ifndef GM_DEP_RF
+#define GM_DEP_RF 24
+#endif
+constexpr int kDepRF = GM_DEP_RF;  // register walker: local frames
 #ifndef GM_PREFETCH_ROWS
 #define GM_PREFETCH_ROWS 0
 #endif

@@ -672,13 +672,13 @@ gm_status launch_step(const DevPool& P, const int32_t* slots, int32_t n, const i
   if (logits) {
     static gm_status attrs = fill_attrs<true, true>();
     if (attrs) return attrs;
-    GM_CUDA_TRY(launch_pdl_w(&win, fill_kernel<true, true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm, bstride,
+    GM_CUDA_TRY(launch_pdl_w(&win, fill_kernel<true, true>, dim3(n, 1), dim3(fill_threads(1)), smem, s, P, slots, n, bm, bstride,
                            rows, nullptr, split_words(Wmax, 1), static_cast<char*>(logits), lstride_bytes, vocab,
                            (int)eb, neg, sa));
   } else {
     static gm_status attrs = fill_attrs<false, true>();
     if (attrs) return attrs;
-    GM_CUDA_TRY(launch_pdl_w(&win, fill_kernel<false, true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm,
+    GM_CUDA_TRY(launch_pdl_w(&win, fill_kernel<false, true>, dim3(n, 1), dim3(fill_threads(1)), smem, s, P, slots, n, bm,
                            bstride, rows, nullptr, split_words(Wmax, 1), nullptr, (int64_t)0, (int64_t)0, 2, 0u, sa));
   }
   GM_LAUNCH_CHECK();
@@ -709,13 +709,13 @@ gm_status launch_step_ptok(const DevPool& P, const int32_t* slots, int32_t n, co
   if (logits) {
     static gm_status attrs = ptok_attrs<true>();
     if (attrs) return attrs;
-    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<true>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm,
+    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<true>, dim3(n, 1), dim3(fill_threads(1)), smem, s, P, slots, n, bm,
                              bstride, (const int32_t*)nullptr, split_words(Wmax, 1), static_cast<char*>(logits),
                              lstride_bytes, vocab, (int)eb, neg, sa, tp));
   } else {
     static gm_status attrs = ptok_attrs<false>();
     if (attrs) return attrs;
-    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<false>, dim3(n, 1), dim3(kFillThreads), smem, s, P, slots, n, bm,
+    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<false>, dim3(n, 1), dim3(fill_threads(1)), smem, s, P, slots, n, bm,
                              bstride, (const int32_t*)nullptr, split_words(Wmax, 1), (char*)nullptr, (int64_t)0,
                              (int64_t)0, 2, 0u, sa, tp));
   }

@@ -830,9 +830,10 @@ def main():
                                             "replay)") if traffic else None,
                          "algorithmic_bytes_per_launch": algo_bytes},
             "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": B,
-                    "path": "DecodeLoop.step per decode step (native gm_decoder_step: host token ids -> pinned "
-                            "staging -> H2D on a copy stream -> K5 -> accepted flags D2H, event-ordered), K steps back "
-                            "to back in one bracket; the host reads every step's flags",
+                    "path": "DecodeLoop.step per decode step (native gm_decoder_step: host token ids passed to K5 "
+                            "by value in the launch parameters (the step's H2D), K5, accepted flags D2H on an output "
+                            "copy stream, event-ordered), K steps back to back in one bracket; the host reads every "
+                            "step's flags",
                     "host_issue_us_per_step": r["e2e_host_us"],
                     "mask_mismatches_latency_pass": r["e2e_mask_mismatches"]},
             "gpu_launches": args.steps,

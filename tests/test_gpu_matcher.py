@@ -513,10 +513,12 @@ def test_decode_step_graph_queued_back_to_back():
     pool.check()
 
 
-def test_decode_loop_native_equals_eager():
-    """DecodeLoop (native gm_decoder_*: host ids -> H2D -> K5 -> D2H, steps
-    queued back to back over 3 reused buffers) == eager batch_step: same
-    accepted flags and masks at every step."""
+@pytest.mark.parametrize("copy_path", [False, True])
+def test_decode_loop_native_equals_eager(copy_path, monkeypatch):
+    """DecodeLoop (native gm_decoder_*: host ids -> K5 (ids in the launch
+    parameters, or pinned staging + H2D copy with GMASK_DECODER_COPY=1) ->
+    accepted flags D2H, steps queued back to back over 3 reused buffers) ==
+    eager batch_step: same accepted flags and masks at every step."""
     import numpy as np
     import torch
 
@@ -551,6 +553,7 @@ def test_decode_loop_native_equals_eager():
     new = [gm.GrammarMatcher(compiled) for _ in range(B)]
     bms = [torch.empty((B, W), dtype=torch.int32, device="cuda") for _ in range(n_buf)]
     bufs = [torch.zeros(B, vocab.size, device="cuda", dtype=torch.bfloat16) for _ in range(n_buf)]
+    monkeypatch.setenv("GMASK_DECODER_COPY", "1" if copy_path else "0")
     loop = DecodeLoop(new, bms, bufs, recycle=True)
     out = np.zeros(B, dtype=np.uint8)
 

@@ -397,6 +397,40 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     k5_mask_mism = int((masks_t != masks_all).any(dim=2).sum())
     k5_all_acc = bool(acc_t[:S - 1].bool().all())
 
+    # diagnostic pass (--diag-k5k0): K5 without logits (accept + fill, bitmask
+    # out) then K0 apply, two launches per step
+    if args.diag_k5k0:
+        def k5k0(s):
+            batch_step(pool, slots, tok_dev[s - 1] if s > 0 else None, acc_t[s - 1] if s > 0 else None, masks_t[s],
+                       None, recycle=True)
+            gm.apply_token_bitmask_inplace(ring[s % n_ring], masks_t[s])
+
+        for m in matchers:
+            m.reset()
+        for s in range(W0):
+            k5k0(s)
+        torch.cuda.synchronize()
+        gd_w, gd_t = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gd_w, stream=cap_stream):
+            for s in range(W0):
+                k5k0(s)
+        with torch.cuda.graph(gd_t, stream=cap_stream):
+            for s in range(W0, S):
+                k5k0(s)
+        reps = []
+        for rep in range(args.repeats):
+            for m in matchers:
+                m.reset()
+            gd_w.replay()
+            sync_ranks()
+            t_ev[0].record(stream)
+            gd_t.replay()
+            t_ev[1].record(stream)
+            torch.cuda.synchronize()
+            reps.append(t_ev[0].elapsed_time(t_ev[1]) / (S - W0))
+        mism = int((masks_t != masks_all).any(dim=2).sum())
+        print(f"diag k5k0: {statistics.median(reps) * 1e3:.2f} us/step, mask mismatches {mism}", file=sys.stderr)
+
     # diagnostic pass (--diag-k4k3): the same steps as K4 accept -> recycle ->
     # K3 fill + apply (three launches per step, PDL), back to back in a graph
     k4k3_ms = None
@@ -750,6 +784,7 @@ def main():
     ap.add_argument("--grammar", default="json", choices=sorted(WORKLOADS),
                     help="SURVEY §8d workload: json = config 3 (default, the headline)")
     ap.add_argument("--diag-k4k3", action="store_true", help="diagnostic: time K4 + recycle + K3 per step")
+    ap.add_argument("--diag-k5k0", action="store_true", help="diagnostic: time K5 (no logits) + K0 per step")
     ap.add_argument("--repeats", type=int, default=7, help="K-step brackets of the value pass (median)")
     ap.add_argument("--cpu-steps", type=int, default=24)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)

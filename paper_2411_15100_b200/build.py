@@ -61,6 +61,8 @@ def build(force: bool = False, verbose: bool = False, out: Path = None) -> Path:
     nvcc = _nvcc()
     BUILD.mkdir(exist_ok=True)
     include = ["-I", str(ROOT / "include"), "-I", str(CSRC)]
+    if os.environ.get("GMASK_TIMELINE") == "1":  # diagnostics build: per-CTA timeline + CTA-0 phase marks
+        include += ["-DGM_TIMELINE", "-DGM_TRACE_MARKS"]
     if os.environ.get("GMASK_PROBES") == "1":  # debug: K5 dry-walk / load-latency probes (GMASK_TRACE=1)
         include += ["-DGM_TRACE_PROBES"]
     if os.environ.get("GMASK_VERIFY") == "1":  # debug: cross-check cached arena keys

@@ -766,12 +766,20 @@ struct DevPool {
 };
 
 // Phase timestamps of CTA 0 (diagnostics only): trace[kernel*16 + phase].
+// Compiled in only with -DGM_TRACE_MARKS: even untaken, the calls sit in
+// every thread's path and ncu attributed ~13 % of K5's warp samples
+// (branch resolution) to them; the per-CTA timeline (GMASK_TRACE=1)
+// supersedes them.
 __device__ __forceinline__ void trace_mark(const DevPool& P, int kernel, int phase) {
+#ifdef GM_TRACE_MARKS
   if (P.trace && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     P.trace[kernel * 16 + phase] = t;
   }
+#else
+  (void)P; (void)kernel; (void)phase;
+#endif
 }
 
 __device__ __forceinline__ int2* slot_tops(const DevPool& P, int32_t slot, int32_t h) {

@@ -44,6 +44,13 @@ constexpr int kDepRF = GM_DEP_RF;  // register walker: local frames
 #define GM_PREFETCH_ROWS 0
 #endif
 constexpr bool kPrefetchRows = GM_PREFETCH_ROWS;  // K5: issue row TMAs from the accept walk
+// per-CTA timeline stamps (GMASK_TRACE=1 at run time) exist only in builds
+// with -DGM_TIMELINE (tools/trace.sh): the untaken branches cost ~0.2 us/step
+#ifdef GM_TIMELINE
+constexpr bool kTimeline = true;
+#else
+constexpr bool kTimeline = false;
+#endif
 
 // K3 tail: mask one logits row in place from the finished mask words in
 // shared memory (coalesced 16-byte chunks, -inf only where masked, logits
@@ -170,7 +177,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   trace_mark(P, 1, 0);
   unsigned long long t_start = 0, t_hdr = 0, t_setup = 0, t_ctx = 0, t_walks = 0, t_walk = 0, walk_info = 0;
   unsigned long long acc_ts[2] = {0, 0};  // accept: frames interned, header state built
-  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int32_t slot = __ldg(slots + i);
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   __shared__ RingPos rp;
@@ -197,7 +204,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
                        hd.tokrec == P.hint_tokrec && hd.V == P.hint_V;
   if (hinted) mbar_wait(&blob_bar, 0);
   trace_mark(P, 1, 1);
-  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_hdr));
+  if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_hdr));
   DevGrammar Gs{};
   unsigned long long t_acc = 0;
   const bool vec = (!bitmask || (reinterpret_cast<uintptr_t>(bitmask + row * bstride) & 15) == 0) && (hd.W % 4 == 0);
@@ -210,7 +217,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
       if (threadIdx.x < 2 && in_range) s_rec[threadIdx.x] = __ldg(hd.tokrec + 2 * (size_t)tok + threadIdx.x);
       Gs = stage_blob(hd.blob, hd.blob_bytes, tables);  // barrier inside
     }
-    if (P.trace && i == 0 && threadIdx.x == 0) {
+    if (kTimeline && P.trace && i == 0 && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       P.trace[49] = t;
@@ -225,7 +232,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
         const int4 e = s_rec[0], inl = s_rec[1];
         const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;
 #ifdef GM_TRACE_PROBES
-        if (P.trace && i == 0 && hd.ntops > 0) {  // diagnostic: dry walk of the same token, timed
+        if (kTimeline && P.trace && i == 0 && hd.ntops > 0) {  // diagnostic: dry walk of the same token, timed
           unsigned long long t0, t1;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
           auto clk = []() { long long t; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) :: "memory"); return t; };
@@ -280,7 +287,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
         // the interning and the header publish
         s_pref = -1;
         auto prefetch_rows = [&](const auto& rw) {
-          if (P.trace) {
+          if (kTimeline && P.trace) {
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_walk));
             walk_info = (unsigned long long)e.y | ((unsigned long long)rw.n << 16) | ((unsigned long long)rw.nf << 24);
           }
@@ -308,7 +315,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
           s_pref = nr;
         };
         acc = accept_one(P, slot, rp, hd, Gs, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
-                         tok == hd.eos, e.x != 0, &hd, prefetch_rows, P.trace ? acc_ts : nullptr);
+                         tok == hd.eos, e.x != 0, &hd, prefetch_rows, (kTimeline && P.trace) ? acc_ts : nullptr);
         if (!acc && s_pref >= 0) s_pref = -2;  // walked but not committed: state unchanged, rows stale
       }
       SA.accepted[i] = (uint8_t)acc;
@@ -316,8 +323,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
       const bool restart = SA.recycle && (hd.flags & 1);
       if (restart) restart_slot(P, slot, Gs, &hd);
       s_dirty = acc || restart;
-      if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_acc));
-      if (P.trace && i == 0) P.trace[48] = t_acc;
+      if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_acc));
+      if (kTimeline && P.trace && i == 0) P.trace[48] = t_acc;
     }
     __syncthreads();
     // publish the new header state (one 16-byte store per lane of warp 0)
@@ -387,7 +394,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   if (threadIdx.x == 0) s_walked = 0;
   __syncthreads();
   trace_mark(P, 1, 2);
-  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
+  if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
   const int nt = s_nt;
   const bool tma = pref >= 0 || (vec && hd.ntops >= 0 && nt <= kTmaRows && nw > 0 && !terminated && pref == -1);
   if (pref == -2) mbar_wait(&rows_bar, 0);  // drain the stale prefetch before leaving
@@ -395,7 +402,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   trace_mark(P, 1, 3);
   int total = 0;
   for (int s = 0; s < nt; ++s) total += s_hi[s] - s_lo[s];
-  if (P.trace && i == 0 && split == 0 && threadIdx.x == 0) {
+  if (kTimeline && P.trace && i == 0 && split == 0 && threadIdx.x == 0) {
     P.trace[16 + 8] = (unsigned long long)total;
     P.trace[16 + 9] = (unsigned long long)(nt > 0 ? s_key[0] : -1);
     P.trace[16 + 10] = (unsigned long long)nt;
@@ -414,7 +421,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
       __syncthreads();
     }
     trace_mark(P, 1, 4);
-    if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ctx));
+    if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ctx));
     const uint8_t* rec_base = reinterpret_cast<const uint8_t*>(hd.tokrec);  // records' byte offsets are into it
     const int32_t tok_lo = w_lo * 32, tok_hi = w_hi * 32;
     // warp-major assignment: consecutive dependents go to different warps, so
@@ -444,7 +451,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
           continue;
         }
       }
-      if (P.trace) atomicAdd(&s_walked, 1 | (e.y << 16));  // diagnostics: walks, bytes walked
+      if (kTimeline && P.trace) atomicAdd(&s_walked, 1 | (e.y << 16));  // diagnostics: walks, bytes walked
       const int4 inl = __ldg(rec + 1);
       const int2 t = s_top[s];
       const uint8_t* far = rec_base + e.z;  // bytes beyond the inline 16
@@ -479,7 +486,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   trace_mark(P, 1, 5);
   __syncthreads();
   trace_mark(P, 1, 6);
-  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_walks));
+  if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_walks));
 
   // Merge and store this CTA's words.
   uint32_t* out = bitmask ? bitmask + row * bstride : nullptr;
@@ -527,7 +534,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   }
   trace_mark(P, 1, 7);
   unsigned long long t_merge = 0;
-  if (P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_merge));
+  if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_merge));
   if (need_apply || APPLY) {
     if (partial) s_partial = 1;
     __syncthreads();
@@ -538,7 +545,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     const int64_t t_lo = (int64_t)w_lo * 32, t_hi = (int64_t)w_hi * 32 < vocab ? (int64_t)w_hi * 32 : vocab;
     if (t_hi > t_lo) apply_row(logits + row * lstride_bytes, dep_acc, t_lo, t_hi, ap_eb, ap_neg);
   }
-  if (P.trace && threadIdx.x == 0) {
+  if (kTimeline && P.trace && threadIdx.x == 0) {
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     const int64_t c = (int64_t)i * n_split + split;

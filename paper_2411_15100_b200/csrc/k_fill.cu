@@ -64,13 +64,15 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
   // words[] holds the mask from token tok_lo (a multiple of 128) on
   constexpr int vec = 16 / EB;
   constexpr uint32_t full = (1u << vec) - 1u;
-  const int64_t chunks = (tok_hi - tok_lo + vec - 1) / vec;
-  for (int64_t c = threadIdx.x; c < chunks; c += blockDim.x) {
-    const int64_t t0 = c * vec;  // relative to tok_lo
+  const int32_t lim = (int32_t)(tok_hi - tok_lo);  // tokens of this span (< 2^31)
+  const int32_t chunks = (lim + vec - 1) / vec;
+  char* base = rowp + tok_lo * EB;
+  for (int32_t c = threadIdx.x; c < chunks; c += blockDim.x) {
+    const int32_t t0 = c * vec;  // relative to tok_lo
     uint32_t keep = (words[t0 >> 5] >> (t0 & 31)) & full;
-    if (tok_lo + t0 + vec > tok_hi) keep |= full & ~((1u << (tok_hi - tok_lo - t0)) - 1u);
+    if (t0 + vec > lim) keep |= full & ~((1u << (lim - t0)) - 1u);
     if (keep == full) continue;
-    char* p = rowp + (tok_lo + t0) * EB;
+    char* p = base + t0 * EB;
     if (keep == 0) {
       st_cs_v4(p, neg);
     } else {

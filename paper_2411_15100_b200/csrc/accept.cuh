@@ -124,7 +124,7 @@ struct NoWalkHook {
 template <class ByteFn, class OnWalk = NoWalkHook>
 __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr, const DevGrammar& G,
                           int64_t len, ByteFn byte, bool is_eos, bool reject_token, SlotHdr* mirror = nullptr,
-                          OnWalk on_walk = OnWalk(), unsigned long long* ts = nullptr) {
+                          OnWalk on_walk = OnWalk(), unsigned long long* ts = nullptr, SpecOut* spec = nullptr) {
   if (hdr.flags & 1) {  // REF matcher.py:276-277 "matcher is terminated"
     atomicOr(P.err, kErrTerminated);
     return 0;
@@ -158,7 +158,7 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
       on_walk(rw);
       int2 out[kAccR];
       if (mirror) {  // fused step kernel: chain rewritten in place in the shared header
-        const int nout = rwalker_commit_inplace(rw, P.arena, out, *mirror);
+        const int nout = rwalker_commit_inplace(rw, P.arena, out, *mirror, spec);
         if (nout < 0) {
           atomicOr(P.err, kErrArena);
           return 0;

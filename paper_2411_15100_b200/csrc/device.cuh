@@ -867,8 +867,23 @@ __device__ inline void header_state(const DevPool& P, SlotHdr& h, const DevGramm
 // chain, w.xh/w.xk == h.chain_h/h.chain_k): the surviving part of the old
 // chain is shifted in place and the fresh frames written in front — no
 // walker-local Chain copy (16 local-memory round trips per accept).
+// Deferred interning (fused step kernel, single surviving stack): a fresh
+// frame's handle is its key's hash slot unless a different key sits there,
+// so the commit uses the slots as handles at once and leaves the CASes to
+// another warp, whose results are checked only at the end of the kernel
+// (spec_fixup re-interns and rewrites the published state on the rare
+// collision).  The step's mask never depends on fresh handle values: fresh
+// frames sit in the header's ancestor chain and are walked by position.
+constexpr int kSpecMax = 8;
+struct SpecOut {
+  int n;                             // fresh frames awaiting their CAS (0: committed synchronously)
+  int32_t slot[kSpecMax];            // speculative handle = hash slot, push order (parents first)
+  unsigned long long key[kSpecMax];  // keys, parents as speculative handles
+};
+
 template <int R, int F>
-__device__ inline int rwalker_commit_inplace(RWalker<R, F>& w, const DevArena& A, int2* out, SlotHdr& h) {
+__device__ inline int rwalker_commit_inplace(RWalker<R, F>& w, const DevArena& A, int2* out, SlotHdr& h,
+                                             SpecOut* spec = nullptr) {
   // scratch in shared memory: one committing thread per CTA (the accept
   // thread); local-memory arrays here cost an L2 round trip per access
   __shared__ int32_t gmap[F];
@@ -895,8 +910,25 @@ __device__ inline int rwalker_commit_inplace(RWalker<R, F>& w, const DevArena& A
     gmap[q] = (int32_t)(mix64(keyq[q]) & A.mask);
   }
   bool redo = false;
+  bool deferred = false;
+  if (spec) {  // single stack, <= kSpecMax fresh frames on pairwise distinct slots: defer the CASes
+    spec->n = 0;
+    if (w.n == 1) {
+      int k = 0;
+      deferred = true;
+      for (int q = 0; q < w.nf && deferred; ++q) {
+        if (gmap[q] < 0) continue;
+        if (k == kSpecMax) { deferred = false; break; }
+        for (int j = 0; j < k; ++j) deferred &= spec->slot[j] != gmap[q];
+        spec->slot[k] = gmap[q];
+        spec->key[k] = keyq[q];
+        ++k;
+      }
+      if (deferred) spec->n = k;
+    }
+  }
   constexpr int kBatch = 8;
-  for (int q0 = 0; q0 < w.nf; q0 += kBatch) {
+  for (int q0 = 0; q0 < w.nf && !deferred; q0 += kBatch) {
     unsigned long long res[kBatch];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
@@ -1018,6 +1050,38 @@ __device__ inline void store_header_state(const DevPool& P, int32_t slot, const 
   int4* dst = reinterpret_cast<int4*>(P.hdr + slot);
 #pragma unroll
   for (int i = kHdrStateVec; i < kHdrVec; ++i) dst[i] = src[i];
+}
+
+// Collision repair of a deferred commit (rare): re-intern the fresh frames in
+// push order with their parents' real handles, then rewrite the shared
+// header's chain and first top and republish it and the ring entry.
+__device__ inline void spec_fixup(const DevPool& P, int32_t slot, const SpecOut& sp, SlotHdr& h) {
+  int32_t real[kSpecMax];
+  unsigned long long rkey[kSpecMax];
+  for (int k = 0; k < sp.n; ++k) {
+    int32_t ph = key_parent(sp.key[k]);
+    for (int j = 0; j < k; ++j)
+      if (sp.slot[j] == ph) { ph = real[j]; break; }
+    rkey[k] = arena_key(ph, key_node(sp.key[k]), key_term(sp.key[k]));
+    real[k] = arena_probe(P.arena, rkey[k], mix64(rkey[k]));
+    if (real[k] < 0) { atomicOr(P.err, kErrArena); return; }
+  }
+  auto fix = [&](int32_t& hh, unsigned long long* kk) {
+    for (int j = 0; j < sp.n; ++j)
+      if (sp.slot[j] == hh) { hh = real[j]; if (kk) *kk = rkey[j]; return; }
+  };
+  for (int i = 0; i < h.nchain; ++i) fix(h.chain_h[i], &h.chain_k[i]);
+  const int nt = h.ntops < 0 ? 0 : h.ntops;
+  for (int s = 0; s < nt; ++s) fix(h.top[s].x, nullptr);
+  const int32_t head = P.head[slot];
+  int2* ring = slot_tops(P, slot, head);
+  const int nr = P.meta[(size_t)slot * P.H + head] & 0xFFFF;
+  for (int s = 0; s < nr; ++s) {
+    int32_t x = ring[s].x;
+    fix(x, nullptr);
+    ring[s].x = x;
+  }
+  store_header_state(P, slot, h);
 }
 
 // Rebuild a slot header from the binding (reset / recycle / rollback path).

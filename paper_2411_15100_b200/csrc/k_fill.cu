@@ -44,6 +44,11 @@ constexpr int kDepRF = GM_DEP_RF;  // register walker: local frames
 #define GM_PREFETCH_ROWS 0
 #endif
 constexpr bool kPrefetchRows = GM_PREFETCH_ROWS;  // K5: issue row TMAs from the accept walk
+#ifdef GM_NO_DEFER_INTERN
+constexpr bool kDeferIntern = false;
+#else
+constexpr bool kDeferIntern = true;  // K5: fresh frames' CASes by warp 2, verified at the end
+#endif
 // per-CTA timeline stamps (GMASK_TRACE=1 at run time) exist only in builds
 // with -DGM_TIMELINE (tools/trace.sh): the untaken branches cost ~0.2 us/step
 #ifdef GM_TIMELINE
@@ -194,7 +199,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   __shared__ RingPos rp;
   __shared__ int4 s_rec[2];
-  __shared__ int s_just_term, s_dirty, s_walked;
+  __shared__ int s_just_term, s_dirty, s_walked, s_spec_bad;
+  __shared__ SpecOut s_spec;  // K5: fresh frames whose interning is deferred (warp 2, checked at the end)
   int32_t tok = -1;
   const bool do_acc = ACCEPT && (SA.tokens || ptok);
   if (do_acc) {
@@ -237,6 +243,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     }
     if (threadIdx.x == 0) {
       int acc = 0;
+      s_spec.n = 0;
       const bool was_term = hd.flags & 1;
       if (!in_range) {  // REF matcher.py:278-279
         atomicOr(P.err, kErrInvalid);
@@ -327,7 +334,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
           s_pref = nr;
         };
         acc = accept_one(P, slot, rp, hd, Gs, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
-                         tok == hd.eos, e.x != 0, &hd, prefetch_rows, (kTimeline && P.trace) ? acc_ts : nullptr);
+                         tok == hd.eos, e.x != 0, &hd, prefetch_rows, (kTimeline && P.trace) ? acc_ts : nullptr,
+                         kDeferIntern ? &s_spec : nullptr);
         if (!acc && s_pref >= 0) s_pref = -2;  // walked but not committed: state unchanged, rows stale
       }
       SA.accepted[i] = (uint8_t)acc;
@@ -342,6 +350,13 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     // publish the new header state (one 16-byte store per lane of warp 0)
     if (s_dirty && threadIdx.x < 32) store_header_state_warp(P, slot, hd, threadIdx.x);
   }
+  // deferred interning: warp 2 issues the fresh frames' CASes now and checks
+  // their results only at the end of the kernel
+  unsigned long long spec_old = kEmptyKey;
+  const int spec_lane = (int)threadIdx.x - 64;
+  const bool spec_mine = do_acc && spec_lane >= 0 && spec_lane < s_spec.n;
+  if (spec_mine)
+    spec_old = atomicCAS(P.arena.keys + s_spec.slot[spec_lane], kEmptyKey, s_spec.key[spec_lane]);
   const int32_t W = hd.W;
   const int32_t per = ((W + 3) / 4 + n_split - 1) / n_split * 4;  // words per split
   const int32_t w_lo = min(W, split * per), w_hi = min(W, w_lo + per), nw = w_hi - w_lo;
@@ -556,6 +571,10 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     const int64_t vocab = ap_vocab < (int64_t)W * 32 ? ap_vocab : (int64_t)W * 32;
     const int64_t t_lo = (int64_t)w_lo * 32, t_hi = (int64_t)w_hi * 32 < vocab ? (int64_t)w_hi * 32 : vocab;
     if (t_hi > t_lo) apply_row(logits + row * lstride_bytes, dep_acc, t_lo, t_hi, ap_eb, ap_neg);
+  }
+  if (do_acc && threadIdx.x >= 64 && threadIdx.x < 96 && s_spec.n > 0) {  // warp 2: verify the deferred commit
+    const bool bad = spec_mine && spec_old != kEmptyKey && spec_old != s_spec.key[spec_lane];
+    if (__any_sync(0xFFFFFFFFu, bad) && threadIdx.x == 64) spec_fixup(P, slot, s_spec, hd);
   }
   if (kTimeline && P.trace && threadIdx.x == 0) {
     unsigned long long t1;

@@ -572,3 +572,20 @@ def test_decode_loop_native_equals_eager(copy_path, monkeypatch):
         check(s)
     loop.close()
     pool.check()
+
+
+@pytest.mark.parametrize("grammar", ["json", "arithmetic"])
+def test_k5_small_arena_collisions(grammar):
+    """K5 with a 1,024-slot arena (hash-slot collisions frequent: exercises the
+    deferred interning's end-of-kernel repair) stays bit-exact with the oracle
+    over 60 steps of 16 requests."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, GMASK_ARENA_LOG2="10")
+    res = subprocess.run([sys.executable, os.path.join(here, "_small_arena_k5.py"), grammar], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    assert "ok" in res.stdout

@@ -362,7 +362,11 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   const int32_t w_lo = min(W, split * per), w_hi = min(W, w_lo + per), nw = w_hi - w_lo;
   const bool terminated = hd.flags & 1;
   const int pref = do_acc ? s_pref : -1;
-  if (threadIdx.x == 0) {
+  // the setup runs on warp 3's lane 0: its mbarrier init fences (MEMBAR)
+  // would otherwise wait for the header/ring stores thread 0 just issued
+  // (warp 1 computes contexts, warp 2 carries the deferred CASes)
+  const unsigned setup_thread = blockDim.x > 96 ? 96u : 0u;
+  if (threadIdx.x == setup_thread) {
     s_partial = 0;
     int nt = hd.ntops;
     if (terminated) {  // a request that terminated in this very step gets an empty row, no error

@@ -473,11 +473,10 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
   const size_t total = o_ctx2 + (size_t)dep_total * kMaxCallers * 4 + 4;
   uint8_t* buf2;
   if ((st = c->mem.alloc(&buf2, total))) return bail(st);
-  // two-level context classes: opt-in (GMASK_TWO_LEVEL=1).  They cut the
-  // median request's dependent walks ~4x on JSON, but the extra context
-  // lookup sits on every request's critical path and the slowest request
-  // (which sets the step time) is bound by its accept: measured 0.2 us/step
-  // slower on the JSON bench, equal on XML
+  // two-level context classes: opt-in (GMASK_TWO_LEVEL=1).  The median
+  // request walks ~4x fewer dependents on JSON (0.1 us/step faster), but
+  // XML-like keys with 10^4 dependents pay an extra load each (+4.6 us/step)
+  // and the precompute costs up to 100 ms per schema (config 5)
   const char* tl = getenv("GMASK_TWO_LEVEL");
   const bool two_level = tl && tl[0] == '1';
   uint32_t* ctx2 = two_level ? reinterpret_cast<uint32_t*>(buf2 + o_ctx2) : nullptr;

@@ -465,8 +465,11 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
         base += s_hi[s] - s_lo[s];
         ++s;
       }
-      const int4* rec = hd.dep_ent + 2 * (size_t)(s_lo[s] + (q - base));
+      const int32_t di = s_lo[s] + (q - base);
+      const int4* rec = hd.dep_ent + 2 * (size_t)di;
       const int4 e = __ldg(rec);
+      // two-level class word fetched alongside the record (not after it)
+      const uint32_t c2w = s_cj2[s] >= 0 ? __ldg(G.ctx2 + (size_t)di * kMaxCallers + s_cj[s]) : 0u;
       const int32_t tid = e.x;
       if (tid < tok_lo || tid >= tok_hi) continue;  // another split's token
       uint32_t* acc_w = dep_acc + ((tid >> 5) - w_lo);
@@ -475,7 +478,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
       if (s_cj[s] >= 0) {
         uint32_t cls = ((uint32_t)e.w >> (2 * s_cj[s])) & 3u;
         if (cls == kCtxDeeper && s_cj2[s] >= 0)  // two-level class from the grandparent frame
-          cls = (__ldg(G.ctx2 + (size_t)(s_lo[s] + (q - base)) * kMaxCallers + s_cj[s]) >> (2 * s_cj2[s])) & 3u;
+          cls = (c2w >> (2 * s_cj2[s])) & 3u;
         if (cls == kCtxReject) continue;
         if (cls == kCtxAccept) {
           atomicOr(acc_w, bit);

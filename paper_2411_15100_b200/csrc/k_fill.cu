@@ -459,15 +459,29 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     // a handful of walks run in parallel instead of diverging inside one warp
     const int32_t n_warps = blockDim.x >> 5;
     const int32_t q0 = (threadIdx.x & 31) * n_warps + (threadIdx.x >> 5);
-    for (int32_t q = q0; q < total; q += blockDim.x) {
-      int s = 0, base = 0;
+    // the next record is loaded before this one is resolved (the loop is
+    // latency-bound for keys with thousands of dependents)
+    auto locate = [&](int32_t q, int& s) -> int32_t {  // top of dependent q, its record index
+      int base = 0;
+      s = 0;
       while (q - base >= s_hi[s] - s_lo[s]) {
         base += s_hi[s] - s_lo[s];
         ++s;
       }
-      const int32_t di = s_lo[s] + (q - base);
+      return s_lo[s] + (q - base);
+    };
+    int s_next = 0;
+    int32_t di_next = q0 < total ? locate(q0, s_next) : 0;
+    int4 e_next = q0 < total ? __ldg(hd.dep_ent + 2 * (size_t)di_next) : make_int4(0, 0, 0, 0);
+    for (int32_t q = q0; q < total; q += blockDim.x) {
+      const int s = s_next;
+      const int32_t di = di_next;
+      const int4 e = e_next;
+      if (q + (int32_t)blockDim.x < total) {
+        di_next = locate(q + blockDim.x, s_next);
+        e_next = __ldg(hd.dep_ent + 2 * (size_t)di_next);
+      }
       const int4* rec = hd.dep_ent + 2 * (size_t)di;
-      const int4 e = __ldg(rec);
       // two-level class word fetched alongside the record (not after it)
       const uint32_t c2w = s_cj2[s] >= 0 ? __ldg(G.ctx2 + (size_t)di * kMaxCallers + s_cj[s]) : 0u;
       const int32_t tid = e.x;

@@ -142,6 +142,7 @@ typedef struct gm_fe_options {
   int32_t max_dfa_states;           /* 200000                                */
   int32_t max_follow_states;        /* 4096                                  */
   int32_t state_cap;                /* 4096 (REF pda.py:53)                  */
+  int32_t inline_calls;             /* 1: also inline single-caller rules    */
 } gm_fe_options;
 
 typedef struct gm_fe_tables {

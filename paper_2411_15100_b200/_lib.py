@@ -63,7 +63,7 @@ class gm_grammar_tables(C.Structure):
 class gm_fe_options(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("determinize", "inline_rules", "ctx_expansion", "inline_max_rule_states",
                                           "inline_max_result_states", "max_dfa_states", "max_follow_states",
-                                          "state_cap")]
+                                          "state_cap", "inline_calls")]
 
 
 class gm_fe_tables(C.Structure):

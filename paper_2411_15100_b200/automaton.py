@@ -48,6 +48,11 @@ class AutomatonOptions:
     ctx_expansion: bool = True    # ≙ CompileOptions.ctx_expansion
     inline_max_rule_states: int = 32
     inline_max_result_states: int = 1024
+    # also inline a rule that calls other rules when exactly one live rule
+    # calls it (no code duplication): collapses call chains such as JSON's
+    # element -> value -> object -> members -> member into one rule, and
+    # removes the repetition ambiguity of `item*` with `item ::= ... | text+`
+    inline_calls: bool = True
     max_dfa_states: int = 200_000
     max_follow_states: int = 4096
     state_cap: int = DEFAULT_STATE_CAP
@@ -316,6 +321,8 @@ def _inline_into(host: _Dfa, callees: Dict[int, _Dfa]) -> _Nfa:
             for q in range(sub.size):
                 for c, v in sub.trans[q].items():
                     a.byte[off + q].append((1 << c, off + v))
+                for r2, v in sub.calls[q].items():
+                    a.call[off + q].append((r2, off + v))
                 if sub.finals[q]:
                     a.eps[off + q].append(t)
             a.eps[s].append(off + sub.start)
@@ -388,6 +395,24 @@ def build_tables(g: ParsedGrammar, opts: Optional[AutomatonOptions] = None) -> C
                 for r, d in dfas.items()
                 if not any(d.calls[s] for s in range(d.size)) and d.size <= opts.inline_max_rule_states
             }
+            if opts.inline_calls:
+                # live callers per rule (the root counts as called from outside)
+                callers: Dict[int, set] = {r: set() for r in dfas}
+                seen, work = {root}, [root]
+                while work:
+                    h = work.pop()
+                    for s_ in range(dfas[h].size):
+                        for r in dfas[h].calls[s_]:
+                            callers[r].add(h)
+                            if r not in seen:
+                                seen.add(r)
+                                work.append(r)
+                for r in sorted(seen):
+                    d = dfas[r]
+                    if r in inlinable or r == root or len(callers[r]) != 1 or r in callers[r]:
+                        continue
+                    if d.size <= opts.inline_max_result_states:
+                        inlinable[r] = d
             changed = False
             for host in list(dfas):
                 hd = dfas[host]
@@ -677,7 +702,7 @@ def build_tables_native(g: ParsedGrammar, opts: Optional[AutomatonOptions] = Non
     ir = np.ascontiguousarray(ir)
     fo = _lib.gm_fe_options(1, int(opts.inline), int(opts.ctx_expansion), opts.inline_max_rule_states,
                             opts.inline_max_result_states, opts.max_dfa_states, opts.max_follow_states,
-                            opts.state_cap)
+                            opts.state_cap, int(opts.inline_calls))
     view = _lib.gm_fe_tables()
     h = C.c_void_p()
     lib = _lib.load()

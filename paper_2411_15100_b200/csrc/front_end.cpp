@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
@@ -370,6 +371,7 @@ Nfa inline_into(const Dfa& host, const std::map<int, const Dfa*>& callees) {
           b.set(te.first);
           a.byte[off + q].push_back({b, off + te.second});
         }
+        for (auto& ce : sub.calls[q]) a.call[off + q].push_back({ce.first, off + ce.second});
         if (sub.finals[q]) a.eps[off + q].push_back(e.second);
       }
       a.eps[s].push_back(off + sub.start);
@@ -468,6 +470,29 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
           inl[r] = 1;
           snap[r] = dfas[r];
         }
+      if (o.inline_calls) {
+        // single-live-caller rules with calls (automaton.py build_tables)
+        std::vector<std::set<int>> callers(n_rules_in);
+        std::vector<char> seen(n_rules_in, 0);
+        std::vector<int> work{root_in};
+        seen[root_in] = 1;
+        while (!work.empty()) {
+          const int h = work.back();
+          work.pop_back();
+          for (auto& cs : dfas[h].calls)
+            for (auto& e : cs) {
+              callers[e.first].insert(h);
+              if (!seen[e.first]) { seen[e.first] = 1; work.push_back(e.first); }
+            }
+        }
+        for (int r = 0; r < n_rules_in; ++r) {
+          if (!seen[r] || inl[r] || r == root_in || callers[r].size() != 1 || callers[r].count(r)) continue;
+          if (dfas[r].size() <= o.inline_max_result_states) {
+            inl[r] = 1;
+            snap[r] = dfas[r];
+          }
+        }
+      }
       bool changed = false;
       for (int host = 0; host < n_rules_in; ++host) {
         std::map<int, const Dfa*> targets;

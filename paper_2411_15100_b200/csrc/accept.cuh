@@ -158,6 +158,7 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
       on_walk(rw);
       int2 out[kAccR];
       if (mirror) {  // fused step kernel: chain rewritten in place in the shared header
+        if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[2]));
         const int nout = rwalker_commit_inplace(rw, P.arena, out, *mirror, spec);
         if (nout < 0) {
           atomicOr(P.err, kErrArena);
@@ -171,6 +172,7 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
         P.head[slot] = nh;
         const int32_t hl = rp.hist_len + 1;
         P.hist_len[slot] = hl < rp.window ? hl : rp.window;
+        if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[3]));
         header_state_inplace(P, *mirror, G, out, nout, 0);
         if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[1]));
         return 1;

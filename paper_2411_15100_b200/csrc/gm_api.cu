@@ -593,8 +593,8 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   unsigned long long* trace = nullptr;
   const char* tr = getenv("GMASK_TRACE");
   if (tr && tr[0] == '1') {
-    if ((st = p->mem.alloc(&trace, 64 + 3 * (size_t)capacity))) return st;
-    GM_CUDA_TRY(cudaMemset(trace, 0, (64 + 3 * (size_t)capacity) * 8));
+    if ((st = p->mem.alloc(&trace, 64 + 16 * (size_t)capacity))) return st;
+    GM_CUDA_TRY(cudaMemset(trace, 0, (64 + 16 * (size_t)capacity) * 8));
   }
   p->dev = DevPool{capacity, max_stacks, H,   tops, meta, head, hist, win, bind,
                    DevArena{keys, acap - 1, err}, err, hdr, trace};

@@ -193,7 +193,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   const int32_t split = blockIdx.y, n_split = gridDim.y;
   trace_mark(P, 1, 0);
   unsigned long long t_start = 0, t_hdr = 0, t_setup = 0, t_ctx = 0, t_walks = 0, t_walk = 0, walk_info = 0;
-  unsigned long long acc_ts[2] = {0, 0};  // accept: frames interned, header state built
+  unsigned long long acc_ts[4] = {0, 0, 0, 0};  // accept: commit start, frames interned, ring written
+  unsigned long long t_pref = 0, t_pre = 0;  // accept: frames interned, header state built
   if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int32_t slot = __ldg(slots + i);
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
@@ -311,6 +312,10 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
             walk_info = (unsigned long long)e.y | ((unsigned long long)rw.n << 16) | ((unsigned long long)rw.nf << 24);
           }
           if (!vec || rw.n > kTmaRows || !kPrefetchRows) return;
+          struct StampPref {  // diagnostics: end of the row prefetch issue
+            unsigned long long& t; bool on;
+            __device__ ~StampPref() { if (on) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); }
+          } stamp_pref{t_pref, kTimeline && P.trace != nullptr};
           const int32_t Wr = hd.W;
           int32_t keys[kTmaRows];
           int nr = 0;
@@ -333,6 +338,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
           bulk_g2s(rows_s + (size_t)kTmaRows * part_bytes, hd.universe, (uint32_t)Wr * 4, &rows_bar);
           s_pref = nr;
         };
+        if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_pre));
         acc = accept_one(P, slot, rp, hd, Gs, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
                          tok == hd.eos, e.x != 0, &hd, prefetch_rows, (kTimeline && P.trace) ? acc_ts : nullptr,
                          kDeferIntern ? &s_spec : nullptr);
@@ -601,8 +607,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
     const int64_t c = (int64_t)i * n_split + split;
-    if (12 * c + 12 <= 3 * (int64_t)P.capacity) {  // per-CTA timeline (absolute %globaltimer stamps)
-      unsigned long long* tr = P.trace + 64 + 12 * c;
+    if (16 * c + 16 <= 16 * (int64_t)P.capacity) {  // per-CTA timeline (absolute %globaltimer stamps)
+      unsigned long long* tr = P.trace + 64 + 16 * c;
       tr[0] = t_start; tr[1] = t_hdr; tr[2] = t_acc; tr[3] = t_setup;
       tr[4] = t_ctx; tr[5] = t_walks; tr[6] = t_merge; tr[7] = t1;
       tr[8] = t_walk;                // accept: register walk done (0: no walk / general path)
@@ -610,6 +616,10 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
       tr[10] = (unsigned long long)total | ((unsigned long long)nt << 32) |
                ((unsigned long long)(s_walked & 0xFFFF) << 40);  // dependents, tops, dependents walked
       tr[11] = acc_ts[0];            // accept: frames interned (publish starts)
+      tr[12] = t_pre;                // accept_one entered
+      tr[13] = t_pref;               // row prefetch issued
+      tr[14] = acc_ts[2];            // commit entered (after on_walk)
+      tr[15] = acc_ts[3];            // ring entry written (header state next)
     }
     if (c == 0) P.trace[63] = (unsigned long long)n_split;
   }

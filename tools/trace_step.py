@@ -33,7 +33,7 @@ def timeline(buf, nc):
     the kernel and p50 / max of every phase over the CTAs."""
     import statistics
 
-    rec = [[buf[64 + 12 * c + k] for k in range(12)] for c in range(nc)]
+    rec = [[buf[64 + 16 * c + k] for k in range(16)] for c in range(nc)]
     t0 = min(r[0] for r in rec)
     t1 = max(r[7] for r in rec)
     out = [f"span {(t1 - t0) / 1e3:.2f} us, CTA start spread {(max(r[0] for r in rec) - t0) / 1e3:.2f}"]
@@ -67,6 +67,16 @@ def timeline(buf, nc):
         out.append(f"[slow {(r[7] - r[0]) / 1e3:.2f}: acc {(r[2] - r[1]) / 1e3 if r[2] else 0:.2f} ({walk}; "
                    f"len {info & 0xFFFF} stacks {(info >> 16) & 0xFF} frames {info >> 24}) "
                    f"deps {r[10] & 0xFFFFFFFF} tops {(r[10] >> 32) & 0xFF} walked {(r[10] >> 40) & 0xFFFF} walks {(r[5] - (r[4] or r[3])) / 1e3:.2f}]")
+    # median split of the register-walk accept over CTAs that took it
+    # (hdr -> accept_one -> walk -> prefetch -> commit -> ring -> header state)
+    segs = [("pre", 1, 12), ("walk", 12, 8), ("pref", 8, 13), ("->commit", 13, 14), ("commit", 14, 11),
+            ("ring", 11, 15), ("hstate+", 15, 2)]
+    parts = []
+    for name, a, b in segs:
+        d = [(r[b] - r[a]) / 1e3 for r in rec if r[a] and r[b] and r[b] >= r[a]]
+        if d:
+            parts.append(f"{name} {statistics.median(d):.2f}/{max(d):.2f}")
+    out.append("accept split p50/max: " + " ".join(parts))
     return " | ".join(out)
 
 
@@ -87,7 +97,7 @@ def main(steps=12, flush=True, fused=False, grammar="json", step_mode=False):
     acc = torch.empty(B, dtype=torch.uint8, device=dev)
     fl = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
     logits = torch.randn((B, vocab.size), dtype=torch.bfloat16, device=dev)
-    NB = 64 + 3 * pool.capacity
+    NB = 64 + 16 * pool.capacity
     buf = (C.c_uint64 * NB)()
     lib = _lib.load()
     for s in range(steps):

@@ -18,7 +18,7 @@ TAG=${1:-r01}
 export GMASK_NO_BUILD=1
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"fill_kernel|apply_tile|accept_tokens|recycle|cache_build|dep_" --csv \
+    -k regex:"fill_kernel|step_ptok|apply_tile|accept_tokens|recycle|cache_build|dep_" --csv \
     --log-file gpurun_out/${TAG}_launches.csv \
     python bench.py --steps 8 --warmup 3 --repeats 1 --no-cpu-baseline > /dev/null 2>&1
 cap() {  # kernel-regex skip tag driver-mode

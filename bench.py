@@ -32,6 +32,7 @@ import statistics
 import sys
 import threading
 import time
+from pathlib import Path
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -77,6 +78,9 @@ WORKLOADS = {
     "xml": dict(config=4, structural=frozenset(b"<>/ab"), force=None, desc="XML_TOY recursive grammar"),
     "arithmetic": dict(config=4, structural=frozenset(b"()+-*/0123456789"), force=(b"(", 40),
                        desc="ARITHMETIC grammar, 40 forced '(' per request (nesting depth >= 32)"),
+    "sql": dict(config=4, structural=frozenset(b"(),.;=<>*' "), force=None,
+                desc="SQL-like query grammar (paper_2411_15100_b200/grammars/sql.gbnf: joins, nested conditions, "
+                     "subqueries)"),
 }
 
 
@@ -89,6 +93,8 @@ def grammar_text(name: str) -> str:
         from paper_2411_15100_b200.schema import schema_to_grammar_text
 
         return schema_to_grammar_text(json.dumps(SAMPLE_SCHEMA))
+    if name == "sql":
+        return (Path(__file__).resolve().parent / "paper_2411_15100_b200" / "grammars" / "sql.gbnf").read_text()
     return {"xml": XML_TOY, "arithmetic": ARITHMETIC}[name]
 
 

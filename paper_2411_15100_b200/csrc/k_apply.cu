@@ -49,15 +49,19 @@ __device__ __forceinline__ void apply_tile(char* __restrict__ tp, int64_t tok_ba
     const uint32_t cw = __shfl_sync(0xFFFFFFFFu, w, c / CPW);
     uint32_t keep = (cw >> ((c % CPW) * VEC)) & FULL;
     const int64_t tok0 = tok_base + (int64_t)c * VEC;
-    if (tok0 + VEC > vocab) {  // ragged tail: tokens >= vocab untouched
+    const bool tail = tok0 + VEC > vocab;
+    if (tail) {  // ragged tail: tokens >= vocab untouched
       const int64_t nvalid = vocab - tok0;
       keep |= nvalid <= 0 ? FULL : (FULL & ~((1u << nvalid) - 1u));
     }
+    const bool dense_mixed = __popc(__ballot_sync(0xFFFFFFFFu, keep != 0 && keep != FULL)) >= kBlendMinLanes;
     if (keep == FULL) continue;
     char* p = tp + c * 16;
     if (keep == 0) {
       st_v4(p, neg);
-    } else {  // mixed chunk: store only the masked elements, never read logits
+    } else if (!tail && dense_mixed) {  // many mixed chunks here: load, blend, one full store each
+      blend_chunk<EB>(p, keep, neg);
+    } else {  // the row's last chunk: element stores, nothing past the vocabulary
       uint32_t m = ~keep & FULL;
       while (m) {
         const int j = __ffs(m) - 1;

@@ -75,12 +75,16 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
   for (int32_t c = threadIdx.x; c < chunks; c += blockDim.x) {
     const int32_t t0 = c * vec;  // relative to tok_lo
     uint32_t keep = (words[t0 >> 5] >> (t0 & 31)) & full;
-    if (t0 + vec > lim) keep |= full & ~((1u << (lim - t0)) - 1u);
+    const bool tail = t0 + vec > lim;
+    if (tail) keep |= full & ~((1u << (lim - t0)) - 1u);
+    const bool dense_mixed = __popc(__ballot_sync(__activemask(), keep != 0 && keep != full)) >= kBlendMinLanes;
     if (keep == full) continue;
     char* p = base + t0 * EB;
     if (keep == 0) {
       st_cs_v4(p, neg);
-    } else {
+    } else if (!tail && dense_mixed) {  // many mixed chunks here: load, blend, one full store each
+      blend_chunk<EB>(p, keep, neg);
+    } else {  // the span's last chunk: element stores, nothing past its end
       uint32_t m = ~keep & full;
       while (m) {
         const int j = __ffs(m) - 1;

@@ -301,10 +301,13 @@ def test_guided_generation_is_in_language():  # REF test_matcher.py:376-386
             m.close()
 
 
-@pytest.mark.parametrize("dtype,B", [("float32", 6), ("bfloat16", 6), ("bfloat16", 100)])
-def test_fused_fill_apply_equals_separate(dtype, B):
-    """K3 (one kernel) == K2 fill then K0 apply, bit for bit, along a trajectory
-    (B = 100: one CTA per request with the cross-CTA apply queue)."""
+@pytest.mark.parametrize("grammar,dtype,B", [("json", "float32", 6), ("json", "bfloat16", 6), ("json", "bfloat16", 100),
+                                             ("sql", "bfloat16", 6), ("sql", "float32", 6)])
+def test_fused_fill_apply_equals_separate(grammar, dtype, B):
+    """K3 (one kernel) == K2 fill then K0 apply == torch.where(bit, x, -inf),
+    bit for bit, along a trajectory (B = 100: one CTA per request with the
+    cross-CTA apply queue; the SQL grammar's identifier-class masks take the
+    load-blend-store path for dense mixed chunks)."""
     import torch
 
     import paper_2411_15100_b200 as gm
@@ -313,11 +316,13 @@ def test_fused_fill_apply_equals_separate(dtype, B):
 
     vocab = vocab_by_name("4000:mixed")
     info = gm.TokenizerInfo.from_vocabulary(vocab)
-    compiled = gm.GrammarCompiler(info).compile_builtin_json_grammar()
+    gc = gm.GrammarCompiler(info)
+    compiled = gc.compile_builtin_json_grammar() if grammar == "json" else gc.compile_grammar(grammar_text(grammar))
     ms = [gm.GrammarMatcher(compiled) for _ in range(B)]
     pool = get_pool()
     slots = torch.tensor([m.slot for m in ms], dtype=torch.int32, device="cuda")
     dt = getattr(torch, dtype)
+    bits = torch.arange(32, device="cuda", dtype=torch.int32)
     g = torch.Generator(device="cuda").manual_seed(3)
     W = (vocab.size + 31) // 32
     for step in range(12):
@@ -329,17 +334,23 @@ def test_fused_fill_apply_equals_separate(dtype, B):
         gm.apply_token_bitmask_inplace(a, bm1)
         batch_fill_apply(pool, slots, b, bm2)
         assert torch.equal(bm1, bm2)
+        allowed = ((bm1.unsqueeze(-1) >> bits) & 1).reshape(B, -1)[:, :vocab.size].bool()
+        want = torch.where(allowed, logits, torch.full_like(logits, float("-inf")))
+        iv = torch.int16 if dt != torch.float32 else torch.int32
+        assert torch.equal(a.view(iv), want.view(iv))
         assert torch.equal(a.view(torch.int16 if dt != torch.float32 else torch.int32),
                            b.view(torch.int16 if dt != torch.float32 else torch.int32))
         c = logits.clone()
         batch_fill_apply(pool, slots, c)  # no bitmask output
         assert torch.equal(a.view(torch.int8), c.view(torch.int8))
         b[:, vocab.eos_id] = float("-inf")
+        if not bool(torch.isfinite(b.float()).any(-1).all()):  # a request can only end (EOS): trajectory done
+            break
         toks = b.float().argmax(-1).tolist()
         assert all(gm.BatchGrammarMatcher.batch_accept_token(ms, toks))
 
 
-@pytest.mark.parametrize("name", ["json", "xml", "arithmetic"])
+@pytest.mark.parametrize("name", ["json", "xml", "arithmetic", "sql"])
 @pytest.mark.parametrize("with_logits", [False, True])
 def test_step_kernel_equals_accept_then_fill(name, with_logits):
     """K5 (accept + recycle + fill [+ apply] in one launch) == K4 accept,

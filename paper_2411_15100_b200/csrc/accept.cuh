@@ -146,7 +146,7 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
     for (int s = 0; s < ntops; ++s) rw.add(rw.ref_of_handle(tops[s].x), tops[s].y);
     for (int64_t i = 0; i < len && rw.n > 0 && !rw.spill; ++i) {
       bool pb = false;
-      rw.step(G, P.arena, byte(i), &pb);
+      rw.template step<true>(G, P.arena, byte(i), &pb);
     }
     trace_mark(P, 0, 3);
     if (!rw.spill) {

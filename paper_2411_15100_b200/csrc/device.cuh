@@ -46,6 +46,8 @@ enum : uint32_t {
 // all sections 16-byte aligned; offsets in bytes from the blob start.
 // node_info[n] = (cache key, first dependent, end dependent, rule) and is only
 // present in binding blobs (grammar blobs have o_ninfo = 0).
+constexpr int32_t kFastPopDies = INT32_MIN;
+
 struct BlobHdr {
   int32_t bytes, n_classes, n_nodes, o_bc;
   int32_t o_flags, o_toff, o_trans, o_pool;
@@ -67,7 +69,8 @@ struct DevGrammar {
   const int32_t* follow_start; // [n_rules]
   const int32_t* follow_next;  // [n_fstates*n_classes]
   const int4* node_info;       // binding views only
-  const int32_t* fast;         // [n_nodes*n_classes] single-stack DFA move, -1 dies, -2 general
+  const int32_t* fast;         // [n_nodes*n_classes] single-stack DFA move, -1 dies, -2 general;
+                               // above the bottom frame also -3 - target / kFastPopDies (gm_grammar_create)
   const int32_t* callers;      // [n_rules*kMaxCallers] return nodes that can sit below a frame of the rule, -1 pad
   const uint32_t* ctx2;        // binding views: [n_dep*kMaxCallers] two-level context classes, or null
   const uint8_t* blob;
@@ -544,12 +547,22 @@ struct RWalker {
   }
 
   // One byte step; same semantics as Walker::step.
+  // kPopFilter (accept and fill walks, which ignore *pop_bottom): also take
+  // the pop-filtered moves of the fast table; the cache build's walks keep
+  // the general step there, so a pop chain that would reach their synthetic
+  // bottom still reports it (ref[0] == -1 is the bottom frame itself).
+  template <bool kPopFilter = false>
   __device__ __forceinline__ int step(const DevGrammar& G, const DevArena& A, uint32_t b, bool* pop_bottom) {
     const int c = G.byte_class[b];
     if (n == 1) {  // plain DFA move
       const int32_t f = G.fast[node[0] * G.n_classes + c];
       if (f >= 0) { node[0] = f; return 1; }
       if (f == -1) { n = 0; return 0; }
+      if (kPopFilter && f < -2 && ref[0] != -1) {  // pops cannot consume c: move (or die) inside the frame
+        if (f == kFastPopDies) { n = 0; return 0; }
+        node[0] = -3 - f;
+        return 1;
+      }
     }
     int32_t nr[R], nn[R];
     int cnt = 0;

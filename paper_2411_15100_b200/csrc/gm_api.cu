@@ -286,22 +286,61 @@ gm_status gm_grammar_create(const gm_grammar_tables* t, gm_grammar** out) {
   // single-stack fast path: for (node, class) the whole byte step when it is
   // a plain DFA move (node cannot pop, exactly one transition, no push, the
   // target is not a spent final): target >= 0; -1 = dies; -2 = general step
-  std::vector<int32_t> fast((size_t)n_idx);
-  for (int32_t u = 0; u < t->n_nodes; ++u)
-    for (int32_t c = 0; c < t->n_classes; ++c) {
-      const int64_t idx = (int64_t)u * t->n_classes + c;
-      const int32_t t0 = t->trans_off[idx], t1 = t->trans_off[idx + 1];
-      int32_t f = -2;
-      if (!(t->node_flags[u] & GM_NODE_POP)) {
-        if (t1 == t0) {
-          f = -1;
-        } else if (t1 - t0 == 1) {
-          const int32_t d = t->trans[2 * t0];
-          const uint32_t plen = (uint32_t)t->trans[2 * t0 + 1] >> 24;
-          if (plen == 0 && !(t->node_flags[d] & GM_NODE_DEAD_END)) f = d;
+  //
+  // A node that can pop (its rule may be complete) still gets a fast entry
+  // for a class no continuation after the pop can consume: FOLLOW(rule) =
+  // the classes with a transition at a return node that can sit below a
+  // frame of the rule, plus FOLLOW of that node's rule when it can pop too
+  // (fixpoint).  Such entries are encoded -3 - target (kFastPopDies: dies)
+  // and taken only above the bottom frame, so the synthetic-bottom walks of
+  // the cache build still see their pop-past-bottom flag.  Identifier and
+  // number runs inside nested rules (SQL, arithmetic) become table moves.
+  const int32_t C = t->n_classes;
+  std::vector<std::vector<int32_t>> returns(t->n_rules);
+  for (int32_t i = 0; i < t->n_trans; ++i) {
+    const int32_t d = t->trans[2 * i];
+    const uint32_t pk = (uint32_t)t->trans[2 * i + 1];
+    const uint32_t poff = pk & 0xFFFFFF, plen = pk >> 24;
+    for (uint32_t k = 0; k < plen; ++k) {
+      const int32_t r = t->node_rule[k + 1 < plen ? t->push_pool[poff + k + 1] : d];
+      if (r >= 0 && r < t->n_rules) returns[r].push_back(t->push_pool[poff + k]);
+    }
+  }
+  std::vector<std::vector<char>> follow(t->n_rules, std::vector<char>((size_t)C, 0));
+  for (bool changed = true; changed;) {
+    changed = false;
+    for (int32_t r = 0; r < t->n_rules; ++r)
+      for (const int32_t ret : returns[r]) {
+        const int32_t rr = t->node_rule[ret];
+        for (int32_t c = 0; c < C; ++c) {
+          if (follow[r][c]) continue;
+          const int64_t idx = (int64_t)ret * C + c;
+          const bool f = t->trans_off[idx + 1] > t->trans_off[idx] ||
+                         ((t->node_flags[ret] & GM_NODE_POP) && rr >= 0 && rr < t->n_rules && follow[rr][c]);
+          if (f) { follow[r][c] = 1; changed = true; }
         }
       }
-      fast[(size_t)idx] = f;
+  }
+  std::vector<int32_t> fast((size_t)n_idx);
+  for (int32_t u = 0; u < t->n_nodes; ++u)
+    for (int32_t c = 0; c < C; ++c) {
+      const int64_t idx = (int64_t)u * C + c;
+      const int32_t t0 = t->trans_off[idx], t1 = t->trans_off[idx + 1];
+      const bool pops = t->node_flags[u] & GM_NODE_POP;
+      const int32_t ru = t->node_rule[u];
+      if (pops && (ru < 0 || ru >= t->n_rules || follow[ru][c])) {
+        fast[(size_t)idx] = -2;
+        continue;
+      }
+      int32_t d = -2;  // plain move target, -1 dies, -2 general
+      if (t1 == t0) {
+        d = -1;
+      } else if (t1 - t0 == 1) {
+        const int32_t dd = t->trans[2 * t0];
+        const uint32_t plen = (uint32_t)t->trans[2 * t0 + 1] >> 24;
+        if (plen == 0 && !(t->node_flags[dd] & GM_NODE_DEAD_END)) d = dd;
+      }
+      fast[(size_t)idx] = !pops ? d : d >= 0 ? -3 - d : d == -1 ? kFastPopDies : -2;
     }
   const size_t o_fast = put(fast.data(), fast.size() * 4);
   // callers[rule]: the return nodes a push run leaves directly below a frame

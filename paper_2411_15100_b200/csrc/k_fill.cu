@@ -519,7 +519,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
       rw.add(rw.ref_of_handle(t.x), t.y);
       for (int b = 0; b < e.y && rw.n > 0 && !rw.spill; ++b) {
         bool pb = false;
-        rw.step(G, P.arena, rec_byte(inl, far, b), &pb);
+        rw.template step<true>(G, P.arena, rec_byte(inl, far, b), &pb);
       }
       bool ok;
       if (!rw.spill) {

@@ -115,6 +115,12 @@ __device__ __forceinline__ void st_cs_u16(void* p, uint32_t v) {
 // mixed chunks among full ones (JSON's bimodal masks) keep the fire-and-forget
 // element stores, which add no load latency to the step (a threshold on the
 // warp's masked-element count via __reduce_add_sync measured 0.7 us slower).
+// Opt-in (-DGM_BLEND=1, GMASK_NVCC_EXTRA): measured K5 SQL 48.2 -> 39.4 us/step
+// but XML_TOY 16.3 -> 31.0 (its load latency sits on the apply's critical
+// path) and JSON +0.1; the default keeps the element stores.
+#ifndef GM_BLEND
+#define GM_BLEND 0
+#endif
 #ifndef GM_BLEND_MIN_LANES
 #define GM_BLEND_MIN_LANES 8
 #endif

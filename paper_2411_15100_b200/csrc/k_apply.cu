@@ -54,7 +54,11 @@ __device__ __forceinline__ void apply_tile(char* __restrict__ tp, int64_t tok_ba
       const int64_t nvalid = vocab - tok0;
       keep |= nvalid <= 0 ? FULL : (FULL & ~((1u << nvalid) - 1u));
     }
+#if GM_BLEND
     const bool dense_mixed = __popc(__ballot_sync(0xFFFFFFFFu, keep != 0 && keep != FULL)) >= kBlendMinLanes;
+#else
+    constexpr bool dense_mixed = false;
+#endif
     if (keep == FULL) continue;
     char* p = tp + c * 16;
     if (keep == 0) {

@@ -77,7 +77,11 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
     uint32_t keep = (words[t0 >> 5] >> (t0 & 31)) & full;
     const bool tail = t0 + vec > lim;
     if (tail) keep |= full & ~((1u << (lim - t0)) - 1u);
+#if GM_BLEND
     const bool dense_mixed = __popc(__ballot_sync(__activemask(), keep != 0 && keep != full)) >= kBlendMinLanes;
+#else
+    constexpr bool dense_mixed = false;
+#endif
     if (keep == full) continue;
     char* p = base + t0 * EB;
     if (keep == 0) {

@@ -6,11 +6,11 @@ set -u
 TAG=${1:-r01}
 export GMASK_NO_BUILD=1
 mkdir -p gpurun_out
-python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+timeout 400 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 : > gpurun_out/${TAG}_configs.jsonl
-python bench.py --grammar schema --batch 64 2>/dev/null | tail -1 >> gpurun_out/${TAG}_configs.jsonl
+timeout 300 python bench.py --grammar schema --batch 64 2>/dev/null | tail -1 >> gpurun_out/${TAG}_configs.jsonl
 for g in xml arithmetic sql json; do
-  python bench.py --grammar $g 2>/dev/null | tail -1 >> gpurun_out/${TAG}_configs.jsonl
+  timeout 300 python bench.py --grammar $g 2>/dev/null | tail -1 >> gpurun_out/${TAG}_configs.jsonl
 done
-python tools/bench_config5.py --out gpurun_out/${TAG}_config5.json > gpurun_out/${TAG}_config5.log 2>&1
+timeout 400 python tools/bench_config5.py --out gpurun_out/${TAG}_config5.json > gpurun_out/${TAG}_config5.log 2>&1
 bash tools/profile_round.sh $TAG

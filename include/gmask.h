@@ -345,9 +345,24 @@ gm_status gm_pool_materialize(gm_pool* p, int32_t handle, int32_t* out,
  * by jump-forward (REF matcher.py:464-486).  Syncs. */
 gm_status gm_pool_first_bytes(gm_pool* p, int32_t slot, uint32_t* bytes8,
                               int32_t* terminable);
-/* Sticky device error flags of the pool (GM_ERR_* bit set), cleared by the
- * read.  Syncs. */
+/* Sticky device error flags, OR over every slot of the pool (bit 1 << GM_ERR_*),
+ * all cleared by the read.  Pool-wide diagnostic; per-request errors come
+ * from gm_pool_errors.  Syncs. */
 gm_status gm_pool_check(gm_pool* p, int32_t* flags_out);
+
+/* Per-request errors.  A device error (stack set over the 4096 cap of REF
+ * matcher.py:116/188-189, a terminated matcher stepped or filled, REF
+ * matcher.py:276-277/379-381, arena exhaustion, a token id out of range) is
+ * recorded in the error word of the slot whose operation failed, never
+ * silently dropped: K4/K5 also return it in accepted_out (bit 1; bit 0 =
+ * accepted) and the state is left unchanged.  gm_pool_errors gathers the
+ * words of slots[0..n) (device int32) into out[0..n) (device uint32, bit
+ * 1 << GM_ERR_*), clearing them when clear != 0.  Stream-ordered, no sync.
+ * gm_status_of_error_bits maps a word to its gm_status (+ gm_last_error()
+ * message), GM_OK for 0. */
+gm_status gm_pool_errors(gm_pool* p, const int32_t* slots, int32_t n,
+                         uint32_t* out, int32_t clear, void* stream);
+gm_status gm_status_of_error_bits(uint32_t bits);
 /* arena statistics: live entries */
 int64_t gm_pool_arena_used(gm_pool* p);
 /* Diagnostics: phase timestamps (ns, %globaltimer) of CTA 0 of the last

@@ -2,6 +2,13 @@
 // step kernel (k_fill.cu): advance one request's stack set by a token's
 // bytes, intern the survivors, append the history ring entry and publish
 // the new slot header.  REF matcher.py:192-217, 239-294.
+//
+// Walk tiers: RWalker (<= kAccR stacks in registers) -> Walker (<= kAccS
+// stacks, local frames) -> BigWalk (<= kWideCap = 4096 stacks in global
+// scratch, the reference's branch cap).  A walk is redone on the next tier
+// whenever it exceeds a cap, so the result never depends on the tier; only
+// exceeding 4096 stacks is an error (GM_ERR_STATE_CAP, REF matcher.py:
+// 188-189).
 #pragma once
 #include "device.cuh"
 
@@ -19,34 +26,41 @@ constexpr int kAccR = GM_ACC_R;  // stacks held in registers by the fast walker
 #endif
 constexpr int kAccRF = GM_ACC_RF;  // its walker-local frames
 
+// accept_one results: bit 0 = accepted, bit 1 = error (the slot's error
+// word says which; the state is unchanged)
+constexpr int kAccOk = 1, kAccErr = 2;
+
 // Current (handle, node) set of a slot: from the header when it fits, else
-// from the ring.
-__device__ inline int load_tops(const DevPool& P, int32_t slot, const SlotHdr& hdr, int2* out) {
+// from the ring (inline entry or its wide block).  Returns the count; *out
+// points at the stacks (shared header or global ring).
+__device__ inline int view_tops(const DevPool& P, int32_t slot, const SlotHdr& hdr, const int2** out) {
   if (hdr.ntops >= 0) {
-    for (int s = 0; s < hdr.ntops; ++s) out[s] = hdr.top[s];
+    *out = hdr.top;
     return hdr.ntops;
   }
   const int32_t h = P.head[slot];
   const int n = P.meta[(size_t)slot * P.H + h] & 0xFFFF;
-  const int2* tops = slot_tops(P, slot, h);
-  for (int s = 0; s < n; ++s) out[s] = tops[s];
+  *out = ring_tops(P, slot, h, n);
   return n;
 }
 
-// Append (refs, nodes) as the next ring entry and publish the new header.
-// `hdr` supplies the binding pointers; `topkeys` the arena keys of the tops
-// when known.
-// Ring position of a slot (head, history length, window), prefetched by
-// lanes 1..3 at kernel entry so the append does not wait on them.
+// Ancestor chain of handle h read from the arena (first kChain frames).
+__device__ inline void chain_from_arena(const DevPool& P, int32_t h, Chain& c) {
+  c.n = 0;
+  while (h >= 0 && c.n < kChain) {
+    const unsigned long long k = arena_load(P.arena, h);
+    if (k == kEmptyKey) break;
+    c.h[c.n] = h;
+    c.k[c.n] = k;
+    ++c.n;
+    h = key_parent(k);
+  }
+}
+
+// Ring position of a slot (head, history length, window).
 struct RingPos {
   int32_t head, hist_len, window;
 };
-
-__device__ __forceinline__ void prefetch_ring(const DevPool& P, int32_t slot, RingPos* rp) {
-  if (threadIdx.x == 1) rp->head = P.head[slot];
-  if (threadIdx.x == 2) rp->hist_len = P.hist_len[slot];
-  if (threadIdx.x == 3) rp->window = P.window[slot];
-}
 
 // Slot header + ring position in ONE round trip: every load is issued before
 // any shared-memory store (a store waiting on its load would otherwise hold
@@ -67,26 +81,31 @@ __device__ __forceinline__ void load_header_ring(const DevPool& P, int32_t slot,
 
 // Append (handle, node) tops as the next ring entry and publish the new
 // header state.  The binding pointers of the global header are unchanged, so
-// only its state fields are rewritten in place.
-__device__ inline void push_tops(const DevPool& P, int32_t slot, const RingPos& rp, const DevGrammar& G, const int2* tops,
-                          int nt, int terminated, const Chain& c, SlotHdr* mirror) {
+// only its state fields are rewritten in place.  False when the set cannot
+// be stored (more than kWideCap stacks, or no wide block free).
+__device__ inline bool push_tops(const DevPool& P, int32_t slot, const RingPos& rp, const DevGrammar& G,
+                                 const int2* tops, int nt, int terminated, const Chain& c, SlotHdr* mirror) {
   const int32_t nh = (rp.head + 1) % P.H;
-  int2* dst = slot_tops(P, slot, nh);
-  for (int s = 0; s < nt; ++s) dst[s] = tops[s];
+  int2* dst = ring_tops_w(P, slot, nh, nt);
+  if (!dst) return false;
+  if (dst != tops)
+    for (int s = 0; s < nt; ++s) dst[s] = tops[s];
   P.meta[(size_t)slot * P.H + nh] = nt | (terminated << 16);
   P.head[slot] = nh;
   const int32_t hl = rp.hist_len + 1;
   P.hist_len[slot] = hl < rp.window ? hl : rp.window;
   if (mirror) {  // new state into the caller's shared copy; the caller publishes it
-    header_state(P, *mirror, G, tops, nt, terminated, &c);
+    header_state(P, *mirror, G, dst, nt, terminated, &c);
   } else {
-    header_state(P, P.hdr[slot], G, tops, nt, terminated, &c);
+    header_state(P, P.hdr[slot], G, dst, nt, terminated, &c);
   }
+  return true;
 }
 
 // Restart a slot at the grammar's start state (recycle_kernel semantics)
 // from inside a step kernel: ring entry 0, empty history, header state.
 __device__ inline void restart_slot(const DevPool& P, int32_t slot, const DevGrammar& G, SlotHdr* mirror) {
+  release_wide(P, slot);
   P.head[slot] = 0;
   P.hist_len[slot] = 0;
   const int2 t0 = make_int2(-1, G.start_node);
@@ -95,9 +114,10 @@ __device__ inline void restart_slot(const DevPool& P, int32_t slot, const DevGra
   header_state(P, *mirror, G, &t0, 1, 0, nullptr);  // the caller publishes it
 }
 
-__device__ inline void push_history(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr,
-                             const DevGrammar& G, int nt, const int32_t* refs, const int32_t* nodes, int terminated,
-                             const int32_t* fh, const unsigned long long* fk, int nfresh, SlotHdr* mirror = nullptr) {
+__device__ inline bool push_history(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr,
+                                    const DevGrammar& G, int nt, const int32_t* refs, const int32_t* nodes,
+                                    int terminated, const int32_t* fh, const unsigned long long* fk, int nfresh,
+                                    SlotHdr* mirror = nullptr) {
   int2 loc[kAccS];
   for (int s = 0; s < nt; ++s) {
     const int32_t r = refs[s];
@@ -105,14 +125,48 @@ __device__ inline void push_history(const DevPool& P, int32_t slot, const RingPo
   }
   Chain c;
   build_chain(c, nt > 0 ? loc[0].x : -1, fh, fk, nfresh, hdr);
-  push_tops(P, slot, rp, G, loc, nt, terminated, c, mirror);
+  return push_tops(P, slot, rp, G, loc, nt, terminated, c, mirror);
 }
 
-// Shared by token and byte-string acceptance (lane 0 only).  byte(i) gives
-// the i-th input byte; is_eos = EOS token.  Returns 1 if accepted.  With
-// `mirror` (== &hdr, the caller's shared header) the new state is written
-// there and the ring updated, but the caller publishes the header (warp-
-// parallel, store_header_state_warp) so a fused step kernel can fill from it.
+// The overflow tier: walk `len` bytes from `tops` in global scratch.  The
+// surviving set is written as the next ring entry.  Returns accept_one's
+// result code.
+template <class ByteFn>
+__device__ inline int accept_wide(const DevPool& P, int32_t slot, const RingPos& rp, const DevGrammar& G,
+                                  const int2* tops, int ntops, int64_t len, ByteFn byte, SlotHdr* mirror) {
+  BigWalk bw;
+  bw.acquire(P.ovf, (uint32_t)slot);
+  bw.start();
+  for (int s = 0; s < ntops; ++s) bw.add(tops[s].x, tops[s].y);
+  for (int64_t i = 0; i < len && bw.n > 0 && !bw.err; ++i) {
+    bool pb = false;
+    bw.step(G, P.arena, byte(i), &pb);
+  }
+  int res = 0;
+  if (bw.err) {
+    slot_error(P, slot, bw.err);
+    res = kAccErr;
+  } else if (bw.n > 0) {
+    Chain c;
+    chain_from_arena(P, bw.cur[0].x, c);
+    if (push_tops(P, slot, rp, G, bw.cur, bw.n, 0, c, mirror)) {
+      res = kAccOk;
+    } else {
+      slot_error(P, slot, kErrCap);
+      res = kAccErr;
+    }
+  }
+  bw.release();
+  return res;
+}
+
+// Shared by token and byte-string acceptance (one thread).  byte(i) gives
+// the i-th input byte; is_eos = EOS token.  Returns kAccOk if accepted, 0 if
+// rejected (state unchanged), kAccErr on an error (recorded in the slot's
+// error word; state unchanged).  With `mirror` (== &hdr, the caller's shared
+// header) the new state is written there and the ring updated, but the
+// caller publishes the header (warp-parallel, store_header_state_warp) so a
+// fused step kernel can fill from it.
 struct NoWalkHook {
   template <class W>
   __device__ __forceinline__ void operator()(const W&) const {}
@@ -122,23 +176,28 @@ struct NoWalkHook {
 // survivors are interned and published: the fused step kernel uses it to
 // start fetching the new tops' cache rows while the commit runs.
 template <class ByteFn, class OnWalk = NoWalkHook>
-__device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr, const DevGrammar& G,
-                          int64_t len, ByteFn byte, bool is_eos, bool reject_token, SlotHdr* mirror = nullptr,
-                          OnWalk on_walk = OnWalk(), unsigned long long* ts = nullptr, SpecOut* spec = nullptr) {
+__device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& rp, const SlotHdr& hdr,
+                                 const DevGrammar& G, int64_t len, ByteFn byte, bool is_eos, bool reject_token,
+                                 SlotHdr* mirror = nullptr, OnWalk on_walk = OnWalk(), unsigned long long* ts = nullptr,
+                                 SpecOut* spec = nullptr) {
   if (hdr.flags & 1) {  // REF matcher.py:276-277 "matcher is terminated"
-    atomicOr(P.err, kErrTerminated);
-    return 0;
+    slot_error(P, slot, kErrTerminated);
+    return kAccErr;
   }
-  int2 tops[kAccS];
-  const int ntops = load_tops(P, slot, hdr, tops);
+  const int2* tops;
+  const int ntops = view_tops(P, slot, hdr, &tops);
   if (is_eos) {  // REF matcher.py:280-288
     if (!(hdr.flags & 2)) return 0;
     Chain c;
     build_chain(c, ntops > 0 ? tops[0].x : -1, nullptr, nullptr, 0, hdr);
-    push_tops(P, slot, rp, G, tops, ntops, 1, c, mirror);
-    return 1;
+    if (!push_tops(P, slot, rp, G, tops, ntops, 1, c, mirror)) {
+      slot_error(P, slot, kErrCap);
+      return kAccErr;
+    }
+    return kAccOk;
   }
   if (reject_token) return 0;  // special or empty token (REF matcher.py:289-293)
+  if (ntops > kAccS) return accept_wide(P, slot, rp, G, tops, ntops, len, byte, mirror);
   // fast path: register walker (<= kAccR stacks)
   if (ntops <= kAccR) {
     RWalker<kAccR, kAccRF> rw;
@@ -151,8 +210,8 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
     trace_mark(P, 0, 3);
     if (!rw.spill) {
       if (rw.err) {
-        atomicOr(P.err, rw.err);
-        return 0;
+        slot_error(P, slot, rw.err);
+        return kAccErr;
       }
       if (rw.n == 0) return 0;
       on_walk(rw);
@@ -161,8 +220,8 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
         if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[2]));
         const int nout = rwalker_commit_inplace(rw, P.arena, out, *mirror, spec);
         if (nout < 0) {
-          atomicOr(P.err, kErrArena);
-          return 0;
+          slot_error(P, slot, kErrArena);
+          return kAccErr;
         }
         if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[0]));
         const int32_t nh = (rp.head + 1) % P.H;
@@ -175,23 +234,23 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
         if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[3]));
         header_state_inplace(P, *mirror, G, out, nout, 0);
         if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[1]));
-        return 1;
+        return kAccOk;
       }
       Chain c;
       const int nout = rwalker_commit(rw, P.arena, out, c);
       if (nout < 0) {
-        atomicOr(P.err, kErrArena);
-        return 0;
+        slot_error(P, slot, kErrArena);
+        return kAccErr;
       }
       trace_mark(P, 0, 4);
       if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[0]));
-      push_tops(P, slot, rp, G, out, nout, 0, c, mirror);
+      push_tops(P, slot, rp, G, out, nout, 0, c, mirror);  // <= kAccR stacks: always inline
       if (ts) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[1]));
       trace_mark(P, 0, 5);
-      return 1;
+      return kAccOk;
     }
   }
-  // general path: any number of stacks / frames
+  // general path: up to kAccS stacks, local frames
   Walker<kAccS, kAccF> w;
   w.reset();
   w.external(hdr.chain_h, hdr.chain_k, hdr.nchain);
@@ -204,24 +263,23 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
     if (!w.template step<kAccS>(G, P.arena, byte(i), &pb)) break;
   }
   trace_mark(P, 0, 3);
+  if (w.err & kErrCap) return accept_wide(P, slot, rp, G, tops, ntops, len, byte, mirror);
   if (w.err) {
-    atomicOr(P.err, w.err);
-    return 0;
+    slot_error(P, slot, w.err);
+    return kAccErr;
   }
   if (w.n == 0) return 0;
   if (!w.intern_all(P.arena)) {
-    atomicOr(P.err, w.err | kErrArena);
-    return 0;
+    slot_error(P, slot, w.err | kErrArena);
+    return kAccErr;
   }
   trace_mark(P, 0, 4);
-  if (w.n > P.max_stacks) {
-    atomicOr(P.err, kErrCap);
-    return 0;
+  if (!push_history(P, slot, rp, hdr, G, w.n, w.ref, w.node, 0, w.kh, w.kk, w.nk, mirror)) {
+    slot_error(P, slot, kErrCap);
+    return kAccErr;
   }
-  push_history(P, slot, rp, hdr, G, w.n, w.ref, w.node, 0, w.kh, w.kk, w.nk, mirror);
   trace_mark(P, 0, 5);
-  return 1;
+  return kAccOk;
 }
-
 
 }  // namespace gm

@@ -235,7 +235,7 @@ __device__ inline int32_t arena_probe(const DevArena& A, unsigned long long key,
     if (cur == kEmptyKey || cur == key) return (int32_t)i;
     i = (i + 1) & A.mask;
   }
-  atomicOr(A.err, kErrArena);
+  if (A.err) atomicOr(A.err, kErrArena);
   return -1;
 }
 __device__ inline int32_t arena_intern(const DevArena& A, int32_t parent, int32_t node, uint32_t term) {
@@ -705,6 +705,138 @@ __device__ inline int rwalker_commit(RWalker<R, F>& w, const DevArena& A, int2* 
   return n;
 }
 
+// ---------------------------------------------------------------------------
+// Overflow walker.  The register and local-memory walkers above hold at most
+// 2-32 stacks; a walk that exceeds them (ambiguous grammars keep one stack
+// per live alternative) is redone here with its stack sets in global-memory
+// scratch, every pushed frame interned into the arena at once, and dedupe
+// through a generation-tagged hash set — up to kWideCap stacks, the
+// reference's branch cap (REF matcher.py:116 DEFAULT_BRANCH_CAP = 4096,
+// cache.py:58, pda.py:53; exceeding it raises there and here).  Scratch comes
+// in "lanes" (pool- or build-level), taken by one thread for the duration of
+// one walk (spin lock: holders never wait on anything, so it cannot
+// deadlock).
+constexpr int kWideCap = 4096;
+constexpr int kHashCap = 2 * kWideCap;  // power of two
+
+struct DevOverflow {
+  int2* bufs;                  // [lanes][2][kWideCap]
+  unsigned long long* hkeys;   // [lanes][kHashCap]
+  uint32_t* hgen;              // [lanes][kHashCap]
+  uint32_t* gen;               // [lanes]
+  int32_t* lock;               // [lanes]
+  int32_t lanes;
+};
+
+struct BigWalk {
+  DevOverflow O;
+  int lane;
+  int2* cur;
+  int2* nxt;
+  int n;
+  uint32_t err;
+
+  __device__ void acquire(const DevOverflow& ov, uint32_t hint) {
+    O = ov;
+    n = 0;
+    err = 0;
+    lane = -1;
+    for (uint32_t i = hint;; ++i) {
+      const int l = (int)(i % (uint32_t)O.lanes);
+      if (atomicCAS(O.lock + l, 0, 1) == 0) { lane = l; break; }
+      if ((i - hint) % (uint32_t)O.lanes == (uint32_t)O.lanes - 1) __nanosleep(256);
+    }
+    __threadfence();
+    cur = O.bufs + (size_t)lane * 2 * kWideCap;
+    nxt = cur + kWideCap;
+  }
+  __device__ void release() {
+    __threadfence();
+    atomicExch(O.lock + lane, 0);
+  }
+  // fresh dedupe set for the next generation of stacks
+  __device__ void new_set() {
+    uint32_t g = O.gen[lane] + 1;
+    if (g == 0) {  // wrapped: clear the tags
+      uint32_t* t = O.hgen + (size_t)lane * kHashCap;
+      for (int i = 0; i < kHashCap; ++i) t[i] = 0;
+      g = 1;
+    }
+    O.gen[lane] = g;
+  }
+  // append (h, node) to `out` (count *cnt) unless already present
+  __device__ void add_to(int2* out, int* cnt, int32_t h, int32_t node) {
+    const unsigned long long key = ((unsigned long long)(uint32_t)(h + 1) << 32) | (uint32_t)node;
+    const uint32_t g = O.gen[lane];
+    unsigned long long* hk = O.hkeys + (size_t)lane * kHashCap;
+    uint32_t* hg = O.hgen + (size_t)lane * kHashCap;
+    for (uint32_t i = mix64(key) & (kHashCap - 1);; i = (i + 1) & (kHashCap - 1)) {
+      if (hg[i] != g) {
+        if (*cnt >= kWideCap) { err |= kErrCap; return; }
+        hg[i] = g;
+        hk[i] = key;
+        out[(*cnt)++] = make_int2(h, node);
+        return;
+      }
+      if (hk[i] == key) return;
+    }
+  }
+  __device__ void start() { new_set(); n = 0; }
+  __device__ void add(int32_t h, int32_t node) { add_to(cur, &n, h, node); }
+
+  __device__ uint32_t term_of(const DevArena& A, int32_t h) {
+    if (h < 0) return 1u;
+    const unsigned long long k = arena_load(A, h);
+    if (k == kEmptyKey) { err |= kErrInvalid; return 0u; }
+    return key_term(k);
+  }
+  __device__ void pop(const DevArena& A, int32_t h, int32_t& ph, int32_t& pn) {
+    const unsigned long long k = arena_load(A, h);
+    if (k == kEmptyKey) { err |= kErrInvalid; ph = -1; pn = 0; return; }
+    ph = key_parent(k);
+    pn = key_node(k);
+  }
+
+  // One byte step of the whole set, Walker::step semantics, all frames
+  // interned.  Returns the number of live stacks.
+  __device__ int step(const DevGrammar& G, const DevArena& A, uint32_t b, bool* pop_bottom) {
+    const int c = G.byte_class[b];
+    new_set();
+    int cnt = 0;
+    for (int s = 0; s < n && !err; ++s) {
+      int32_t h = cur[s].x, m = cur[s].y;
+      while (true) {
+        const int32_t idx = m * G.n_classes + c;
+        const int32_t t0 = G.trans_off[idx], t1 = G.trans_off[idx + 1];
+        for (int32_t t = t0; t < t1; ++t) {
+          const int2 tr = G.trans[t];
+          int32_t d = tr.x;
+          const int plen = (int)((uint32_t)tr.y >> 24);
+          const int poff = tr.y & 0xFFFFFF;
+          int32_t hh = h;
+          for (int k = 0; k < plen; ++k) {
+            const int32_t ret = G.push_pool[poff + k];
+            const uint32_t term = ((G.node_flags[ret] & GM_NODE_POP) ? 1u : 0u) & term_of(A, hh);
+            hh = arena_intern(A, hh, ret, term);
+            if (hh < 0) { err |= kErrArena; return 0; }
+          }
+          if (plen == 0)
+            while ((G.node_flags[d] & GM_NODE_DEAD_END) && hh >= 0) pop(A, hh, hh, d);
+          add_to(nxt, &cnt, hh, d);
+        }
+        if (!(G.node_flags[m] & GM_NODE_POP)) break;
+        if (h < 0) { *pop_bottom = true; break; }
+        pop(A, h, h, m);
+        if ((uint32_t)m >= (uint32_t)G.n_nodes) { err |= kErrInvalid; break; }
+      }
+    }
+    int2* t = cur; cur = nxt; nxt = t;
+    n = err ? 0 : cnt;
+    return n;
+  }
+};
+
+// ---------------------------------------------------------------------------
 // Allowed-continuation check of the context-expansion DFA (REF cache.py:
 // 303-333 FollowFsa.allows): may some legal continuation of rule `rid` start
 // with (or extend) data[0:len)?
@@ -760,7 +892,15 @@ struct DevPool {
   int32_t* window;            // [capacity]
   const DevBinding** binding; // [capacity]
   DevArena arena;
-  uint32_t* err;
+  uint32_t* err;              // [capacity] per-slot sticky error bits (GM_ERR_* as 1 << code)
+  // wide top sets (more than max_stacks stacks, up to kWideCap): a ring
+  // entry's stacks then live in a block of wide_pool, owned by that (slot,
+  // ring position) until the slot is reset / recycled
+  int2* wide_pool;            // [n_wide][kWideCap]
+  int32_t* wide;              // [capacity][H] block index or -1
+  uint32_t* wide_bits;        // allocation bitmap [ceil(n_wide/32)]
+  int32_t n_wide;
+  DevOverflow ovf;            // overflow-walker scratch lanes
   SlotHdr* hdr;               // [capacity]
   unsigned long long* trace;  // optional phase timestamps (GMASK_TRACE=1), else null
   // launch hint: the binding every bound slot shares (host bookkeeping,
@@ -797,6 +937,57 @@ __device__ __forceinline__ void trace_mark(const DevPool& P, int kernel, int pha
 
 __device__ __forceinline__ int2* slot_tops(const DevPool& P, int32_t slot, int32_t h) {
   return P.tops + ((size_t)slot * P.H + h) * P.max_stacks;
+}
+
+// Per-slot error reporting: the request whose operation failed gets the bit
+// (REF raises MatcherError on that matcher, matcher.py:188-189, 379-381).
+__device__ __forceinline__ void slot_error(const DevPool& P, int32_t slot, uint32_t bits) {
+  if (bits) atomicOr(P.err + slot, bits);
+}
+
+// Stacks of ring entry h holding n stacks (inline or in its wide block).
+__device__ __forceinline__ const int2* ring_tops(const DevPool& P, int32_t slot, int32_t h, int n) {
+  if (n <= P.max_stacks) return slot_tops(P, slot, h);
+  const int32_t b = P.wide[(size_t)slot * P.H + h];
+  return b >= 0 ? P.wide_pool + (size_t)b * kWideCap : slot_tops(P, slot, h);
+}
+
+// Destination for n stacks in ring entry h: inline, or the entry's wide
+// block (allocated on first use); null when n exceeds the cap or no block is
+// free.
+__device__ inline int2* ring_tops_w(const DevPool& P, int32_t slot, int32_t h, int n) {
+  if (n <= P.max_stacks) return slot_tops(P, slot, h);
+  if (n > kWideCap || P.n_wide <= 0) return nullptr;
+  int32_t* wb = P.wide + (size_t)slot * P.H + h;
+  if (*wb >= 0) return P.wide_pool + (size_t)*wb * kWideCap;
+  const int nw = (P.n_wide + 31) >> 5;
+  for (int w0 = 0; w0 < nw; ++w0) {
+    const int w = (w0 + slot) % nw;
+    for (;;) {
+      const uint32_t cur = ((volatile uint32_t*)P.wide_bits)[w];
+      const uint32_t avail = ~cur & (w == nw - 1 && (P.n_wide & 31) ? ((1u << (P.n_wide & 31)) - 1u) : ~0u);
+      if (!avail) break;
+      const int bit = __ffs(avail) - 1;
+      if (!(atomicOr(P.wide_bits + w, 1u << bit) & (1u << bit))) {
+        *wb = w * 32 + bit;
+        return P.wide_pool + (size_t)*wb * kWideCap;
+      }
+    }
+  }
+  return nullptr;
+}
+
+// Return every wide block of a slot (reset / recycle / fork target).
+__device__ inline void release_wide(const DevPool& P, int32_t slot, int lane = 0, int nlanes = 1) {
+  if (P.n_wide <= 0) return;
+  for (int h = lane; h < P.H; h += nlanes) {
+    int32_t* wb = P.wide + (size_t)slot * P.H + h;
+    const int32_t b = *wb;
+    if (b >= 0) {
+      atomicAnd(P.wide_bits + (b >> 5), ~(1u << (b & 31)));
+      *wb = -1;
+    }
+  }
 }
 
 __device__ __forceinline__ void load_header(const DevPool& P, int32_t slot, SlotHdr* s_hdr) {
@@ -1068,33 +1259,75 @@ __device__ inline void store_header_state(const DevPool& P, int32_t slot, const 
 // Collision repair of a deferred commit (rare): re-intern the fresh frames in
 // push order with their parents' real handles, then rewrite the shared
 // header's chain and first top and republish it and the ring entry.
-__device__ inline void spec_fixup(const DevPool& P, int32_t slot, const SpecOut& sp, SlotHdr& h) {
-  int32_t real[kSpecMax];
-  unsigned long long rkey[kSpecMax];
+// Real handles of a deferred commit's fresh frames (push order, parents
+// first): probe each with its parent's real handle.  Idempotent (hash-consed:
+// every caller gets the same handles, whether or not the speculative CAS has
+// landed yet).  False on arena exhaustion.
+__device__ inline bool spec_real_handles(const DevArena& A, const SpecOut& sp, int32_t* real,
+                                         unsigned long long* rkey) {
   for (int k = 0; k < sp.n; ++k) {
     int32_t ph = key_parent(sp.key[k]);
     for (int j = 0; j < k; ++j)
       if (sp.slot[j] == ph) { ph = real[j]; break; }
     rkey[k] = arena_key(ph, key_node(sp.key[k]), key_term(sp.key[k]));
-    real[k] = arena_probe(P.arena, rkey[k], mix64(rkey[k]));
-    if (real[k] < 0) { atomicOr(P.err, kErrArena); return; }
+    real[k] = arena_probe(A, rkey[k], mix64(rkey[k]));
+    if (real[k] < 0) return false;
   }
-  auto fix = [&](int32_t& hh, unsigned long long* kk) {
-    for (int j = 0; j < sp.n; ++j)
-      if (sp.slot[j] == hh) { hh = real[j]; if (kk) *kk = rkey[j]; return; }
-  };
-  for (int i = 0; i < h.nchain; ++i) fix(h.chain_h[i], &h.chain_k[i]);
-  const int nt = h.ntops < 0 ? 0 : h.ntops;
-  for (int s = 0; s < nt; ++s) fix(h.top[s].x, nullptr);
-  const int32_t head = P.head[slot];
-  int2* ring = slot_tops(P, slot, head);
-  const int nr = P.meta[(size_t)slot * P.H + head] & 0xFFFF;
-  for (int s = 0; s < nr; ++s) {
-    int32_t x = ring[s].x;
-    fix(x, nullptr);
-    ring[s].x = x;
+  return true;
+}
+
+// A fresh frame is identified by (speculative slot, key): an older ancestor
+// whose real handle happens to equal a fresh frame's slot (the very key that
+// caused the collision may be that ancestor) has a different key and keeps
+// its handle.  Fresh frames sit at the front of the chain.
+__device__ __forceinline__ int spec_fresh_index(const SpecOut& sp, int32_t hh, unsigned long long kk) {
+  for (int j = 0; j < sp.n; ++j)
+    if (sp.slot[j] == hh && sp.key[j] == kk) return j;
+  return -1;
+}
+
+// Rewrite a chain copy (and the top handle *th when it heads the chain) to
+// real handles.  Used by walks that look frames up by handle (the general
+// and overflow walkers) while a deferred commit's CASes may be in flight.
+__device__ inline bool spec_realize(const DevArena& A, const SpecOut& sp, int32_t* ch_h, unsigned long long* ch_k,
+                                    int nc, int32_t* th) {
+  int32_t real[kSpecMax];
+  unsigned long long rkey[kSpecMax];
+  if (!spec_real_handles(A, sp, real, rkey)) return false;
+  for (int i = 0; i < nc; ++i) {
+    const int j = spec_fresh_index(sp, ch_h[i], ch_k[i]);
+    if (j < 0) break;
+    if (i == 0 && *th == ch_h[0]) *th = real[j];
+    ch_h[i] = real[j];
+    ch_k[i] = rkey[j];
+  }
+  return true;
+}
+
+__device__ inline bool spec_fixup(const DevPool& P, int32_t slot, const SpecOut& sp, SlotHdr& h) {
+  int32_t real[kSpecMax];
+  unsigned long long rkey[kSpecMax];
+  if (!spec_real_handles(P.arena, sp, real, rkey)) {
+    slot_error(P, slot, kErrArena);
+    return false;
+  }
+  // the single surviving top is fresh iff chain position 0 is
+  const int32_t top_old = h.ntops > 0 ? h.top[0].x : -1;
+  const int top_j = (h.nchain > 0 && h.chain_h[0] == top_old) ? spec_fresh_index(sp, h.chain_h[0], h.chain_k[0]) : -1;
+  for (int i = 0; i < h.nchain; ++i) {
+    const int j = spec_fresh_index(sp, h.chain_h[i], h.chain_k[i]);
+    if (j < 0) break;  // past the fresh frames: the rest of the chain is older
+    h.chain_h[i] = real[j];
+    h.chain_k[i] = rkey[j];
+  }
+  if (top_j >= 0) {
+    h.top[0].x = real[top_j];
+    const int32_t head = P.head[slot];
+    int2* ring = slot_tops(P, slot, head);  // deferred commits keep one stack: ring entry 0 is the top
+    if (ring[0].x == top_old) ring[0].x = real[top_j];
   }
   store_header_state(P, slot, h);
+  return true;
 }
 
 // Rebuild a slot header from the binding (reset / recycle / rollback path).

@@ -23,8 +23,9 @@ gm_status fail(gm_status code, const std::string& msg) {
 }
 
 // kernel launchers (k_*.cu)
-gm_status launch_cache_build(const DevGrammar&, const DevVocab&, const DevArena&, int32_t, int32_t,
-                             uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+gm_status launch_cache_build(const DevGrammar&, const DevVocab&, const DevArena&, const DevOverflow&, int32_t,
+                             int32_t, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+gm_status launch_pool_errors(const DevPool&, const int32_t*, int32_t, uint32_t*, int32_t, cudaStream_t);
 gm_status launch_row_popcount(const uint32_t*, int32_t, int32_t, int64_t*, cudaStream_t);
 gm_status launch_dep_compact(const uint32_t*, int32_t, int32_t, const int32_t*, int32_t*, cudaStream_t);
 gm_status launch_dep_records(const int32_t*, int64_t, const int4*, int4*, cudaStream_t);
@@ -74,27 +75,67 @@ struct DevAllocs {
   }
 };
 
-// scratch arena for cache builds (walker frame overflow only), per process
-static DevArena g_build_arena{nullptr, 0, nullptr};
-static gm_status build_arena(DevArena* out) {
-  if (!g_build_arena.keys) {
-    const uint32_t cap = 1u << 20;
+// Overflow-walker lanes (DevOverflow): `lanes` scratch sets of two
+// kWideCap stack buffers + a kHashCap dedupe table each.
+static gm_status alloc_overflow(int32_t lanes, DevOverflow* O, std::vector<void*>* owned) {
+  *O = DevOverflow{};
+  if (lanes <= 0) return GM_OK;
+  void *bufs, *hk, *hg, *gen, *lock;
+  GM_CUDA_TRY(cudaMalloc(&bufs, (size_t)lanes * 2 * kWideCap * sizeof(int2)));
+  GM_CUDA_TRY(cudaMalloc(&hk, (size_t)lanes * kHashCap * 8));
+  GM_CUDA_TRY(cudaMalloc(&hg, (size_t)lanes * kHashCap * 4));
+  GM_CUDA_TRY(cudaMalloc(&gen, (size_t)lanes * 4));
+  GM_CUDA_TRY(cudaMalloc(&lock, (size_t)lanes * 4));
+  GM_CUDA_TRY(cudaMemset(hg, 0, (size_t)lanes * kHashCap * 4));
+  GM_CUDA_TRY(cudaMemset(gen, 0, (size_t)lanes * 4));
+  GM_CUDA_TRY(cudaMemset(lock, 0, (size_t)lanes * 4));
+  for (void* q : {bufs, hk, hg, gen, lock}) owned->push_back(q);
+  *O = DevOverflow{static_cast<int2*>(bufs), static_cast<unsigned long long*>(hk), static_cast<uint32_t*>(hg),
+                   static_cast<uint32_t*>(gen), static_cast<int32_t*>(lock), lanes};
+  return GM_OK;
+}
+
+static int32_t env_i32(const char* name, int32_t dflt) {
+  const char* e = getenv(name);
+  return e && *e ? (int32_t)atoi(e) : dflt;
+}
+
+// Scratch for cache builds, per host thread (builds on one thread are
+// serial: gm_cache_build_rows syncs its stream): an arena for the walkers'
+// interned frames, cleared before every build, and overflow lanes.
+struct BuildScratch {
+  DevArena arena{nullptr, 0, nullptr};
+  DevOverflow ovf{};
+  std::vector<void*> owned;
+  ~BuildScratch() {
+    for (void* q : owned) cudaFree(q);
+  }
+};
+static thread_local BuildScratch g_build;
+static gm_status build_scratch(BuildScratch** out, cudaStream_t s) {
+  BuildScratch& b = g_build;
+  if (!b.arena.keys) {
+    const uint32_t cap = 1u << 22;
     unsigned long long* keys = nullptr;
     uint32_t* err = nullptr;
     GM_CUDA_TRY(cudaMalloc(&keys, sizeof(unsigned long long) * cap));
-    GM_CUDA_TRY(cudaMemset(keys, 0xFF, sizeof(unsigned long long) * cap));
+    b.owned.push_back(keys);
     GM_CUDA_TRY(cudaMalloc(&err, sizeof(uint32_t)));
-    GM_CUDA_TRY(cudaMemset(err, 0, sizeof(uint32_t)));
-    g_build_arena = DevArena{keys, cap - 1, err};
+    b.owned.push_back(err);
+    b.arena = DevArena{keys, cap - 1, err};
+    gm_status st = alloc_overflow(env_i32("GMASK_BUILD_OVF_LANES", 64), &b.ovf, &b.owned);
+    if (st) return st;
   }
-  *out = g_build_arena;
+  GM_CUDA_TRY(cudaMemsetAsync(b.arena.keys, 0xFF, sizeof(unsigned long long) * ((size_t)b.arena.mask + 1), s));
+  GM_CUDA_TRY(cudaMemsetAsync(b.arena.err, 0, 4, s));
+  *out = &b;
   return GM_OK;
 }
 
 static gm_status err_bits_to_status(uint32_t bits, const char* where) {
   if (!bits) return GM_OK;
   std::string w(where);
-  if (bits & kErrCap) return fail(GM_ERR_STATE_CAP, w + ": stack set exceeded cap");
+  if (bits & kErrCap) return fail(GM_ERR_STATE_CAP, w + ": stack set exceeded cap of " + std::to_string(kWideCap));
   if (bits & kErrArena) return fail(GM_ERR_ARENA_FULL, w + ": device stack arena is full");
   if (bits & kErrTerminated) return fail(GM_ERR_TERMINATED, w + ": matcher is terminated");
   if (bits & (1u << GM_ERR_ROLLBACK)) return fail(GM_ERR_ROLLBACK, w + ": cannot roll back beyond history");
@@ -441,15 +482,14 @@ gm_status gm_cache_build_rows(const gm_grammar* g, const gm_vocab* v, int32_t ke
   const size_t bytes = (size_t)n * v->dev.W * 4;
   GM_CUDA_TRY(cudaMemsetAsync(acc_rows, 0, bytes, s));
   GM_CUDA_TRY(cudaMemsetAsync(dep_rows, 0, bytes, s));
-  DevArena A;
-  gm_status st = build_arena(&A);
+  BuildScratch* B;
+  gm_status st = build_scratch(&B, s);
   if (st) return st;
-  GM_CUDA_TRY(cudaMemsetAsync(A.err, 0, 4, s));
-  st = launch_cache_build(g->dev, v->dev, A, key_begin, n, reinterpret_cast<uint32_t*>(acc_rows),
-                          reinterpret_cast<uint32_t*>(dep_rows), A.err, s);
+  st = launch_cache_build(g->dev, v->dev, B->arena, B->ovf, key_begin, n, reinterpret_cast<uint32_t*>(acc_rows),
+                          reinterpret_cast<uint32_t*>(dep_rows), B->arena.err, s);
   if (st) return st;
   uint32_t bits = 0;
-  GM_CUDA_TRY(cudaMemcpyAsync(&bits, A.err, 4, cudaMemcpyDeviceToHost, s));
+  GM_CUDA_TRY(cudaMemcpyAsync(&bits, B->arena.err, 4, cudaMemcpyDeviceToHost, s));
   GM_CUDA_TRY(cudaStreamSynchronize(s));
   return err_bits_to_status(bits, "cache build");
 }
@@ -605,26 +645,41 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   gm_pool* p = new gm_pool();
   const int32_t H = max_window + 1;
   const uint32_t acap = 1u << arena_log2;
+  // wide top sets (> max_stacks stacks, up to kWideCap): blocks of kWideCap
+  // stacks shared by the pool; overflow-walker lanes
+  const int32_t n_wide = std::max(0, env_i32("GMASK_WIDE_BLOCKS", 64));
+  const int32_t lanes = std::max(1, env_i32("GMASK_OVF_LANES", 32));
   gm_status st;
-  int2* tops;
-  int32_t *meta, *head, *hist, *win, *scr;
+  int2 *tops, *wide_pool;
+  int32_t *meta, *head, *hist, *win, *scr, *wide;
   const DevBinding** bind;
   unsigned long long* keys;
-  uint32_t* err;
+  uint32_t *err, *arena_err, *wide_bits;
   uint8_t* sb;
   SlotHdr* hdr;
+  DevOverflow ovf;
+  auto bail = [&](gm_status e) {
+    p->mem.release();
+    delete p;
+    return e;
+  };
   if ((st = p->mem.alloc(&hdr, (size_t)capacity)) || (st = p->mem.alloc(&tops, (size_t)capacity * H * max_stacks)) ||
       (st = p->mem.alloc(&meta, (size_t)capacity * H)) || (st = p->mem.alloc(&head, (size_t)capacity)) ||
       (st = p->mem.alloc(&hist, (size_t)capacity)) || (st = p->mem.alloc(&win, (size_t)capacity)) ||
       (st = p->mem.alloc(&bind, (size_t)capacity)) || (st = p->mem.alloc(&keys, (size_t)acap)) ||
-      (st = p->mem.alloc(&err, 1)) || (st = p->mem.alloc(&sb, 1 << 16)) || (st = p->mem.alloc(&scr, 1024))) {
-    p->mem.release();
-    delete p;
-    return st;
-  }
+      (st = p->mem.alloc(&err, (size_t)capacity)) || (st = p->mem.alloc(&arena_err, 1)) ||
+      (st = p->mem.alloc(&sb, 1 << 16)) || (st = p->mem.alloc(&scr, 1024)) ||
+      (st = p->mem.alloc(&wide_pool, (size_t)std::max(n_wide, 1) * kWideCap)) ||
+      (st = p->mem.alloc(&wide, (size_t)capacity * H)) ||
+      (st = p->mem.alloc(&wide_bits, (size_t)(n_wide + 31) / 32 + 1)) ||
+      (st = alloc_overflow(lanes, &ovf, &p->mem.ptrs)))
+    return bail(st);
   GM_CUDA_TRY(cudaMemset(keys, 0xFF, sizeof(unsigned long long) * acap));
-  GM_CUDA_TRY(cudaMemset(err, 0, 4));
+  GM_CUDA_TRY(cudaMemset(err, 0, 4 * (size_t)capacity));
+  GM_CUDA_TRY(cudaMemset(arena_err, 0, 4));
   GM_CUDA_TRY(cudaMemset(meta, 0, sizeof(int32_t) * (size_t)capacity * H));
+  GM_CUDA_TRY(cudaMemset(wide, 0xFF, sizeof(int32_t) * (size_t)capacity * H));
+  GM_CUDA_TRY(cudaMemset(wide_bits, 0, 4 * ((size_t)(n_wide + 31) / 32 + 1)));
   GM_CUDA_TRY(cudaMemset(head, 0, sizeof(int32_t) * (size_t)capacity));
   GM_CUDA_TRY(cudaMemset(hist, 0, sizeof(int32_t) * (size_t)capacity));
   GM_CUDA_TRY(cudaMemset(bind, 0, sizeof(void*) * (size_t)capacity));
@@ -632,11 +687,28 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   unsigned long long* trace = nullptr;
   const char* tr = getenv("GMASK_TRACE");
   if (tr && tr[0] == '1') {
-    if ((st = p->mem.alloc(&trace, 64 + 16 * (size_t)capacity))) return st;
+    if ((st = p->mem.alloc(&trace, 64 + 16 * (size_t)capacity))) return bail(st);
     GM_CUDA_TRY(cudaMemset(trace, 0, (64 + 16 * (size_t)capacity) * 8));
   }
-  p->dev = DevPool{capacity, max_stacks, H,   tops, meta, head, hist, win, bind,
-                   DevArena{keys, acap - 1, err}, err, hdr, trace};
+  p->dev = DevPool{};
+  p->dev.capacity = capacity;
+  p->dev.max_stacks = max_stacks;
+  p->dev.H = H;
+  p->dev.tops = tops;
+  p->dev.meta = meta;
+  p->dev.head = head;
+  p->dev.hist_len = hist;
+  p->dev.window = win;
+  p->dev.binding = bind;
+  p->dev.arena = DevArena{keys, acap - 1, arena_err};
+  p->dev.err = err;
+  p->dev.wide_pool = wide_pool;
+  p->dev.wide = wide;
+  p->dev.wide_bits = wide_bits;
+  p->dev.n_wide = n_wide;
+  p->dev.ovf = ovf;
+  p->dev.hdr = hdr;
+  p->dev.trace = trace;
   // opt-in L2 persistence for the arena (GMASK_L2_PERSIST=1): a device-wide
   // persisting carve-out + a persisting access-policy window on the step
   // launches; measured no gain on the JSON bench (the contended arena lines
@@ -957,13 +1029,22 @@ gm_status gm_pool_recycle(gm_pool* p, const int32_t* slots, int32_t n, void* str
 
 gm_status gm_pool_check(gm_pool* p, int32_t* flags_out) {
   if (!p) return fail(GM_ERR_INVALID, "null pool");
-  uint32_t bits = 0;
   GM_CUDA_TRY(cudaDeviceSynchronize());
-  GM_CUDA_TRY(cudaMemcpy(&bits, p->dev.err, 4, cudaMemcpyDeviceToHost));
-  GM_CUDA_TRY(cudaMemset(p->dev.err, 0, 4));
+  std::vector<uint32_t> words((size_t)p->dev.capacity);
+  GM_CUDA_TRY(cudaMemcpy(words.data(), p->dev.err, words.size() * 4, cudaMemcpyDeviceToHost));
+  GM_CUDA_TRY(cudaMemset(p->dev.err, 0, words.size() * 4));
+  uint32_t bits = 0;
+  for (uint32_t w : words) bits |= w;
   if (flags_out) *flags_out = (int32_t)bits;
   return err_bits_to_status(bits, "matcher");
 }
+
+gm_status gm_pool_errors(gm_pool* p, const int32_t* slots, int32_t n, uint32_t* out, int32_t clear, void* stream) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  return launch_pool_errors(p->dev, slots, n, out, clear, as_stream(stream));
+}
+
+gm_status gm_status_of_error_bits(uint32_t bits) { return err_bits_to_status(bits, "matcher"); }
 
 gm_status gm_pool_slot_info(gm_pool* p, int32_t slot, int32_t* info5, int32_t* stacks_out, int32_t max_out) {
   if (!p || slot < 0 || slot >= p->dev.capacity) return fail(GM_ERR_INVALID, "slot out of range");

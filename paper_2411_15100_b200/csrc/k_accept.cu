@@ -39,15 +39,15 @@ accept_tokens_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t
   trace_mark(P, 0, 2);
   if (threadIdx.x != 0) return;
   if (!in_range) {  // REF matcher.py:278-279
-    atomicOr(P.err, kErrInvalid);
-    accepted[i] = 0;
+    slot_error(P, slot, kErrInvalid);
+    accepted[i] = kAccErr;
     return;
   }
   const int4 e = s_rec[0], inl = s_rec[1];
   const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;
   const int acc = accept_one(P, slot, rp, hd, G, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
                              tid == hd.eos, e.x != 0, &hd);
-  if (acc) store_header_state(P, slot, hd);  // accept_one leaves the mirror's publish to the caller
+  if (acc & kAccOk) store_header_state(P, slot, hd);  // accept_one leaves the mirror's publish to the caller
   accepted[i] = (uint8_t)acc;
 }
 
@@ -61,29 +61,32 @@ accept_bytes_kernel(DevPool P, int32_t slot, const uint8_t* data, int64_t len, u
   const DevGrammar G = stage_blob(hd.blob, hd.blob_bytes, tables);
   if (threadIdx.x != 0) return;
   if (hd.flags & 1) {
-    atomicOr(P.err, kErrTerminated);
-    *accepted = 0;
+    slot_error(P, slot, kErrTerminated);
+    *accepted = kAccErr;
     return;
   }
   if (len == 0) {  // REF matcher.py:253-258: empty input records a history entry
-    int2 tops[kAccS];
-    int32_t refs[kAccS], nodes[kAccS];
-    const int nt = load_tops(P, slot, hd, tops);
-    for (int s = 0; s < nt; ++s) {
-      refs[s] = tops[s].x < 0 ? -1 : -2 - tops[s].x;
-      nodes[s] = tops[s].y;
+    const int2* tops;
+    const int nt = view_tops(P, slot, hd, &tops);
+    Chain c;
+    build_chain(c, nt > 0 ? tops[0].x : -1, nullptr, nullptr, 0, hd);
+    if (!push_tops(P, slot, rp, G, tops, nt, 0, c, nullptr)) {
+      slot_error(P, slot, kErrCap);
+      *accepted = kAccErr;
+      return;
     }
-    push_history(P, slot, rp, hd, G, nt, refs, nodes, 0, nullptr, nullptr, 0);
-    *accepted = 1;
+    *accepted = kAccOk;
     return;
   }
   const int acc = accept_one(P, slot, rp, hd, G, len, [&](int64_t b) { return __ldg(data + b); }, false, false, &hd);
-  if (acc) store_header_state(P, slot, hd);  // accept_one leaves the mirror's publish to the caller
+  if (acc & kAccOk) store_header_state(P, slot, hd);  // accept_one leaves the mirror's publish to the caller
   *accepted = (uint8_t)acc;
 }
 
 __global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32_t start, int32_t window) {
   if (threadIdx.x != 0) return;
+  release_wide(P, slot);
+  P.err[slot] = 0;
   P.binding[slot] = b;
   P.head[slot] = 0;
   P.hist_len[slot] = 0;
@@ -104,6 +107,7 @@ __global__ void recycle_kernel(DevPool P, const int32_t* __restrict__ slots, int
   const int32_t slot = slots[i];
   if (!(P.hdr[slot].flags & 1)) return;
   const DevBinding* b = P.binding[slot];
+  release_wide(P, slot);
   P.head[slot] = 0;
   P.hist_len[slot] = 0;
   int2* t = slot_tops(P, slot, 0);
@@ -119,7 +123,7 @@ __global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots, co
   const int32_t slot = slots[i], k = steps[i];
   const int32_t hl = P.hist_len[slot];
   if (k < 0 || k > hl) {  // REF matcher.py:313-314
-    atomicOr(P.err, 1u << GM_ERR_ROLLBACK);
+    slot_error(P, slot, 1u << GM_ERR_ROLLBACK);
     return;
   }
   if (k == 0) return;
@@ -127,7 +131,7 @@ __global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots, co
   P.head[slot] = h;
   P.hist_len[slot] = hl - k;
   const int32_t meta = P.meta[(size_t)slot * P.H + h];
-  write_header(P, slot, P.binding[slot], slot_tops(P, slot, h), meta & 0xFFFF, (meta >> 16) & 1);
+  write_header(P, slot, P.binding[slot], ring_tops(P, slot, h, meta & 0xFFFF), meta & 0xFFFF, (meta >> 16) & 1);
 }
 
 // info: n_stacks, terminated, history_len, terminable, window; stacks copy;
@@ -140,7 +144,7 @@ __global__ void slot_probe_kernel(DevPool P, int32_t slot, int32_t* info, int2* 
   const int32_t h = P.head[slot];
   const int32_t meta = P.meta[(size_t)slot * P.H + h];
   const int nt = meta & 0xFFFF;
-  const int2* tops = slot_tops(P, slot, h);
+  const int2* tops = ring_tops(P, slot, h, nt);
   int term = 0;
   uint32_t fb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int s = 0; s < nt; ++s) {
@@ -166,11 +170,32 @@ __global__ void slot_probe_kernel(DevPool P, int32_t slot, int32_t* info, int2* 
   for (int i = 0; i < 8; ++i) bytes8[i] = fb[i];
 }
 
-// branch / fork (REF matcher.py:328-355): copy the whole slot state.
+// branch / fork (REF matcher.py:328-355): copy the whole slot state (wide
+// ring entries get blocks of their own).
 __global__ void fork_kernel(DevPool P, int32_t src, int32_t dst) {
+  __shared__ int2* s_dst;
+  release_wide(P, dst, threadIdx.x, blockDim.x);
+  if (threadIdx.x == 0) P.err[dst] = 0;
+  __syncthreads();
   const size_t per = (size_t)P.H * P.max_stacks;
   for (size_t k = threadIdx.x; k < per; k += blockDim.x) P.tops[dst * per + k] = P.tops[src * per + k];
   for (int k = threadIdx.x; k < P.H; k += blockDim.x) P.meta[(size_t)dst * P.H + k] = P.meta[(size_t)src * P.H + k];
+  for (int h = 0; h < P.H; ++h) {
+    const int n = P.meta[(size_t)src * P.H + h] & 0xFFFF;
+    if (n <= P.max_stacks) continue;
+    if (threadIdx.x == 0) {
+      s_dst = ring_tops_w(P, dst, h, n);
+      if (!s_dst) {
+        slot_error(P, dst, kErrCap);
+        P.meta[(size_t)dst * P.H + h] = 0;
+      }
+    }
+    __syncthreads();
+    const int2* from = ring_tops(P, src, h, n);
+    if (s_dst)
+      for (int k = threadIdx.x; k < n; k += blockDim.x) s_dst[k] = from[k];
+    __syncthreads();
+  }
   if (threadIdx.x < kHdrVec)
     reinterpret_cast<int4*>(P.hdr + dst)[threadIdx.x] = reinterpret_cast<const int4*>(P.hdr + src)[threadIdx.x];
   if (threadIdx.x == 0) {
@@ -179,6 +204,19 @@ __global__ void fork_kernel(DevPool P, int32_t src, int32_t dst) {
     P.window[dst] = P.window[src];
     P.binding[dst] = P.binding[src];
   }
+}
+
+// Per-slot error words of `slots` (gathered; cleared with `clear`).
+__global__ void pool_errors_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ out,
+                                   int32_t clear) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t slot = slots[i];
+  if (slot < 0 || slot >= P.capacity) {
+    out[i] = kErrInvalid;
+    return;
+  }
+  out[i] = clear ? atomicExch(P.err + slot, 0u) : P.err[slot];
 }
 
 static gm_status set_smem_attr(const void* fn) {
@@ -227,6 +265,13 @@ gm_status launch_rollback(const DevPool& P, const int32_t* slots, const int32_t*
 gm_status launch_probe(const DevPool& P, int32_t slot, int32_t* info, int2* stacks, int32_t max_out,
                        uint32_t* bytes8, cudaStream_t s) {
   slot_probe_kernel<<<1, 32, 0, s>>>(P, slot, info, stacks, max_out, bytes8);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_pool_errors(const DevPool& P, const int32_t* slots, int32_t n, uint32_t* out, int32_t clear,
+                             cudaStream_t s) {
+  if (n <= 0) return GM_OK;
+  pool_errors_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(P, slots, n, out, clear);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

@@ -25,7 +25,7 @@ constexpr int kBuildS = 16;   // stacks per walk
 constexpr int kBuildF = 96;   // walker-local frames
 
 __global__ void __launch_bounds__(128)
-cache_build_kernel(DevGrammar G, DevVocab Vc, DevArena A, int32_t key_begin,
+cache_build_kernel(DevGrammar G, DevVocab Vc, DevArena A, DevOverflow O, int32_t key_begin,
                    uint32_t* __restrict__ acc_rows, uint32_t* __restrict__ dep_rows,
                    uint32_t* __restrict__ err_out) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -37,25 +37,53 @@ cache_build_kernel(DevGrammar G, DevVocab Vc, DevArena A, int32_t key_begin,
   const int len = __ldg(Vc.off + tid + 1) - o0;
   const uint8_t* tok = Vc.bytes + o0;
 
-  Walker<kBuildS, kBuildF> w;
-  w.reset();
-  w.add(-1, key_node);
   uint64_t pops = 0;     // bit d: popped past the frame before byte d
   bool far_pop = false;  // popped at depth >= 64 (treated as "allowed", sound)
-  for (int i = 0; i < len; ++i) {
-    if (w.nf > kBuildF / 2) w.intern_all(A);
-    bool pb = false;
-    const int alive = w.template step<kBuildS>(G, A, tok[i], &pb);
-    if (pb) {
-      if (i < 64) pops |= 1ull << i;
-      else far_pop = true;
+  bool alive_end = false;
+  uint32_t err = 0;
+  {
+    Walker<kBuildS, kBuildF> w;
+    w.reset();
+    w.add(-1, key_node);
+    for (int i = 0; i < len; ++i) {
+      if (w.nf > kBuildF / 2) w.intern_all(A);
+      bool pb = false;
+      const int alive = w.template step<kBuildS>(G, A, tok[i], &pb);
+      if (pb) {
+        if (i < 64) pops |= 1ull << i;
+        else far_pop = true;
+      }
+      if (!alive) break;
     }
-    if (!alive) break;
+    alive_end = w.n > 0;
+    err = w.err;
   }
-  if (w.err) atomicOr(err_out, w.err);
+  if (err & kErrCap) {
+    // more than kBuildS stacks (ambiguous grammar): redo the walk in the
+    // overflow tier, up to the reference's 4096-state cap (REF cache.py:
+    // 58, 137-138)
+    pops = 0;
+    far_pop = false;
+    BigWalk bw;
+    bw.acquire(O, (uint32_t)j * 7u + (uint32_t)k);
+    bw.start();
+    bw.add(-1, key_node);
+    for (int i = 0; i < len && bw.n > 0 && !bw.err; ++i) {
+      bool pb = false;
+      bw.step(G, A, tok[i], &pb);
+      if (pb) {
+        if (i < 64) pops |= 1ull << i;
+        else far_pop = true;
+      }
+    }
+    alive_end = bw.n > 0 && !bw.err;
+    err = bw.err;
+    bw.release();
+  }
+  if (err) atomicOr(err_out, err);
   const uint32_t bit = 1u << (tid & 31);
   const size_t word = (size_t)k * Vc.W + (tid >> 5);
-  if (w.n > 0) {
+  if (alive_end) {
     atomicOr(acc_rows + word, bit);
     return;
   }
@@ -242,7 +270,7 @@ __global__ void dep_context2_kernel(DevGrammar G, const int32_t* __restrict__ de
 using namespace gm;
 
 namespace gm {
-gm_status launch_cache_build(const DevGrammar& G, const DevVocab& V, const DevArena& A,
+gm_status launch_cache_build(const DevGrammar& G, const DevVocab& V, const DevArena& A, const DevOverflow& O,
                              int32_t key_begin, int32_t n, uint32_t* acc, uint32_t* dep,
                              uint32_t* err, cudaStream_t s) {
   if (n <= 0 || V.n_sorted == 0) return GM_OK;
@@ -250,7 +278,7 @@ gm_status launch_cache_build(const DevGrammar& G, const DevVocab& V, const DevAr
   for (int32_t k0 = 0; k0 < n; k0 += 65535) {
     const int32_t kn = (n - k0) < 65535 ? (n - k0) : 65535;
     dim3 grid((unsigned)ceil_div(V.n_sorted, threads), (unsigned)kn);
-    cache_build_kernel<<<grid, threads, 0, s>>>(G, V, A, key_begin + k0, acc + (size_t)k0 * V.W,
+    cache_build_kernel<<<grid, threads, 0, s>>>(G, V, A, O, key_begin + k0, acc + (size_t)k0 * V.W,
                                                 dep + (size_t)k0 * V.W, err);
     GM_LAUNCH_CHECK();
   }

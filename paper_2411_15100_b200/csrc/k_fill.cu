@@ -144,6 +144,162 @@ __device__ __forceinline__ void context_of(const DevPool& P, const SlotHdr& hd, 
   }
 }
 
+// General and overflow tiers of a dependent walk (rare: the register walker
+// spilled).  Walker (<= kDepS stacks, local frames) first, then BigWalk
+// (<= kWideCap stacks in the pool's global scratch lanes).  Both look frames
+// up by handle, so while a deferred commit's CASes may still be in flight
+// (K5) they walk a private copy of the chain rewritten to real handles.
+// Out of line: keeps the step kernels' executed code small.
+__device__ __noinline__ bool walk_dep_general(const DevPool* Pp, int32_t slot, const SlotHdr* hd,
+                                              const DevGrammar* Gp, int32_t th, int32_t node, int4 e, int4 inl,
+                                              const uint8_t* far, const SpecOut* spec, uint32_t* err_out) {
+  const DevPool& P = *Pp;
+  const DevGrammar& G = *Gp;
+  int32_t ch_h[kChain];
+  unsigned long long ch_k[kChain];
+  const int nc = hd->nchain;
+  for (int i = 0; i < nc; ++i) {
+    ch_h[i] = hd->chain_h[i];
+    ch_k[i] = hd->chain_k[i];
+  }
+  if (spec && spec->n > 0 && !spec_realize(P.arena, *spec, ch_h, ch_k, nc, &th)) {
+    *err_out |= kErrArena;
+    return false;
+  }
+  {
+    Walker<kDepS, kDepF> w;
+    w.reset();
+    w.external(ch_h, ch_k, nc);
+    w.add(th < 0 ? -1 : -2 - th, node);
+    for (int b = 0; b < e.y; ++b) {
+      if (w.nf > kDepF / 2) w.intern_all(P.arena);
+      bool pb = false;
+      if (!w.template step<kDepS>(G, P.arena, rec_byte(inl, far, b), &pb)) break;
+    }
+    if (!(w.err & kErrCap)) {
+      *err_out |= w.err;
+      return w.n > 0;
+    }
+  }
+  BigWalk bw;
+  bw.acquire(P.ovf, (uint32_t)slot * 131u + threadIdx.x);
+  bw.start();
+  bw.add(th, node);
+  for (int b = 0; b < e.y && bw.n > 0 && !bw.err; ++b) {
+    bool pb = false;
+    bw.step(G, P.arena, rec_byte(inl, far, b), &pb);
+  }
+  const bool ok = bw.n > 0 && !bw.err;
+  *err_out |= bw.err;
+  bw.release();
+  return ok;
+}
+
+// Resolve dependent record di of top t (context indices cj, cj2) into this
+// CTA's shared mask words: the context class when it decides, else a walk
+// against the request's full stack.
+__device__ __forceinline__ void resolve_dep(const DevPool& P, int32_t slot, const SlotHdr& hd, const DevGrammar& G,
+                                            int32_t di, const int4& e, int2 t, int cj, int cj2, uint32_t* dep_acc,
+                                            int32_t w_lo, int32_t tok_lo, int32_t tok_hi, const SpecOut* spec,
+                                            int* s_err) {
+  const int4* rec = hd.dep_ent + 2 * (size_t)di;
+  // two-level class word fetched alongside the record (not after it)
+  const uint32_t c2w = cj2 >= 0 ? __ldg(G.ctx2 + (size_t)di * kMaxCallers + cj) : 0u;
+  const int32_t tid = e.x;
+  if (tid < tok_lo || tid >= tok_hi) return;  // another split's token
+  uint32_t* acc_w = dep_acc + ((tid >> 5) - w_lo);
+  const uint32_t bit = 1u << (tid & 31);
+  if (*acc_w & bit) return;  // already allowed by another stack
+  if (cj >= 0) {
+    uint32_t cls = ((uint32_t)e.w >> (2 * cj)) & 3u;
+    if (cls == kCtxDeeper && cj2 >= 0)  // two-level class from the grandparent frame
+      cls = (c2w >> (2 * cj2)) & 3u;
+    if (cls == kCtxReject) return;
+    if (cls == kCtxAccept) {
+      atomicOr(acc_w, bit);
+      return;
+    }
+  }
+  const int4 inl = __ldg(rec + 1);
+  const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;  // bytes beyond the inline 16
+  // fast path: register walker; general / overflow walkers only on spill
+  RWalker<kDepR, kDepRF> rw;
+  rw.init(hd.chain_h, hd.chain_k, hd.nchain);
+  rw.add(rw.ref_of_handle(t.x), t.y);
+  for (int b = 0; b < e.y && rw.n > 0 && !rw.spill; ++b) {
+    bool pb = false;
+    rw.template step<true>(G, P.arena, rec_byte(inl, far, b), &pb);
+  }
+  bool ok;
+  uint32_t err = 0;
+  if (!rw.spill) {
+    err = rw.err;
+    ok = rw.n > 0;
+  } else {
+    ok = walk_dep_general(&P, slot, &hd, &G, t.x, t.y, e, inl, far, spec, &err);
+  }
+  if (err) {
+    slot_error(P, slot, err);
+    *s_err = 1;
+  }
+  if (ok) atomicOr(acc_w, bit);
+}
+
+// Request with more stacks than the fill's per-top arrays hold (wide ring
+// entry, up to kWideCap): rows and dependents are OR-ed into dep_acc batch
+// by batch (all threads; rare path, out of line).
+constexpr int kFillTops = 32;
+__device__ __noinline__ void wide_accumulate(const DevPool* Pp, int32_t slot, const SlotHdr* hdp, const DevGrammar* Gp,
+                                             uint32_t* dep_acc, int32_t w_lo, int32_t nw, const SpecOut* spec,
+                                             int* s_err) {
+  const DevPool& P = *Pp;
+  const SlotHdr& hd = *hdp;
+  const DevGrammar& G = *Gp;
+  __shared__ int32_t b_key[kFillTops], b_lo[kFillTops], b_hi[kFillTops];
+  __shared__ int2 b_top[kFillTops];
+  __shared__ int b_cj[kFillTops], b_cj2[kFillTops];
+  const int32_t head = P.head[slot];
+  const int ntw = P.meta[(size_t)slot * P.H + head] & 0xFFFF;
+  const int2* tops = ring_tops(P, slot, head, ntw);
+  const int32_t W = hd.W, tok_lo = w_lo * 32, tok_hi = (w_lo + nw) * 32;
+  for (int b0 = 0; b0 < ntw; b0 += kFillTops) {
+    const int nb = min(kFillTops, ntw - b0);
+    if ((int)threadIdx.x < nb) {
+      const int2 t = tops[b0 + threadIdx.x];
+      const int4 ni = G.node_info[t.y];
+      b_key[threadIdx.x] = ni.x;
+      b_lo[threadIdx.x] = ni.y;
+      b_hi[threadIdx.x] = ni.z;
+      b_top[threadIdx.x] = t;
+      int cj, cj2;
+      context_of(P, hd, G, t, cj, cj2);
+      b_cj[threadIdx.x] = cj;
+      b_cj2[threadIdx.x] = cj2;
+    }
+    __syncthreads();
+    for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) {
+      uint32_t a = dep_acc[w];
+      for (int s = 0; s < nb; ++s)
+        if (b_key[s] >= 0) a |= __ldg(hd.acc_rows + (size_t)b_key[s] * W + w_lo + w);
+      dep_acc[w] = a;
+    }
+    __syncthreads();
+    int total = 0;
+    for (int s = 0; s < nb; ++s) total += b_hi[s] - b_lo[s];
+    for (int32_t q = threadIdx.x; q < total; q += blockDim.x) {
+      int s = 0, base = 0;
+      while (q - base >= b_hi[s] - b_lo[s]) {
+        base += b_hi[s] - b_lo[s];
+        ++s;
+      }
+      const int32_t di = b_lo[s] + (q - base);
+      const int4 e = __ldg(hd.dep_ent + 2 * (size_t)di);
+      resolve_dep(P, slot, hd, G, di, e, b_top[s], b_cj[s], b_cj2[s], dep_acc, w_lo, tok_lo, tok_hi, spec, s_err);
+    }
+    __syncthreads();
+  }
+}
+
 // Grid: (requests, splits).  A request's mask is cut into `splits` word
 // ranges (multiples of 4 words, i.e. 128 tokens) and each CTA owns one: it
 // merges only its slice of the rows, walks only the dependents whose token
@@ -208,7 +364,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   __shared__ RingPos rp;
   __shared__ int4 s_rec[2];
-  __shared__ int s_just_term, s_dirty, s_walked, s_spec_bad;
+  __shared__ int s_just_term, s_dirty, s_walked, s_acc, s_err, s_wide;
   __shared__ SpecOut s_spec;  // K5: fresh frames whose interning is deferred (warp 2, checked at the end)
   int32_t tok = -1;
   const bool do_acc = ACCEPT && (SA.tokens || ptok);
@@ -255,7 +411,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
       s_spec.n = 0;
       const bool was_term = hd.flags & 1;
       if (!in_range) {  // REF matcher.py:278-279
-        atomicOr(P.err, kErrInvalid);
+        slot_error(P, slot, kErrInvalid);
+        acc = kAccErr;
       } else {
         const int4 e = s_rec[0], inl = s_rec[1];
         const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;
@@ -350,13 +507,14 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
         acc = accept_one(P, slot, rp, hd, Gs, e.y, [&](int64_t b) { return rec_byte(inl, far, (int)b); },
                          tok == hd.eos, e.x != 0, &hd, prefetch_rows, (kTimeline && P.trace) ? acc_ts : nullptr,
                          kDeferIntern ? &s_spec : nullptr);
-        if (!acc && s_pref >= 0) s_pref = -2;  // walked but not committed: state unchanged, rows stale
+        if (!(acc & kAccOk) && s_pref >= 0) s_pref = -2;  // walked but not committed: state unchanged, rows stale
       }
       SA.accepted[i] = (uint8_t)acc;
+      s_acc = acc;
       s_just_term = !was_term && (hd.flags & 1);
       const bool restart = SA.recycle && (hd.flags & 1);
       if (restart) restart_slot(P, slot, Gs, &hd);
-      s_dirty = acc || restart;
+      s_dirty = (acc & kAccOk) || restart;
       if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_acc));
       if (kTimeline && P.trace && i == 0) P.trace[48] = t_acc;
     }
@@ -382,9 +540,12 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   const unsigned setup_thread = blockDim.x > 96 ? 96u : 0u;
   if (threadIdx.x == setup_thread) {
     s_partial = 0;
+    s_wide = 0;
     int nt = hd.ntops;
     if (terminated) {  // a request that terminated in this very step gets an empty row, no error
-      if (split == 0 && !(do_acc && s_just_term)) atomicOr(P.err, kErrTerminated);
+      // (REF matcher.py:379-381: fill on a terminated matcher raises); K5's
+      // accept already reported a terminated slot
+      if (split == 0 && !do_acc) slot_error(P, slot, kErrTerminated);
       nt = 0;
     } else if (nt >= 0) {
       // issue the row copies first: they are the longest-latency loads
@@ -413,8 +574,12 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     } else {  // more stacks than the header holds: read the ring entry
       const int32_t h = P.head[slot];
       nt = P.meta[(size_t)slot * P.H + h] & 0xFFFF;
-      const int2* tops = slot_tops(P, slot, h);
+      const int2* tops = ring_tops(P, slot, h, nt);
       const DevGrammar Gg = blob_view(hd.blob);
+      if (nt > kFillTops) {  // wide set: accumulated batch by batch below
+        s_wide = 1;
+        nt = 0;
+      }
       for (int s = 0; s < nt; ++s) {
         const int4 ni = Gg.node_info[tops[s].y];
         s_key[s] = ni.x;
@@ -436,8 +601,16 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     s_cj2[st] = cj2;
   }
   for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) dep_acc[w] = 0u;
-  if (threadIdx.x == 0) s_walked = 0;
+  if (threadIdx.x == 0) {
+    s_walked = 0;
+    s_err = 0;
+  }
   __syncthreads();
+  const SpecOut* spec = do_acc ? &s_spec : nullptr;
+  if (s_wide) {
+    const DevGrammar Gw = do_acc ? Gs : hint_ok ? blob_view(tables) : stage_blob(hd.blob, hd.blob_bytes, tables);
+    wide_accumulate(&P, slot, &hd, &Gw, dep_acc, w_lo, nw, spec, &s_err);
+  }
   trace_mark(P, 1, 2);
   if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
   const int nt = s_nt;
@@ -467,7 +640,6 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     }
     trace_mark(P, 1, 4);
     if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ctx));
-    const uint8_t* rec_base = reinterpret_cast<const uint8_t*>(hd.tokrec);  // records' byte offsets are into it
     const int32_t tok_lo = w_lo * 32, tok_hi = w_hi * 32;
     // warp-major assignment: consecutive dependents go to different warps, so
     // a handful of walks run in parallel instead of diverging inside one warp
@@ -495,59 +667,16 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
         di_next = locate(q + blockDim.x, s_next);
         e_next = __ldg(hd.dep_ent + 2 * (size_t)di_next);
       }
-      const int4* rec = hd.dep_ent + 2 * (size_t)di;
-      // two-level class word fetched alongside the record (not after it)
-      const uint32_t c2w = s_cj2[s] >= 0 ? __ldg(G.ctx2 + (size_t)di * kMaxCallers + s_cj[s]) : 0u;
-      const int32_t tid = e.x;
-      if (tid < tok_lo || tid >= tok_hi) continue;  // another split's token
-      uint32_t* acc_w = dep_acc + ((tid >> 5) - w_lo);
-      const uint32_t bit = 1u << (tid & 31);
-      if (*acc_w & bit) continue;  // already allowed by another stack
-      if (s_cj[s] >= 0) {
-        uint32_t cls = ((uint32_t)e.w >> (2 * s_cj[s])) & 3u;
-        if (cls == kCtxDeeper && s_cj2[s] >= 0)  // two-level class from the grandparent frame
-          cls = (c2w >> (2 * s_cj2[s])) & 3u;
-        if (cls == kCtxReject) continue;
-        if (cls == kCtxAccept) {
-          atomicOr(acc_w, bit);
-          continue;
-        }
-      }
-      if (kTimeline && P.trace) atomicAdd(&s_walked, 1 | (e.y << 16));  // diagnostics: walks, bytes walked
-      const int4 inl = __ldg(rec + 1);
-      const int2 t = s_top[s];
-      const uint8_t* far = rec_base + e.z;  // bytes beyond the inline 16
-      // fast path: register walker; general walker only on spill
-      RWalker<kDepR, kDepRF> rw;
-      rw.init(hd.chain_h, hd.chain_k, hd.nchain);
-      rw.add(rw.ref_of_handle(t.x), t.y);
-      for (int b = 0; b < e.y && rw.n > 0 && !rw.spill; ++b) {
-        bool pb = false;
-        rw.template step<true>(G, P.arena, rec_byte(inl, far, b), &pb);
-      }
-      bool ok;
-      if (!rw.spill) {
-        if (rw.err) atomicOr(P.err, rw.err);
-        ok = rw.n > 0;
-      } else {
-        Walker<kDepS, kDepF> w;
-        w.reset();
-        w.external(hd.chain_h, hd.chain_k, hd.nchain);
-        w.add(t.x < 0 ? -1 : -2 - t.x, t.y);
-        for (int b = 0; b < e.y; ++b) {
-          if (w.nf > kDepF / 2) w.intern_all(P.arena);
-          bool pb = false;
-          if (!w.template step<kDepS>(G, P.arena, rec_byte(inl, far, b), &pb)) break;
-        }
-        if (w.err) atomicOr(P.err, w.err);
-        ok = w.n > 0;
-      }
-      if (ok) atomicOr(acc_w, bit);
+      if (kTimeline && P.trace) atomicAdd(&s_walked, 1 | (e.y << 16));  // diagnostics: visits, bytes
+      resolve_dep(P, slot, hd, G, di, e, s_top[s], s_cj[s], s_cj2[s], dep_acc, w_lo, tok_lo, tok_hi, spec, &s_err);
     }
   }
   trace_mark(P, 1, 5);
   __syncthreads();
   trace_mark(P, 1, 6);
+  // a walk error this step: the request's flag says so (bit 1) next to
+  // whether its token was accepted (bit 0); the slot's error word says which
+  if (do_acc && threadIdx.x == 0 && s_err) SA.accepted[i] = (uint8_t)(s_acc | kAccErr);
   if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_walks));
 
   // Merge and store this CTA's words.
@@ -602,14 +731,17 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     __syncthreads();
     if (need_apply && threadIdx.x == 0) need_apply[i] = (uint8_t)s_partial;  // launched with one split
   }
-  if (APPLY && s_partial) {
+  // an all-allowed row still masks logits columns in [V, vocab) (their bits
+  // are zero, as gm_apply_inplace treats them)
+  if (APPLY && (s_partial || ap_vocab > (int64_t)hd.V)) {
     const int64_t vocab = ap_vocab < (int64_t)W * 32 ? ap_vocab : (int64_t)W * 32;
     const int64_t t_lo = (int64_t)w_lo * 32, t_hi = (int64_t)w_hi * 32 < vocab ? (int64_t)w_hi * 32 : vocab;
     if (t_hi > t_lo) apply_row(logits + row * lstride_bytes, dep_acc, t_lo, t_hi, ap_eb, ap_neg);
   }
   if (do_acc && threadIdx.x >= 64 && threadIdx.x < 96 && s_spec.n > 0) {  // warp 2: verify the deferred commit
     const bool bad = spec_mine && spec_old != kEmptyKey && spec_old != s_spec.key[spec_lane];
-    if (__any_sync(0xFFFFFFFFu, bad) && threadIdx.x == 64) spec_fixup(P, slot, s_spec, hd);
+    if (__any_sync(0xFFFFFFFFu, bad) && threadIdx.x == 64 && !spec_fixup(P, slot, s_spec, hd))
+      SA.accepted[i] = (uint8_t)(s_acc | kAccErr);
   }
   if (kTimeline && P.trace && threadIdx.x == 0) {
     unsigned long long t1;

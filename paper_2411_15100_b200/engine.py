@@ -25,12 +25,35 @@ from .automaton import AutomatonOptions, CompiledTables, StateLimitError, build_
 from .grammar import parse_grammar
 from .vocab import Vocabulary
 
-__all__ = ["MatcherError", "DeviceVocab", "DeviceGrammar", "DeviceCache", "CompiledDeviceGrammar",
+__all__ = ["MatcherError", "RequestErrors", "DeviceVocab", "DeviceGrammar", "DeviceCache", "CompiledDeviceGrammar",
            "MatcherPool", "compile_on_device", "get_pool"]
 
 
 class MatcherError(RuntimeError):
     """Runtime matcher misuse (REF matcher.py:35-36)."""
+
+
+class RequestErrors(MatcherError):
+    """Several requests of one batched call failed; ``errors`` maps the
+    request's index in the batch to its MatcherError."""
+
+    def __init__(self, errors: dict):
+        self.errors = errors
+        super().__init__("; ".join(f"request {i}: {e}" for i, e in sorted(errors.items())))
+
+
+def error_for_status(status: int) -> Exception:
+    """MatcherError for a device-side matcher status (REF matcher.py:35-36,
+    188-189, 276-277, 313-314, 379-381); GmaskError otherwise."""
+    msg = _lib.load().gm_last_error().decode(errors="replace")
+    if status in (_lib.GM_ERR_STATE_CAP, _lib.GM_ERR_TERMINATED, _lib.GM_ERR_ROLLBACK, _lib.GM_ERR_INVALID,
+                  _lib.GM_ERR_ARENA_FULL):
+        return MatcherError(msg)
+    return _lib.GmaskError(status, msg)
+
+
+def error_for_bits(bits: int) -> Exception:
+    return error_for_status(_lib.load().gm_status_of_error_bits(C.c_uint32(bits)))
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -255,15 +278,38 @@ class MatcherPool:
             self._free.append(slot)
 
     def check(self, runtime: bool = True):
-        """Raise the sticky device error, if any (syncs)."""
+        """Raise the OR of every slot's sticky error, clearing them all (syncs).
+        Pool-wide diagnostic: per-request errors use ``slot_errors``."""
         flags = C.c_int32()
         status = _lib.load().gm_pool_check(self.handle, C.byref(flags))
         if status != _lib.GM_OK:
-            msg = _lib.load().gm_last_error().decode()
-            if status in (_lib.GM_ERR_STATE_CAP, _lib.GM_ERR_TERMINATED, _lib.GM_ERR_ROLLBACK,
-                          _lib.GM_ERR_INVALID, _lib.GM_ERR_ARENA_FULL):
-                raise MatcherError(msg)
-            _lib.check(status, "matcher")
+            raise error_for_status(status)
+
+    def slot_errors(self, slots: torch.Tensor, clear: bool = True) -> np.ndarray:
+        """Per-slot error words (uint32, bit 1 << GM_ERR_*) of ``slots``
+        (int32 CUDA tensor), cleared by the read.  Syncs the current stream."""
+        out = torch.empty(slots.numel(), dtype=torch.int32, device=slots.device)
+        _lib.check(_lib.load().gm_pool_errors(self.handle, slots.data_ptr(), slots.numel(), out.data_ptr(),
+                                               1 if clear else 0, _lib.stream_ptr()), "gm_pool_errors")
+        return out.cpu().numpy().view(np.uint32)
+
+    def raise_slot_errors(self, slots: torch.Tensor, flags: Optional[np.ndarray] = None):
+        """Raise for the requests among ``slots`` whose device operation
+        failed (REF raises MatcherError on that matcher, matcher.py:188-189,
+        379-381).  With ``flags`` (K4/K5 accepted flags, bit 1 = error) only
+        a flagged batch pays the read.  One request: its MatcherError; more:
+        RequestErrors carrying each request's exception."""
+        if flags is not None and not (np.asarray(flags) & 2).any():
+            return
+        words = self.slot_errors(slots)
+        bad = {i: error_for_bits(int(w)) for i, w in enumerate(words) if w}
+        if not bad:
+            return
+        if len(bad) == 1:
+            (i, exc), = bad.items()
+            exc.request_index = i
+            raise exc
+        raise RequestErrors(bad)
 
     def __del__(self):
         if getattr(self, "handle", None) is not None and _lib._lib is not None:

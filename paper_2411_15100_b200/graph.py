@@ -43,6 +43,9 @@ class DecodeStepGraph:
         dev = pool.device
         B = len(matchers)
         self.B = B
+        # the graph replays raw slot ids: keep the matchers (and so their
+        # slots) alive for the graph's lifetime
+        self._matchers = list(matchers)
         self.slots = torch.tensor([m.slot for m in matchers], dtype=torch.int32, device=dev)
         n = len(logits)
         # per logits buffer: its own pinned staging (token ids in, accepted
@@ -109,6 +112,9 @@ class DecodeStepGraph:
             self.done[i].record(self.stream)
         if wait:
             self.stream.synchronize()
+            flags = self.accepted_host[i].numpy()
+            if (flags & 2).any():  # bit 1: that request's step failed
+                get_pool().raise_slot_errors(self.slots, flags)
         return self.accepted_host[i]
 
 
@@ -137,6 +143,10 @@ class DecodeLoop:
         dev = pool.device
         n_buf = len(logits)
         self.B = len(matchers)
+        # the native decoder steps raw slot ids: keep the matchers (and so
+        # their slots) alive until close()
+        self._matchers = list(matchers)
+        self._pool = pool
         self.slots = torch.tensor([m.slot for m in matchers], dtype=torch.int32, device=dev)
         self.bitmasks = list(bitmask) if isinstance(bitmask, (list, tuple)) else [bitmask] * n_buf
         self.logits = list(logits)
@@ -174,18 +184,26 @@ class DecodeLoop:
         if st:
             self._check(st, "gm_decoder_step")
 
-    def flags(self, i: int = 0, out: Optional[np.ndarray] = None, wait: bool = True) -> np.ndarray:
-        """Accepted flags (uint8 [B]) of buffer i's latest step."""
+    def flags(self, i: int = 0, out: Optional[np.ndarray] = None, wait: bool = True,
+              raise_errors: bool = True) -> np.ndarray:
+        """Accepted flags (uint8 [B]) of buffer i's latest step: bit 0 =
+        token accepted, bit 1 = the request's step failed (cap, terminated,
+        arena...).  With ``raise_errors`` a failed request raises its
+        MatcherError (RequestErrors for several, each keyed by its index in
+        the batch); an error-free step costs nothing extra."""
         o = self._flags if out is None else out
         st = self._lib.gm_decoder_flags(self._h, i, o.ctypes.data, 1 if wait else 0)
         if st:
             self._check(st, "gm_decoder_flags")
+        if raise_errors and (o & 2).any():
+            self._pool.raise_slot_errors(self.slots, o)
         return o
 
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._lib.gm_decoder_release(self._h)
             self._h = None
+        self._matchers = []
 
     def __del__(self):
         try:

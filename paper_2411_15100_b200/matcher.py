@@ -21,9 +21,9 @@ import torch
 
 from . import _lib
 from .bitmask import apply_token_bitmask_inplace  # noqa: F401  (re-export)
-from .engine import MatcherError, MatcherPool, get_pool
+from .engine import MatcherError, MatcherPool, RequestErrors, get_pool
 
-__all__ = ["SlotMatcher", "GrammarMatcher", "BatchGrammarMatcher", "MatcherError"]
+__all__ = ["SlotMatcher", "GrammarMatcher", "BatchGrammarMatcher", "MatcherError", "RequestErrors"]
 
 
 class SlotMatcher:
@@ -98,26 +98,30 @@ class SlotMatcher:
             mask |= int(words[i]) << (32 * i)
         return mask, bool(term.value)
 
+    def check(self):
+        """Raise this matcher's own device error, if any (syncs; clears it)."""
+        self.pool.raise_slot_errors(self._slot_t)
+
     # -- stepping -----------------------------------------------------------------
     def accept_token(self, tid: int) -> bool:
-        """Device accept; raises MatcherError on a sticky device error
-        (terminated / cap / range)."""
+        """Device accept; False = rejected (state unchanged); raises this
+        matcher's MatcherError on a device error (terminated / cap / range)."""
         self._tok_t.fill_(int(tid))
         _lib.check(_lib.load().gm_accept_tokens(self.pool.handle, self._slot_t.data_ptr(), self._tok_t.data_ptr(), 1,
                                                  self._out_t.data_ptr(), _lib.stream_ptr()), "gm_accept_tokens")
-        ok = bool(self._out_t.item())
-        if not ok:
-            self.pool.check()
-        return ok
+        flag = int(self._out_t.item())
+        if flag & 2:
+            self.check()
+        return bool(flag & 1)
 
     def accept_bytes(self, data: bytes) -> bool:
         buf = np.frombuffer(bytes(data), dtype=np.uint8) if data else np.zeros(1, np.uint8)
         _lib.check(_lib.load().gm_accept_bytes(self.pool.handle, self.slot, buf.ctypes.data, len(data),
                                                 self._out_t.data_ptr(), _lib.stream_ptr()), "gm_accept_bytes")
-        ok = bool(self._out_t.item())
-        if not ok:
-            self.pool.check()
-        return ok
+        flag = int(self._out_t.item())
+        if flag & 2:
+            self.check()
+        return bool(flag & 1)
 
     def fill_row(self, bitmask: torch.Tensor, index: int = 0, need_apply: bool = True) -> Optional[bool]:
         """K2 for this slot into bitmask[index] (CUDA int32 2-D)."""
@@ -133,7 +137,7 @@ class SlotMatcher:
         steps_t = torch.tensor([int(steps)], dtype=torch.int32, device=self.pool.device)
         _lib.check(_lib.load().gm_rollback(self.pool.handle, self._slot_t.data_ptr(), steps_t.data_ptr(), 1,
                                             _lib.stream_ptr()), "gm_rollback")
-        self.pool.check()
+        self.check()
 
     def jump_forward(self, max_len: int = 4096) -> bytes:
         """Longest forced byte string (REF matcher.py:464-486); state unchanged."""
@@ -214,7 +218,7 @@ class GrammarMatcher:
             tmp = torch.empty((1, bitmask.shape[1]), dtype=torch.int32, device=self._core.pool.device)
             need = self._core.fill_row(tmp, 0)
             bitmask[index].copy_(tmp[0])
-        self._core.pool.check()  # terminated matcher -> MatcherError (REF matcher.py:379-381)
+        self._core.check()  # this matcher's error: terminated -> MatcherError (REF matcher.py:379-381)
         return bool(need)
 
     def find_jump_forward_string(self) -> str:
@@ -269,7 +273,13 @@ class BatchGrammarMatcher:
         return t
 
     def batch_fill_next_token_bitmask(self, matchers: Sequence[GrammarMatcher], bitmask: torch.Tensor,
-                                      indices: Optional[Sequence[int]] = None, debug_print: bool = False) -> None:
+                                      indices: Optional[Sequence[int]] = None, debug_print: bool = False,
+                                      check_errors: bool = True) -> None:
+        """K2 over the batch.  With ``check_errors`` (default, the reference's
+        behaviour) a request whose fill failed raises its MatcherError
+        (RequestErrors for several; syncs); ``check_errors=False`` keeps the
+        call sync-free and leaves the errors in the slots' error words
+        (``check_errors(matchers)``)."""
         if not matchers:
             return
         if bitmask.device.type != "cuda" or bitmask.dtype != torch.int32 or bitmask.dim() != 2:
@@ -277,7 +287,17 @@ class BatchGrammarMatcher:
         rows = None
         if indices is not None:
             rows = torch.as_tensor(list(indices), dtype=torch.int32).to(bitmask.device, non_blocking=True)
-        batch_fill(get_pool(), self._slots(matchers), bitmask, rows)
+        slots = self._slots(matchers)
+        batch_fill(get_pool(), slots, bitmask, rows)
+        if check_errors:
+            get_pool().raise_slot_errors(slots)
+
+    def check_errors(self, matchers: Sequence[GrammarMatcher], flags=None) -> None:
+        """Raise the device errors of ``matchers`` (per request; syncs).
+        ``flags``: the accepted flags of a batch_step (bit 1 = error), so an
+        error-free batch costs nothing beyond reading them."""
+        if matchers:
+            get_pool().raise_slot_errors(self._slots(matchers), flags)
 
     def batch_fill_and_apply(self, matchers: Sequence[GrammarMatcher], logits: torch.Tensor,
                              bitmask: Optional[torch.Tensor] = None, vocab_size: Optional[int] = None) -> None:
@@ -313,8 +333,9 @@ class BatchGrammarMatcher:
         pool = get_pool()
         slots = torch.tensor([m.slot for m in matchers], dtype=torch.int32, device=pool.device)
         toks = torch.tensor(list(tokens), dtype=torch.int32, device=pool.device)
-        out = batch_accept(pool, slots, toks)
-        return [bool(x) for x in out.cpu().tolist()]
+        flags = batch_accept(pool, slots, toks).cpu().numpy()
+        pool.raise_slot_errors(slots, flags)  # per-request MatcherError (bit 1 = error)
+        return [bool(x & 1) for x in flags.tolist()]
 
 
 def batch_fill(pool: MatcherPool, slots: torch.Tensor, bitmask: torch.Tensor, rows: Optional[torch.Tensor] = None,

@@ -150,6 +150,8 @@ def load() -> C.CDLL:
         raise ImportError(f"libgmask.so not built at {LIB_PATH}; run paper_2411_15100_b200/build.py")
     lib = C.CDLL(str(LIB_PATH))
     for name, (args, res) in _SIGNATURES.items():
+        if os.environ.get("GMASK_LIB") and not hasattr(lib, name):
+            continue  # diagnostics: an older library variant (tools/ab_libs.sh)
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res

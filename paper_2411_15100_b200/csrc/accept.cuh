@@ -88,6 +88,7 @@ __device__ inline bool push_tops(const DevPool& P, int32_t slot, const RingPos& 
   const int32_t nh = (rp.head + 1) % P.H;
   int2* dst = ring_tops_w(P, slot, nh, nt);
   if (!dst) return false;
+  if (nt > P.max_stacks) (mirror ? mirror : &P.hdr[slot])->wide_owned = 1;
   if (dst != tops)
     for (int s = 0; s < nt; ++s) dst[s] = tops[s];
   P.meta[(size_t)slot * P.H + nh] = nt | (terminated << 16);
@@ -105,7 +106,10 @@ __device__ inline bool push_tops(const DevPool& P, int32_t slot, const RingPos& 
 // Restart a slot at the grammar's start state (recycle_kernel semantics)
 // from inside a step kernel: ring entry 0, empty history, header state.
 __device__ inline void restart_slot(const DevPool& P, int32_t slot, const DevGrammar& G, SlotHdr* mirror) {
-  release_wide(P, slot);
+  if (mirror->wide_owned) {
+    release_wide(P, slot);
+    mirror->wide_owned = 0;
+  }
   P.head[slot] = 0;
   P.hist_len[slot] = 0;
   const int2 t0 = make_int2(-1, G.start_node);
@@ -132,7 +136,12 @@ __device__ inline bool push_history(const DevPool& P, int32_t slot, const RingPo
 // surviving set is written as the next ring entry.  Returns accept_one's
 // result code.
 template <class ByteFn>
-__device__ inline int accept_wide(const DevPool& P, int32_t slot, const RingPos& rp, const DevGrammar& G,
+#ifdef GM_ACC_WIDE_NOINLINE
+__device__ __noinline__ int accept_wide(
+#else
+__device__ inline int accept_wide(
+#endif
+    const DevPool& P, int32_t slot, const RingPos& rp, const DevGrammar& G,
                                   const int2* tops, int ntops, int64_t len, ByteFn byte, SlotHdr* mirror) {
   BigWalk bw;
   bw.acquire(P.ovf, (uint32_t)slot);

@@ -874,7 +874,8 @@ struct __align__(16) SlotHdr {
   // ancestor-chain cache: arena keys of the tops' chain frames (top 0's chain
   // first), so walks pop through the first kChain frames without touching
   // the arena
-  int32_t nchain, pad0;
+  int32_t nchain;
+  int32_t wide_owned;          // 1: some ring entry of the slot holds a wide block (release on restart)
   int32_t chain_h[kChain];
   int32_t pad1[2];
   unsigned long long chain_k[kChain];
@@ -1332,9 +1333,10 @@ __device__ inline bool spec_fixup(const DevPool& P, int32_t slot, const SpecOut&
 
 // Rebuild a slot header from the binding (reset / recycle / rollback path).
 __device__ inline void write_header(const DevPool& P, int32_t slot, const DevBinding* B, const int2* tops, int n,
-                                    int terminated) {
+                                    int terminated, int wide_owned) {
   SlotHdr h;
   header_pointers(h, B);
+  h.wide_owned = wide_owned;
   const DevGrammar G = blob_view(B->c.blob);
   header_state(P, h, G, tops, n, terminated, nullptr);
   store_header(P, slot, h);

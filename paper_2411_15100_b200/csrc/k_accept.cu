@@ -94,7 +94,7 @@ __global__ void reset_kernel(DevPool P, int32_t slot, const DevBinding* b, int32
   int2* t = slot_tops(P, slot, 0);
   t[0] = make_int2(-1, start);
   P.meta[(size_t)slot * P.H] = 1;
-  write_header(P, slot, b, t, 1, 0);
+  write_header(P, slot, b, t, 1, 0, 0);
 }
 
 // Request recycling for serving loops: a terminated slot restarts at the
@@ -107,13 +107,13 @@ __global__ void recycle_kernel(DevPool P, const int32_t* __restrict__ slots, int
   const int32_t slot = slots[i];
   if (!(P.hdr[slot].flags & 1)) return;
   const DevBinding* b = P.binding[slot];
-  release_wide(P, slot);
+  if (P.hdr[slot].wide_owned) release_wide(P, slot);
   P.head[slot] = 0;
   P.hist_len[slot] = 0;
   int2* t = slot_tops(P, slot, 0);
   t[0] = make_int2(-1, b->g.start_node);
   P.meta[(size_t)slot * P.H] = 1;
-  write_header(P, slot, b, t, 1, 0);
+  write_header(P, slot, b, t, 1, 0, 0);
 }
 
 __global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots, const int32_t* __restrict__ steps,
@@ -131,7 +131,8 @@ __global__ void rollback_kernel(DevPool P, const int32_t* __restrict__ slots, co
   P.head[slot] = h;
   P.hist_len[slot] = hl - k;
   const int32_t meta = P.meta[(size_t)slot * P.H + h];
-  write_header(P, slot, P.binding[slot], ring_tops(P, slot, h, meta & 0xFFFF), meta & 0xFFFF, (meta >> 16) & 1);
+  write_header(P, slot, P.binding[slot], ring_tops(P, slot, h, meta & 0xFFFF), meta & 0xFFFF, (meta >> 16) & 1,
+               P.hdr[slot].wide_owned);
 }
 
 // info: n_stacks, terminated, history_len, terminable, window; stacks copy;

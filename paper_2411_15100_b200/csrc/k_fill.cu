@@ -149,8 +149,12 @@ __device__ __forceinline__ void context_of(const DevPool& P, const SlotHdr& hd, 
 // (<= kWideCap stacks in the pool's global scratch lanes).  Both look frames
 // up by handle, so while a deferred commit's CASes may still be in flight
 // (K5) they walk a private copy of the chain rewritten to real handles.
-// Out of line: keeps the step kernels' executed code small.
-__device__ __noinline__ bool walk_dep_general(const DevPool* Pp, int32_t slot, const SlotHdr* hd,
+#ifdef GM_DEP_GENERAL_NOINLINE  // measured: the call ABI costs ~3 us/step (K5, JSON)
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+bool walk_dep_general(const DevPool* Pp, int32_t slot, const SlotHdr* hd,
                                               const DevGrammar* Gp, int32_t th, int32_t node, int4 e, int4 inl,
                                               const uint8_t* far, const SpecOut* spec, uint32_t* err_out) {
   const DevPool& P = *Pp;
@@ -181,6 +185,10 @@ __device__ __noinline__ bool walk_dep_general(const DevPool* Pp, int32_t slot, c
       return w.n > 0;
     }
   }
+#ifdef GM_DIAG_NO_DEP_BIGWALK
+  *err_out |= kErrCap;
+  return false;
+#endif
   BigWalk bw;
   bw.acquire(P.ovf, (uint32_t)slot * 131u + threadIdx.x);
   bw.start();
@@ -245,59 +253,26 @@ __device__ __forceinline__ void resolve_dep(const DevPool& P, int32_t slot, cons
   if (ok) atomicOr(acc_w, bit);
 }
 
-// Request with more stacks than the fill's per-top arrays hold (wide ring
-// entry, up to kWideCap): rows and dependents are OR-ed into dep_acc batch
-// by batch (all threads; rare path, out of line).
-constexpr int kFillTops = 32;
-__device__ __noinline__ void wide_accumulate(const DevPool* Pp, int32_t slot, const SlotHdr* hdp, const DevGrammar* Gp,
-                                             uint32_t* dep_acc, int32_t w_lo, int32_t nw, const SpecOut* spec,
-                                             int* s_err) {
-  const DevPool& P = *Pp;
-  const SlotHdr& hd = *hdp;
-  const DevGrammar& G = *Gp;
-  __shared__ int32_t b_key[kFillTops], b_lo[kFillTops], b_hi[kFillTops];
-  __shared__ int2 b_top[kFillTops];
-  __shared__ int b_cj[kFillTops], b_cj2[kFillTops];
-  const int32_t head = P.head[slot];
-  const int ntw = P.meta[(size_t)slot * P.H + head] & 0xFFFF;
-  const int2* tops = ring_tops(P, slot, head, ntw);
-  const int32_t W = hd.W, tok_lo = w_lo * 32, tok_hi = (w_lo + nw) * 32;
-  for (int b0 = 0; b0 < ntw; b0 += kFillTops) {
-    const int nb = min(kFillTops, ntw - b0);
-    if ((int)threadIdx.x < nb) {
-      const int2 t = tops[b0 + threadIdx.x];
-      const int4 ni = G.node_info[t.y];
-      b_key[threadIdx.x] = ni.x;
-      b_lo[threadIdx.x] = ni.y;
-      b_hi[threadIdx.x] = ni.z;
-      b_top[threadIdx.x] = t;
-      int cj, cj2;
-      context_of(P, hd, G, t, cj, cj2);
-      b_cj[threadIdx.x] = cj;
-      b_cj2[threadIdx.x] = cj2;
-    }
-    __syncthreads();
-    for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) {
-      uint32_t a = dep_acc[w];
-      for (int s = 0; s < nb; ++s)
-        if (b_key[s] >= 0) a |= __ldg(hd.acc_rows + (size_t)b_key[s] * W + w_lo + w);
-      dep_acc[w] = a;
-    }
-    __syncthreads();
-    int total = 0;
-    for (int s = 0; s < nb; ++s) total += b_hi[s] - b_lo[s];
-    for (int32_t q = threadIdx.x; q < total; q += blockDim.x) {
-      int s = 0, base = 0;
-      while (q - base >= b_hi[s] - b_lo[s]) {
-        base += b_hi[s] - b_lo[s];
-        ++s;
-      }
-      const int32_t di = b_lo[s] + (q - base);
-      const int4 e = __ldg(hd.dep_ent + 2 * (size_t)di);
-      resolve_dep(P, slot, hd, G, di, e, b_top[s], b_cj[s], b_cj2[s], dep_acc, w_lo, tok_lo, tok_hi, spec, s_err);
-    }
-    __syncthreads();
+constexpr int kFillTops = 32;  // tops per pass of the fill's per-top arrays (wide sets: several passes)
+
+// Tops b0 .. b0+kFillTops of the slot's current ring entry into the fill's
+// per-top arrays (key, dependent range, top); returns how many.
+__device__ __forceinline__ int load_ring_tops(const DevPool& P, int32_t slot, const SlotHdr& hd, int b0, int32_t* key,
+                                              int32_t* lo, int32_t* hi, int2* top) {
+  const int32_t h = P.head[slot];
+  const int n = P.meta[(size_t)slot * P.H + h] & 0xFFFF;
+  const int2* tops = ring_tops(P, slot, h, n);
+  const DevGrammar Gg = blob_view(hd.blob);
+  const int nb = min(kFillTops, n - b0);
+  for (int s = 0; s < nb; ++s) {
+    const int2 t = tops[b0 + s];
+    const int4 ni = Gg.node_info[t.y];
+    key[s] = ni.x;
+    lo[s] = ni.y;
+    hi[s] = ni.z;
+    top[s] = t;
   }
+  return nb;
 }
 
 // Grid: (requests, splits).  A request's mask is cut into `splits` word
@@ -574,19 +549,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     } else {  // more stacks than the header holds: read the ring entry
       const int32_t h = P.head[slot];
       nt = P.meta[(size_t)slot * P.H + h] & 0xFFFF;
-      const int2* tops = ring_tops(P, slot, h, nt);
-      const DevGrammar Gg = blob_view(hd.blob);
-      if (nt > kFillTops) {  // wide set: accumulated batch by batch below
-        s_wide = 1;
-        nt = 0;
-      }
-      for (int s = 0; s < nt; ++s) {
-        const int4 ni = Gg.node_info[tops[s].y];
-        s_key[s] = ni.x;
-        s_lo[s] = ni.y;
-        s_hi[s] = ni.z;
-        s_top[s] = tops[s];
-      }
+      if (nt > kFillTops) s_wide = nt;  // wide set: kFillTops tops per pass below
+      nt = load_ring_tops(P, slot, hd, 0, s_key, s_lo, s_hi, s_top);
     }
     s_nt = nt;
   }
@@ -607,18 +571,18 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   }
   __syncthreads();
   const SpecOut* spec = do_acc ? &s_spec : nullptr;
-  if (s_wide) {
-    const DevGrammar Gw = do_acc ? Gs : hint_ok ? blob_view(tables) : stage_blob(hd.blob, hd.blob_bytes, tables);
-    wide_accumulate(&P, slot, &hd, &Gw, dep_acc, w_lo, nw, spec, &s_err);
-  }
   trace_mark(P, 1, 2);
   if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_setup));
-  const int nt = s_nt;
+  int nt = s_nt;
   const bool tma = pref >= 0 || (vec && hd.ntops >= 0 && nt <= kTmaRows && nw > 0 && !terminated && pref == -1);
   if (pref == -2) mbar_wait(&rows_bar, 0);  // drain the stale prefetch before leaving
 
   trace_mark(P, 1, 3);
+  // one pass over the tops' dependents — several for a wide set (more than
+  // kFillTops stacks), each OR-ing its tops' rows into dep_acc
   int total = 0;
+  for (int b0 = 0;;) {
+  total = 0;
   for (int s = 0; s < nt; ++s) total += s_hi[s] - s_lo[s];
   if (kTimeline && P.trace && i == 0 && split == 0 && threadIdx.x == 0) {
     P.trace[16 + 8] = (unsigned long long)total;
@@ -670,6 +634,25 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
       if (kTimeline && P.trace) atomicAdd(&s_walked, 1 | (e.y << 16));  // diagnostics: visits, bytes
       resolve_dep(P, slot, hd, G, di, e, s_top[s], s_cj[s], s_cj2[s], dep_acc, w_lo, tok_lo, tok_hi, spec, &s_err);
     }
+  }
+  if (!s_wide) break;
+  // wide set: this pass's rows into dep_acc, then the next kFillTops tops
+  __syncthreads();
+  for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) {
+    uint32_t a = dep_acc[w];
+    for (int s = 0; s < nt; ++s)
+      if (s_key[s] >= 0) a |= __ldg(hd.acc_rows + (size_t)s_key[s] * W + w_lo + w);
+    dep_acc[w] = a;
+  }
+  b0 += kFillTops;
+  __syncthreads();
+  if (b0 >= s_wide) {
+    nt = 0;  // every row is in dep_acc already
+    break;
+  }
+  if (threadIdx.x == setup_thread) s_nt = load_ring_tops(P, slot, hd, b0, s_key, s_lo, s_hi, s_top);
+  __syncthreads();
+  nt = s_nt;
   }
   trace_mark(P, 1, 5);
   __syncthreads();

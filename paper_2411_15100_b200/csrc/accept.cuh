@@ -29,6 +29,9 @@ constexpr int kAccRF = GM_ACC_RF;  // its walker-local frames
 // accept_one results: bit 0 = accepted, bit 1 = error (the slot's error
 // word says which; the state is unchanged)
 constexpr int kAccOk = 1, kAccErr = 2;
+#ifndef GM_ACC_MICRO
+#define GM_ACC_MICRO 0  // measured: K5 b2b +0.8 us (code layout), cold -1.8 us
+#endif
 
 // Current (handle, node) set of a slot: from the header when it fits, else
 // from the ring (inline entry or its wide block).  Returns the count; *out
@@ -143,6 +146,10 @@ __device__ inline int accept_wide(
 #endif
     const DevPool& P, int32_t slot, const RingPos& rp, const DevGrammar& G,
                                   const int2* tops, int ntops, int64_t len, ByteFn byte, SlotHdr* mirror) {
+#ifdef GM_DIAG_NO_DEP_BIGWALK  // diagnostics: code-size experiment (wide sets then fail)
+  slot_error(P, slot, kErrCap);
+  return kAccErr;
+#endif
   BigWalk bw;
   bw.acquire(P.ovf, (uint32_t)slot);
   bw.start();
@@ -206,7 +213,52 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
     return kAccOk;
   }
   if (reject_token) return 0;  // special or empty token (REF matcher.py:289-293)
-  if (ntops > kAccS) return accept_wide(P, slot, rp, G, tops, ntops, len, byte, mirror);
+  if (__builtin_expect(ntops > kAccS, 0)) return accept_wide(P, slot, rp, G, tops, ntops, len, byte, mirror);
+  // micro path: one stack, every byte a plain table move inside its frame
+  // (no push, no pop, no dead end: the fast table's -1 / >= 0 entries and,
+  // above the bottom frame, the pop-filtered ones) — the chain is
+  // unchanged, so the commit is the new top node.  Same result as the
+  // walkers (their n == 1 step takes exactly these entries first); a few
+  // dozen instructions instead of the walker + commit code.
+  if (GM_ACC_MICRO && ntops == 1 && mirror) {
+    int32_t node = tops[0].y;
+    const bool above = tops[0].x >= 0;
+    int64_t i = 0;
+    for (; i < len; ++i) {
+      const int32_t f = G.fast[node * G.n_classes + G.byte_class[byte(i)]];
+      if (f >= 0) {
+        node = f;
+      } else if (f == -1 || (above && f == kFastPopDies)) {
+        return 0;  // the only stack dies: rejected, state unchanged
+      } else if (above && f < -2) {
+        node = -3 - f;
+      } else {
+        break;  // a push / pop / several targets: the walkers below
+      }
+    }
+    if (i == len) {
+      const int2 t = make_int2(tops[0].x, node);
+      const int32_t nh = (rp.head + 1) % P.H;
+      *slot_tops(P, slot, nh) = t;
+      P.meta[(size_t)slot * P.H + nh] = 1;
+      P.head[slot] = nh;
+      const int32_t hl = rp.hist_len + 1;
+      P.hist_len[slot] = hl < rp.window ? hl : rp.window;
+      SlotHdr& h = *mirror;
+      int term = 0;
+      if (G.node_flags[node] & GM_NODE_POP)
+        term = t.x < 0 ? 1 : (int)key_term((h.nchain && h.chain_h[0] == t.x) ? h.chain_k[0] : arena_load(P.arena, t.x));
+      const int4 ni = G.node_info[node];
+      h.key[0] = ni.x;
+      h.dep_lo[0] = ni.y;
+      h.dep_hi[0] = ni.z;
+      h.top[0] = t;
+      h.ntops = 1;
+      h.flags = term ? 2 : 0;
+      if (spec) spec->n = 0;
+      return kAccOk;
+    }
+  }
   // fast path: register walker (<= kAccR stacks)
   if (ntops <= kAccR) {
     RWalker<kAccR, kAccRF> rw;
@@ -217,7 +269,7 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
       rw.template step<true>(G, P.arena, byte(i), &pb);
     }
     trace_mark(P, 0, 3);
-    if (!rw.spill) {
+    if (__builtin_expect(!rw.spill, 1)) {
       if (rw.err) {
         slot_error(P, slot, rw.err);
         return kAccErr;
@@ -272,7 +324,7 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
     if (!w.template step<kAccS>(G, P.arena, byte(i), &pb)) break;
   }
   trace_mark(P, 0, 3);
-  if (w.err & kErrCap) return accept_wide(P, slot, rp, G, tops, ntops, len, byte, mirror);
+  if (__builtin_expect(w.err & kErrCap, 0)) return accept_wide(P, slot, rp, G, tops, ntops, len, byte, mirror);
   if (w.err) {
     slot_error(P, slot, w.err);
     return kAccErr;

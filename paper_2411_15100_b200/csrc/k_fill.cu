@@ -180,7 +180,7 @@ bool walk_dep_general(const DevPool* Pp, int32_t slot, const SlotHdr* hd,
       bool pb = false;
       if (!w.template step<kDepS>(G, P.arena, rec_byte(inl, far, b), &pb)) break;
     }
-    if (!(w.err & kErrCap)) {
+    if (__builtin_expect(!(w.err & kErrCap), 1)) {
       *err_out |= w.err;
       return w.n > 0;
     }
@@ -203,34 +203,39 @@ bool walk_dep_general(const DevPool* Pp, int32_t slot, const SlotHdr* hd,
   return ok;
 }
 
-// Resolve dependent record di of top t (context indices cj, cj2) into this
-// CTA's shared mask words: the context class when it decides, else a walk
-// against the request's full stack.
-__device__ __forceinline__ void resolve_dep(const DevPool& P, int32_t slot, const SlotHdr& hd, const DevGrammar& G,
-                                            int32_t di, const int4& e, int2 t, int cj, int cj2, uint32_t* dep_acc,
-                                            int32_t w_lo, int32_t tok_lo, int32_t tok_hi, const SpecOut* spec,
-                                            int* s_err) {
-  const int4* rec = hd.dep_ent + 2 * (size_t)di;
+// Dependent record di of top t (context indices cj, cj2): decided by its
+// context class when possible.  Returns 0 when nothing is left to do (out of
+// this split's range, already allowed, rejected, or accepted — bit set in
+// dep_acc), 1 when it needs a walk against the request's full stack.
+__device__ __forceinline__ int dep_decide(const DevGrammar& G, int32_t di, const int4& e, int cj, int cj2,
+                                          uint32_t* dep_acc, int32_t w_lo, int32_t tok_lo, int32_t tok_hi) {
   // two-level class word fetched alongside the record (not after it)
   const uint32_t c2w = cj2 >= 0 ? __ldg(G.ctx2 + (size_t)di * kMaxCallers + cj) : 0u;
   const int32_t tid = e.x;
-  if (tid < tok_lo || tid >= tok_hi) return;  // another split's token
+  if (tid < tok_lo || tid >= tok_hi) return 0;  // another split's token
   uint32_t* acc_w = dep_acc + ((tid >> 5) - w_lo);
   const uint32_t bit = 1u << (tid & 31);
-  if (*acc_w & bit) return;  // already allowed by another stack
+  if (*acc_w & bit) return 0;  // already allowed by another stack
   if (cj >= 0) {
     uint32_t cls = ((uint32_t)e.w >> (2 * cj)) & 3u;
     if (cls == kCtxDeeper && cj2 >= 0)  // two-level class from the grandparent frame
       cls = (c2w >> (2 * cj2)) & 3u;
-    if (cls == kCtxReject) return;
+    if (cls == kCtxReject) return 0;
     if (cls == kCtxAccept) {
       atomicOr(acc_w, bit);
-      return;
+      return 0;
     }
   }
-  const int4 inl = __ldg(rec + 1);
+  return 1;
+}
+
+// Walk dependent record di (first int4 e) from top t; on success its bit is
+// set in dep_acc.  Register walker; general / overflow walkers on spill.
+__device__ __forceinline__ void dep_walk(const DevPool& P, int32_t slot, const SlotHdr& hd, const DevGrammar& G,
+                                         int32_t di, const int4& e, int2 t, uint32_t* dep_acc, int32_t w_lo,
+                                         const SpecOut* spec, int* s_err) {
+  const int4 inl = __ldg(hd.dep_ent + 2 * (size_t)di + 1);
   const uint8_t* far = reinterpret_cast<const uint8_t*>(hd.tokrec) + e.z;  // bytes beyond the inline 16
-  // fast path: register walker; general / overflow walkers only on spill
   RWalker<kDepR, kDepRF> rw;
   rw.init(hd.chain_h, hd.chain_k, hd.nchain);
   rw.add(rw.ref_of_handle(t.x), t.y);
@@ -240,7 +245,7 @@ __device__ __forceinline__ void resolve_dep(const DevPool& P, int32_t slot, cons
   }
   bool ok;
   uint32_t err = 0;
-  if (!rw.spill) {
+  if (__builtin_expect(!rw.spill, 1)) {
     err = rw.err;
     ok = rw.n > 0;
   } else {
@@ -250,10 +255,51 @@ __device__ __forceinline__ void resolve_dep(const DevPool& P, int32_t slot, cons
     slot_error(P, slot, err);
     *s_err = 1;
   }
-  if (ok) atomicOr(acc_w, bit);
+  if (ok) atomicOr(dep_acc + ((e.x >> 5) - w_lo), 1u << (e.x & 31));
 }
 
-constexpr int kFillTops = 32;  // tops per pass of the fill's per-top arrays (wide sets: several passes)
+// K3/K5 apply overlapped with the dependent walks: the apply warps mask
+// every token whose bit is 0 in `base` (cached rows | dependents decided so
+// far, AND universe) and that is not `pend`ing a walk; thread `ti` of `nt`.
+template <int EB>
+__device__ __forceinline__ void apply_row_keep(char* __restrict__ rowp, const uint32_t* __restrict__ base,
+                                               const uint32_t* __restrict__ pend, int64_t tok_lo, int64_t tok_hi,
+                                               uint32_t neg, int ti, int nthr) {
+  constexpr int vec = 16 / EB;
+  constexpr uint32_t full = (1u << vec) - 1u;
+  const int32_t lim = (int32_t)(tok_hi - tok_lo);
+  const int32_t chunks = (lim + vec - 1) / vec;
+  char* bp = rowp + tok_lo * EB;
+  for (int32_t c = ti; c < chunks; c += nthr) {
+    const int32_t t0 = c * vec;
+    const int32_t w = t0 >> 5, sh = t0 & 31;
+    uint32_t keep = ((base[w] | pend[w]) >> sh) & full;
+    const bool tail = t0 + vec > lim;
+    if (tail) keep |= full & ~((1u << (lim - t0)) - 1u);
+    if (keep == full) continue;
+    char* q = bp + t0 * EB;
+    if (keep == 0) {
+      st_cs_v4(q, neg);
+    } else {
+      uint32_t m = ~keep & full;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        if (EB == 4) st_cs_u32(q + j * 4, neg);
+        else st_cs_u16(q + j * 2, neg);
+      }
+    }
+  }
+}
+
+constexpr int kFillTops = 32;
+constexpr int kWalkQueue = 512;
+#ifndef GM_OVERLAP_APPLY
+#define GM_OVERLAP_APPLY 0  // measured: K5 b2b +0.6 us, cold -2 us (tools/variants J/K/L)
+#endif
+#ifndef GM_WALK_DIV
+#define GM_WALK_DIV 2  // overlap: 1/GM_WALK_DIV of the warps walk, the rest apply
+#endif  // overlap: dependent walks queued per CTA (more: walked at once)  // tops per pass of the fill's per-top arrays (wide sets: several passes)
 
 // Tops b0 .. b0+kFillTops of the slot's current ring entry into the fill's
 // per-top arrays (key, dependent range, top); returns how many.
@@ -311,6 +357,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   uint32_t* dep_acc = reinterpret_cast<uint32_t*>(smem);  // [Wp] this CTA's words
   uint8_t* tables = smem + part_bytes;                    // staged blob
   uint8_t* rows_s = tables + kStageBytes;                 // [kTmaRows + 1][part_bytes]
+  uint32_t* pend = reinterpret_cast<uint32_t*>(rows_s + (size_t)(kTmaRows + 1) * part_bytes);  // [Wp] walks pending
   __shared__ SlotHdr hd;
   __shared__ int s_partial, s_nt, s_nrows;
   __shared__ int32_t s_key[32], s_lo[32], s_hi[32];
@@ -339,7 +386,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   __shared__ RingPos rp;
   __shared__ int4 s_rec[2];
-  __shared__ int s_just_term, s_dirty, s_walked, s_acc, s_err, s_wide;
+  __shared__ int s_just_term, s_dirty, s_walked, s_acc, s_err, s_wide, s_nwalk;
+  __shared__ int2 s_wq[kWalkQueue];  // overlap: queued dependent walks (record index, top)
   __shared__ SpecOut s_spec;  // K5: fresh frames whose interning is deferred (warp 2, checked at the end)
   int32_t tok = -1;
   const bool do_acc = ACCEPT && (SA.tokens || ptok);
@@ -568,6 +616,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   if (threadIdx.x == 0) {
     s_walked = 0;
     s_err = 0;
+    s_nwalk = 0;
   }
   __syncthreads();
   const SpecOut* spec = do_acc ? &s_spec : nullptr;
@@ -576,11 +625,24 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   int nt = s_nt;
   const bool tma = pref >= 0 || (vec && hd.ntops >= 0 && nt <= kTmaRows && nw > 0 && !terminated && pref == -1);
   if (pref == -2) mbar_wait(&rows_bar, 0);  // drain the stale prefetch before leaving
+  // K3/K5: the apply starts before the dependent walks finish.  The walks
+  // that context classes cannot decide are queued (their tokens marked
+  // pending); half of the warps walk them while the other half mask every
+  // token that is neither allowed by the rows / decided dependents nor
+  // pending, then the few pending tokens that stayed rejected are masked.
+  // Wide sets (several passes) keep the serial order.
+  const bool overlap = GM_OVERLAP_APPLY && APPLY && !s_wide;
+  const int32_t n_warps = blockDim.x >> 5;
+  const int32_t walk_warps = overlap ? n_warps / GM_WALK_DIV : n_warps;
+  if (overlap)
+    for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) pend[w] = 0u;
 
   trace_mark(P, 1, 3);
   // one pass over the tops' dependents — several for a wide set (more than
   // kFillTops stacks), each OR-ing its tops' rows into dep_acc
   int total = 0;
+  DevGrammar Gd = do_acc ? Gs : hint_ok ? blob_view(tables) : Gs;  // staged below when needed
+  bool staged = do_acc || hint_ok;
   for (int b0 = 0;;) {
   total = 0;
   for (int s = 0; s < nt; ++s) total += s_hi[s] - s_lo[s];
@@ -590,13 +652,16 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     P.trace[16 + 10] = (unsigned long long)nt;
   }
   if (total) {
-    const DevGrammar G = do_acc ? Gs : hint_ok ? blob_view(tables) : stage_blob(hd.blob, hd.blob_bytes, tables);
+    if (!staged) {
+      Gd = stage_blob(hd.blob, hd.blob_bytes, tables);  // barrier inside (total is CTA-uniform)
+      staged = true;
+    }
     // caller index of each top's parent frame within the callers of the
     // top's rule: selects the dependents' one-level context class
     if (!early_ctx) {
       if ((int)threadIdx.x < nt) {
         int cj, cj2;
-        context_of(P, hd, G, s_top[threadIdx.x], cj, cj2);
+        context_of(P, hd, Gd, s_top[threadIdx.x], cj, cj2);
         s_cj[threadIdx.x] = cj;
         s_cj2[threadIdx.x] = cj2;
       }
@@ -607,7 +672,6 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     const int32_t tok_lo = w_lo * 32, tok_hi = w_hi * 32;
     // warp-major assignment: consecutive dependents go to different warps, so
     // a handful of walks run in parallel instead of diverging inside one warp
-    const int32_t n_warps = blockDim.x >> 5;
     const int32_t q0 = (threadIdx.x & 31) * n_warps + (threadIdx.x >> 5);
     // the next record is loaded before this one is resolved (the loop is
     // latency-bound for keys with thousands of dependents)
@@ -631,8 +695,17 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
         di_next = locate(q + blockDim.x, s_next);
         e_next = __ldg(hd.dep_ent + 2 * (size_t)di_next);
       }
-      if (kTimeline && P.trace) atomicAdd(&s_walked, 1 | (e.y << 16));  // diagnostics: visits, bytes
-      resolve_dep(P, slot, hd, G, di, e, s_top[s], s_cj[s], s_cj2[s], dep_acc, w_lo, tok_lo, tok_hi, spec, &s_err);
+      if (!dep_decide(Gd, di, e, s_cj[s], s_cj2[s], dep_acc, w_lo, tok_lo, tok_hi)) continue;
+      if (kTimeline && P.trace) atomicAdd(&s_walked, 1 | (e.y << 16));  // diagnostics: walks, bytes
+      if (overlap) {  // queue the walk, mark the token pending
+        const int k = atomicAdd(&s_nwalk, 1);
+        if (k < kWalkQueue) {
+          s_wq[k] = make_int2(di, s);
+          atomicOr(pend + ((e.x >> 5) - w_lo), 1u << (e.x & 31));
+          continue;
+        }
+      }
+      dep_walk(P, slot, hd, Gd, di, e, s_top[s], dep_acc, w_lo, spec, &s_err);
     }
   }
   if (!s_wide) break;
@@ -656,6 +729,65 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   }
   trace_mark(P, 1, 5);
   __syncthreads();
+
+  uint32_t* out = bitmask ? bitmask + row * bstride : nullptr;
+  const int32_t eos_w = hd.eos >> 5;
+  const uint32_t eos_bit = (!terminated && (hd.flags & 2)) ? (1u << (hd.eos & 31)) : 0u;
+  const uint32_t tail = (hd.V & 31) ? ((1u << (hd.V & 31)) - 1u) : 0xFFFFFFFFu;
+  const int64_t vocab = ap_vocab < (int64_t)W * 32 ? ap_vocab : (int64_t)W * 32;
+  const int64_t t_lo = (int64_t)w_lo * 32, t_hi = (int64_t)w_hi * 32 < vocab ? (int64_t)w_hi * 32 : vocab;
+  uint32_t* base = reinterpret_cast<uint32_t*>(rows_s);  // overlap: rows | decided dependents, AND universe
+  if (overlap) {
+    const int32_t warp = threadIdx.x >> 5;
+    if (warp < walk_warps) {  // walk warps: the queued walks, warp-major
+      const int nq = min(s_nwalk, kWalkQueue);
+      for (int32_t k = (threadIdx.x & 31) * walk_warps + warp; k < nq; k += walk_warps * 32) {
+        const int2 wq = s_wq[k];
+        const int4 e = __ldg(hd.dep_ent + 2 * (size_t)wq.x);
+        dep_walk(P, slot, hd, Gd, wq.x, e, s_top[wq.y], dep_acc, w_lo, spec, &s_err);
+      }
+    } else {  // apply warps: base words, then mask all but allowed and pending tokens
+      const int ti = (int)threadIdx.x - walk_warps * 32, nthr = (int)blockDim.x - walk_warps * 32;
+      if (tma) {
+        mbar_wait(&rows_bar, 0);
+        const int nr = s_nrows;
+        const uint4* univ = reinterpret_cast<const uint4*>(rows_s + (size_t)kTmaRows * part_bytes);
+        for (int32_t w4 = ti; w4 < (nw >> 2); w4 += nthr) {
+          uint4 a = reinterpret_cast<const uint4*>(dep_acc)[w4];
+          for (int k = 0; k < nr; ++k) {
+            const uint4 r = reinterpret_cast<const uint4*>(rows_s + (size_t)k * part_bytes)[w4];
+            a.x |= r.x; a.y |= r.y; a.z |= r.z; a.w |= r.w;
+          }
+          const uint4 u = univ[w4];
+          uint32_t v[4] = {a.x & u.x, a.y & u.y, a.z & u.z, a.w & u.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int32_t w = w_lo + w4 * 4 + e;
+            if (w == eos_w) v[e] |= eos_bit;
+            if (w == W - 1) v[e] &= tail;
+          }
+          reinterpret_cast<uint4*>(base)[w4] = make_uint4(v[0], v[1], v[2], v[3]);
+        }
+      } else {
+        for (int32_t w = w_lo + ti; w < w_hi; w += nthr) {
+          uint32_t a = dep_acc[w - w_lo];
+          for (int s = 0; s < nt; ++s)
+            if (s_key[s] >= 0) a |= __ldg(hd.acc_rows + (size_t)s_key[s] * W + w);
+          a &= __ldg(hd.universe + w);
+          if (w == eos_w) a |= eos_bit;
+          if (w == W - 1) a &= tail;
+          base[w - w_lo] = a;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");  // apply warps only: base complete
+      if (t_hi > t_lo) {
+        char* rowp = logits + row * lstride_bytes;
+        if (ap_eb == 4) apply_row_keep<4>(rowp, base, pend, t_lo, t_hi, ap_neg, ti, nthr);
+        else apply_row_keep<2>(rowp, base, pend, t_lo, t_hi, ap_neg, ti, nthr);
+      }
+    }
+    __syncthreads();
+  }
   trace_mark(P, 1, 6);
   // a walk error this step: the request's flag says so (bit 1) next to
   // whether its token was accepted (bit 0); the slot's error word says which
@@ -663,12 +795,28 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_walks));
 
   // Merge and store this CTA's words.
-  uint32_t* out = bitmask ? bitmask + row * bstride : nullptr;
-  const int32_t eos_w = hd.eos >> 5;
-  const uint32_t eos_bit = (!terminated && (hd.flags & 2)) ? (1u << (hd.eos & 31)) : 0u;
-  const uint32_t tail = (hd.V & 31) ? ((1u << (hd.V & 31)) - 1u) : 0xFFFFFFFFu;
   bool partial = false;
-  if (tma) {
+  if (overlap) {
+    // final = base | walked dependents; the pending tokens that stayed
+    // rejected are the apply's last stores
+    char* rowp = logits + row * lstride_bytes;
+    for (int32_t w = threadIdx.x; w < nw; w += blockDim.x) {
+      const int32_t wg = w_lo + w;
+      const uint32_t f = base[w] | dep_acc[w];
+      partial |= (f != ((wg == W - 1) ? tail : 0xFFFFFFFFu));
+      if (out) out[wg] = f;
+      uint32_t m = pend[w] & ~f;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t t = (int64_t)wg * 32 + j;
+        if (t < t_hi) {
+          if (ap_eb == 4) st_cs_u32(rowp + t * 4, ap_neg);
+          else st_cs_u16(rowp + t * 2, ap_neg);
+        }
+      }
+    }
+  } else if (tma) {
     mbar_wait(&rows_bar, 0);
     const int nr = s_nrows;
     const uint4* univ = reinterpret_cast<const uint4*>(rows_s + (size_t)kTmaRows * part_bytes);
@@ -709,16 +857,15 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   trace_mark(P, 1, 7);
   unsigned long long t_merge = 0;
   if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_merge));
-  if (need_apply || APPLY) {
+  if (need_apply || (APPLY && !overlap)) {
     if (partial) s_partial = 1;
     __syncthreads();
     if (need_apply && threadIdx.x == 0) need_apply[i] = (uint8_t)s_partial;  // launched with one split
   }
-  // an all-allowed row still masks logits columns in [V, vocab) (their bits
-  // are zero, as gm_apply_inplace treats them)
-  if (APPLY && (s_partial || ap_vocab > (int64_t)hd.V)) {
-    const int64_t vocab = ap_vocab < (int64_t)W * 32 ? ap_vocab : (int64_t)W * 32;
-    const int64_t t_lo = (int64_t)w_lo * 32, t_hi = (int64_t)w_hi * 32 < vocab ? (int64_t)w_hi * 32 : vocab;
+  // serial order (wide sets): apply from the final words.  An all-allowed
+  // row still masks logits columns in [V, vocab) (their bits are zero, as
+  // gm_apply_inplace treats them)
+  if (APPLY && !overlap && (s_partial || ap_vocab > (int64_t)hd.V)) {
     if (t_hi > t_lo) apply_row(logits + row * lstride_bytes, dep_acc, t_lo, t_hi, ap_eb, ap_neg);
   }
   if (do_acc && threadIdx.x >= 64 && threadIdx.x < 96 && s_spec.n > 0) {  // warp 2: verify the deferred commit
@@ -812,7 +959,7 @@ static int32_t split_words(int32_t Wmax, int splits) { return ((Wmax + 3) / 4 + 
 
 static size_t fill_smem(int32_t Wp) {
   const size_t part = ((size_t)Wp * 4 + 15) & ~(size_t)15;
-  return part + kStageBytes + (kTmaRows + 1) * part;
+  return part + kStageBytes + (kTmaRows + 2) * part;
 }
 
 gm_status launch_fill(const DevPool& P, const int32_t* slots, int32_t n, int32_t* bitmask, int64_t bstride,

@@ -3,24 +3,25 @@
 Workload (per GPU, weak scaling): the builtin ECMA-404 JSON grammar over
 synth_vocab(128256) (the reference's synthetic Llama-3.1-shaped vocabulary,
 REF synthvocab.py), batch 128 requests, bf16 logits [128 x 128256].  One
-step = batched fill_next_token_bitmask (K2) + apply_token_bitmask_inplace (K0)
-on the device; between steps the requests advance by a deterministic
-structure-biased sampler (integer-hash scores, identical on CPU and GPU, half
-of the draws restricted to short structural tokens) followed by batched
-accept_token (K4) and recycling of finished requests — so the masks are real
-decode-trajectory masks, bimodal between string interiors and structural
-positions.
+step = accept the previous step's sampled tokens, restart finished requests,
+fill the next masks and apply them to the logits — requests advance by a
+deterministic structure-biased sampler (integer-hash scores, identical on CPU
+and GPU), so the masks are real decode-trajectory masks.
 
-Timing: CUDA events on the launching stream around every step's fill+apply
-(``value``), L2 flushed (256 MiB write) before every step and logits ring of
-8 x 32.8 MB; max over ranks.  ``e2e`` replays the same trajectories through
-the public API with host buffers: pinned token ids H2D, batch accept, batch
-fill, apply, D2H of the accepted flags, per step.
+``value``: K5 steps (gm_step_tokens: accept + recycle + fill + apply in one
+launch) back to back in one CUDA graph, K steps in ONE CUDA-event bracket,
+median of ``--repeats`` brackets.  No flush between steps: the inputs are
+larger than L2 (8 x 32.8 MB logits ring + a fresh 2 MB bitmask slice per
+step).  Every mask of every timed step is compared with pass A's.
+``latency_l2_flushed``: single steps with a 256 MiB L2 flush before each.
+``e2e``: the same steps through the native decode loop (graph.DecodeLoop:
+host token ids in, accepted flags out).  ``cpu_baseline``: the reference
+itself (grammask, installed in baseline/_ref) on 1 core over 8 requests of
+the same trajectories, masks compared with the GPU's.
 
-``--impl reference`` runs the CPU oracle (oracle/, the restated reference
-algorithm; /root/reference cannot travel) on the host cores: B matchers
-spread over a process pool, per step fill (Algorithm 1 + dependent walks)
-then torch-CPU apply, same sampler.
+``--impl reference`` runs the reference (grammask from baseline/_ref; the
+oracle port of oracle/ only if it is missing) on all host cores: the batch
+split over one process per core, fills timed per step, + torch-CPU apply.
 """
 
 from __future__ import annotations
@@ -612,40 +613,119 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     return res
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _grammask():
+    """The reference itself (grammask, pure Python + NumPy), installed into
+    baseline/_ref by ``pip install --target baseline/_ref /root/reference/pkg``
+    (DESIGN.md §6); it travels to the GPU box with the repository.  None when
+    it is not installed (the legs then time the oracle port)."""
+    if not os.path.isdir(os.path.join(REF_DIR, "grammask")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import grammask
+
+    return grammask
+
+
+def _reference_bundle(gmk, grammar: str, vocab_size: int):
+    """compile_bundle of the reference for this workload (REF bundle.py:65-93),
+    its synth_vocab (REF synthvocab.py:63-154; content hash equal to ours)."""
+    from grammask.bundle import compile_bundle
+    from grammask.synthvocab import synth_vocab
+
+    from grammask import grammars as rg
+    from grammask.schema import schema_to_grammar_text as ref_schema
+
+    text = {"json": rg.JSON_ECMA404, "xml": rg.XML_TOY, "arithmetic": rg.ARITHMETIC,
+            "schema": ref_schema(rg.SAMPLE_SCHEMA)}.get(grammar) or grammar_text(grammar)
+    vocab = synth_vocab(vocab_size)
+    t0 = time.perf_counter()
+    b = compile_bundle(text, vocab)
+    return vocab, b, time.perf_counter() - t0
+
+
 def cpu_baseline(args, ours: dict) -> dict:
-    """Oracle (restated reference) on a bounded sample of the same workload:
-    replay the GPU run's token trajectories for a few requests, time the
-    oracle's fill per request-step (1 core), check its masks against the
-    GPU's, and time a torch-CPU apply of the full [B, V] bf16 step."""
-    from oracle import compile_oracle_bundle
-    from oracle.matcher import OracleMatcher
+    """The reference on a bounded sample of the same workload, 1 core: its
+    compile, then the GPU run's token trajectories of 8 requests replayed
+    through Matcher.fill_next_token_mask with the reference's own timing
+    method (REF bench.py:182-229: gc off, per-step minimum over repeats),
+    every mask compared with the GPU's; plus a torch-CPU apply of the full
+    [B, V] bf16 step (the reference has no apply).  Falls back to the oracle
+    port (kind "port") when baseline/_ref is absent."""
+    import gc
+
     import paper_2411_15100_b200 as gm
 
-    vocab = gm.synth_vocab(args.vocab)
-    t0 = time.perf_counter()
-    b = compile_oracle_bundle(grammar_text(args.grammar), vocab)
-    compile_s = time.perf_counter() - t0
+    gmk = _grammask()
     toks = ours["tokens"]
     keep = ours["mask_keep"]
-    n_req = min(keep.shape[1], 4)
-    n_steps = min(toks.shape[0], args.cpu_steps)
+    n_req = keep.shape[1]
+    n_steps = toks.shape[0]
+    if gmk is not None:
+        from grammask.matcher import Matcher, TokenMask
+
+        vocab, b, compile_s = _reference_bundle(gmk, args.grammar, args.vocab)
+        assert vocab.content_hash() == gm.synth_vocab(args.vocab).content_hash()
+        kind = "reference"
+
+        def new_matcher():
+            return Matcher(b, vocab, history_window=1)
+
+        def fill(m, mask):
+            m.fill_next_token_mask(mask)
+            return np.frombuffer(mask.to_bytes(), dtype=np.int32)
+
+        mask_obj = TokenMask(vocab.size)
+    else:
+        from oracle import compile_oracle_bundle
+        from oracle.matcher import OracleMatcher
+
+        vocab = gm.synth_vocab(args.vocab)
+        t0 = time.perf_counter()
+        b = compile_oracle_bundle(grammar_text(args.grammar), vocab)
+        compile_s = time.perf_counter() - t0
+        kind = "port"
+
+        def new_matcher():
+            return OracleMatcher(b, history_window=1)
+
+        def fill(m, mask):
+            return m.fill().view(np.int32)
+
+        mask_obj = None
     fills = []
-    mismatches = 0
+    mismatches = checked = 0
     budget = time.perf_counter() + args.cpu_budget_s
-    for r in range(n_req):
-        m = OracleMatcher(b, history_window=1)
-        for s in range(n_steps):
-            t1 = time.perf_counter()
-            words = m.fill()
-            fills.append(time.perf_counter() - t1)
-            if not np.array_equal(words.view(np.int32), keep[s, r]):
-                mismatches += 1
-            t = int(toks[s, r])
-            assert m.accept_token(t)
-            if t == vocab.eos_id:
-                m = OracleMatcher(b, history_window=1)
+    gc_on = gc.isenabled()
+    gc.disable()
+    try:
+        for r in range(n_req):
+            m = new_matcher()
+            for s in range(n_steps):
+                best = None
+                for rep in range(2):  # per-step minimum over repeats (REF bench.py:205-226)
+                    t1 = time.perf_counter()
+                    words = fill(m, mask_obj)
+                    dt = time.perf_counter() - t1
+                    best = dt if best is None else min(best, dt)
+                fills.append(best)
+                checked += 1
+                if not np.array_equal(words, keep[s, r]):
+                    mismatches += 1
+                t = int(toks[s, r])
+                assert m.accept_token(t)
+                if t == vocab.eos_id:
+                    m = new_matcher()
+                if time.perf_counter() > budget:
+                    break
             if time.perf_counter() > budget:
                 break
+    finally:
+        if gc_on:
+            gc.enable()
     threads = torch.get_num_threads()
     logits = torch.randn(args.batch, vocab.size).to(torch.bfloat16)
     bm = torch.from_numpy(keep[0, :1].repeat(args.batch, 0))
@@ -657,15 +737,17 @@ def cpu_baseline(args, ours: dict) -> dict:
         apply_s.append(time.perf_counter() - t1)
     fill_us = statistics.fmean(fills) * 1e6
     step_us = args.batch * fill_us + min(apply_s) * 1e6
+    who = "reference grammask (baseline/_ref)" if kind == "reference" else "oracle port"
     return {
-        "value": step_us, "unit": UNIT, "cores": 1, "kind": "port",
+        "value": step_us, "unit": UNIT, "cores": 1, "kind": kind,
         "apply_threads": threads,
-        "sample": f"oracle fill on {len(fills)} request-steps ({n_req} requests x <= {n_steps} steps of the GPU "
-                  f"run's trajectories) scaled to batch {args.batch}, + torch-CPU apply [{args.batch} x {vocab.size}] "
-                  f"bf16 ({threads} threads)",
+        "sample": f"{who} Matcher.fill_next_token_mask on {checked} request-steps ({n_req} requests x up to "
+                  f"{n_steps} steps of the GPU run's trajectories, per-step min of 2 repeats, gc off) scaled to "
+                  f"batch {args.batch}, + torch-CPU apply [{args.batch} x {vocab.size}] bf16 ({threads} threads)",
         "fill_us_per_request": fill_us,
         "apply_us": min(apply_s) * 1e6,
         "compile_ms": compile_s * 1e3,
+        "parity_checked_request_steps": checked,
         "parity_mismatches": mismatches,
         "cpu": _cpu_name(),
     }
@@ -688,55 +770,112 @@ def _cpu_name() -> str:
 _W_STATE = {}
 
 
-def _ref_worker_init(vocab_size, n_local, seed_rows, grammar="json"):
-    import paper_2411_15100_b200 as gm
-    from oracle import compile_oracle_bundle
+def _ref_worker_init(vocab_size, seed_rows, grammar="json"):
+    # one host core per worker: no torch intra-op threads competing with the
+    # other workers' fills
+    torch.set_num_threads(1)
+    st = _W_STATE
+    if "bundle" not in st:  # not inherited from the parent (spawn): compile here
+        gmk = _grammask()
+        if gmk is not None:
+            st["vocab"], st["bundle"], _ = _reference_bundle(gmk, grammar, vocab_size)
+            st["kind"] = "reference"
+        else:
+            import paper_2411_15100_b200 as gm
+            from oracle import compile_oracle_bundle
+
+            st["vocab"] = gm.synth_vocab(vocab_size)
+            st["bundle"] = compile_oracle_bundle(grammar_text(grammar), st["vocab"])
+            st["kind"] = "port"
+    vocab = st["vocab"]
+    st.update(rows=seed_rows, structural=torch.from_numpy(structural_flags(vocab, WORKLOADS[grammar]["structural"])),
+              force=forced_token(vocab, grammar))
+    st["ms"] = [_ref_matcher() for _ in seed_rows]
+
+
+def _ref_matcher():
+    st = _W_STATE
+    if st["kind"] == "reference":
+        from grammask.matcher import Matcher
+
+        return Matcher(st["bundle"], st["vocab"], history_window=1)
     from oracle.matcher import OracleMatcher
 
-    vocab = gm.synth_vocab(vocab_size)
-    b = compile_oracle_bundle(grammar_text(grammar), vocab)
-    _W_STATE.update(vocab=vocab, b=b, rows=seed_rows,
-                    ms=[OracleMatcher(b, history_window=1) for _ in seed_rows],
-                    structural=torch.from_numpy(structural_flags(vocab, WORKLOADS[grammar]["structural"])),
-                    force=forced_token(vocab, grammar))
+    return OracleMatcher(st["bundle"], history_window=1)
 
 
-def _ref_worker_step(step):
-    from oracle.matcher import OracleMatcher
+def _ref_worker_fill(step):
+    """Timed part of a step: every request's fill (REF matcher.py:377)."""
+    import gc
 
     st = _W_STATE
     vocab = st["vocab"]
+    gc.disable()
     t0 = time.perf_counter()
-    words = [m.fill() for m in st["ms"]]
-    dt = time.perf_counter() - t0
-    bm = torch.from_numpy(np.stack(words).view(np.int32))
-    allowed = unpack_allowed(bm, vocab.size)
+    if st["kind"] == "reference":
+        from grammask.matcher import TokenMask
+
+        masks = [TokenMask(vocab.size) for _ in st["ms"]]
+        for m, mk in zip(st["ms"], masks):
+            m.fill_next_token_mask(mk)
+        dt = time.perf_counter() - t0
+        words = np.stack([np.frombuffer(mk.to_bytes(), dtype=np.int32) for mk in masks])
+    else:
+        words = np.stack([m.fill() for m in st["ms"]]).view(np.int32)
+        dt = time.perf_counter() - t0
+    gc.enable()
+    st["words"] = words
+    return dt, words
+
+
+def _ref_worker_advance(step):
+    """Untimed: sample and accept the next tokens (same sampler as the GPU run)."""
+    st = _W_STATE
+    vocab = st["vocab"]
+    allowed = unpack_allowed(torch.from_numpy(st["words"]), vocab.size)
     toks = sample_tokens(allowed, st["structural"], step, torch.tensor(st["rows"]), force=st["force"]).tolist()
     for i, t in enumerate(toks):
         assert st["ms"][i].accept_token(t)
         if t == vocab.eos_id:
-            st["ms"][i] = OracleMatcher(st["b"], history_window=1)
-    return dt, bm.numpy()
+            st["ms"][i] = _ref_matcher()
+    return True
 
 
 def run_reference(args) -> dict:
+    """--impl reference: the reference itself (grammask from baseline/_ref;
+    the oracle port only if it is not installed) on all host cores — the
+    batch split over one worker process per core, each step's fills timed
+    (max over workers) with the sampling of the next tokens outside the
+    timed region, + torch-CPU apply of the [B, V] bf16 logits."""
     import multiprocessing as mp
 
     cores = len(os.sched_getaffinity(0))
     nproc = max(1, min(cores, args.batch))
     rows = list(range(args.batch))
     chunks = [rows[i::nproc] for i in range(nproc)]
-    ctx = mp.get_context("fork")
+    # compile once here; the forked workers inherit the bundle
     t0 = time.perf_counter()
-    pools = [ctx.Pool(1, initializer=_ref_worker_init, initargs=(args.vocab, len(c), c, args.grammar))
-             for c in chunks]
+    gmk = _grammask()
+    if gmk is not None:
+        _W_STATE["vocab"], _W_STATE["bundle"], _ = _reference_bundle(gmk, args.grammar, args.vocab)
+        _W_STATE["kind"] = "reference"
+    else:
+        import paper_2411_15100_b200 as gm
+        from oracle import compile_oracle_bundle
+
+        _W_STATE["vocab"] = gm.synth_vocab(args.vocab)
+        _W_STATE["bundle"] = compile_oracle_bundle(grammar_text(args.grammar), _W_STATE["vocab"])
+        _W_STATE["kind"] = "port"
+    compile_s = time.perf_counter() - t0
+    kind = _W_STATE["kind"]
+    ctx = mp.get_context("fork")
+    pools = [ctx.Pool(1, initializer=_ref_worker_init, initargs=(args.vocab, c, args.grammar)) for c in chunks]
     for p in pools:
         p.apply(time.time)
-    compile_s = time.perf_counter() - t0
     logits = torch.randn(args.batch, args.vocab).to(torch.bfloat16)
     step_us = []
     for s in range(args.warmup + args.steps):
-        futs = [p.apply_async(_ref_worker_step, (s,)) for p in pools]
+        futs = [p.apply_async(_ref_worker_fill, (s,)) for p in pools]
         outs = [f.get() for f in futs]
         fill_s = max(o[0] for o in outs)
         bm = np.zeros((args.batch, (args.vocab + 31) // 32), dtype=np.int32)
@@ -748,17 +887,21 @@ def run_reference(args) -> dict:
         apply_s = time.perf_counter() - t1
         if s >= args.warmup:
             step_us.append((fill_s + apply_s) * 1e6)
+        for f in [p.apply_async(_ref_worker_advance, (s,)) for p in pools]:
+            f.get()
     for p in pools:
         p.terminate()
     v = statistics.fmean(step_us)
+    who = "reference grammask (baseline/_ref)" if kind == "reference" else "oracle port"
     return {
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 bitmask / bf16 logits", "data": "synthetic",
         "config": _config(args, 1),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": nproc, "kind": "port",
-                         "sample": f"oracle fill for all {args.batch} requests per step over {nproc} worker "
-                                   f"processes (max over workers) + torch-CPU apply; compile+setup "
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": nproc, "kind": kind,
+                         "sample": f"{who}: Matcher.fill_next_token_mask for all {args.batch} requests per step "
+                                   f"over {nproc} worker processes (1 thread each; max over workers, sampling "
+                                   f"outside the timed region) + torch-CPU apply; compile "
                                    f"{compile_s:.1f}s excluded", "cpu": _cpu_name()},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "compile_ms": compile_s * 1e3,
@@ -792,8 +935,7 @@ def main():
     ap.add_argument("--diag-k4k3", action="store_true", help="diagnostic: time K4 + recycle + K3 per step")
     ap.add_argument("--diag-k5k0", action="store_true", help="diagnostic: time K5 (no logits) + K0 per step")
     ap.add_argument("--repeats", type=int, default=7, help="K-step brackets of the value pass (median)")
-    ap.add_argument("--cpu-steps", type=int, default=24)
-    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic only: keep L2 warm between steps")
     args = ap.parse_args()

@@ -196,6 +196,20 @@ gm_status gm_cache_build_rows(const gm_grammar* g, const gm_vocab* v,
                               int32_t* acc_rows, int32_t* dep_rows,
                               void* stream);
 
+/* Position sharding with any subset of keys: rows of the keys listed in the
+ * HOST array key_list[0..n) (indices into tables.cache_keys, any order; row
+ * i of acc_rows/dep_rows belongs to key_list[i]).  The Python layer deals
+ * the keys of a build round-robin in decreasing order of estimated walk
+ * cost and replicates the rows with one all-gather issued
+ * through torch.distributed (ProcessGroupNCCL over NVLink): the library
+ * takes no NCCL dependency, the payload is one contiguous device buffer per
+ * rank either way.  Syncs the stream. */
+gm_status gm_cache_build_keys(const gm_grammar* g, const gm_vocab* v,
+                              const int32_t* key_list, int32_t n,
+                              int32_t* acc_rows, int32_t* dep_rows,
+                              void* stream);
+int32_t gm_grammar_num_keys(const gm_grammar* g);
+
 /* Assemble a cache from complete rows for all keys (device pointers; the
  * rows are copied).  Dependent bit rows are compacted to sorted id lists
  * (REF cache.py:400-402).  Syncs the stream. */

@@ -99,6 +99,8 @@ _SIGNATURES = {
     "gm_grammar_create": ([C.POINTER(gm_grammar_tables), C.POINTER(_P)], _I32),
     "gm_grammar_release": ([_P], None),
     "gm_cache_build_rows": ([_P, _P, _I32, _I32, _P, _P, _P], _I32),
+    "gm_cache_build_keys": ([_P, _P, _P, _I32, _P, _P, _P], _I32),
+    "gm_grammar_num_keys": ([_P], _I32),
     "gm_cache_create": ([_P, _P, _P, _P, C.POINTER(_P), C.POINTER(gm_cache_stats), _P], _I32),
     "gm_cache_release": ([_P], None),
     "gm_cache_export": ([_P, _P, _P, _P, C.POINTER(_I64)], _I32),

@@ -24,7 +24,7 @@ gm_status fail(gm_status code, const std::string& msg) {
 
 // kernel launchers (k_*.cu)
 gm_status launch_cache_build(const DevGrammar&, const DevVocab&, const DevArena&, const DevOverflow&, int32_t,
-                             int32_t, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
+                             const int32_t*, int32_t, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
 gm_status launch_pool_errors(const DevPool&, const int32_t*, int32_t, uint32_t*, int32_t, cudaStream_t);
 gm_status launch_row_popcount(const uint32_t*, int32_t, int32_t, int64_t*, cudaStream_t);
 gm_status launch_dep_compact(const uint32_t*, int32_t, int32_t, const int32_t*, int32_t*, cudaStream_t);
@@ -473,10 +473,18 @@ void gm_grammar_release(gm_grammar* g) {
 }
 
 // ---------------------------------------------------------------------------
-gm_status gm_cache_build_rows(const gm_grammar* g, const gm_vocab* v, int32_t key_begin, int32_t n,
-                              int32_t* acc_rows, int32_t* dep_rows, void* stream) {
+// Rows of cache keys [key_begin, key_begin + n), or of the keys listed in
+// host array key_list[0..n) (position sharding: any subset in any order).
+static gm_status cache_build(const gm_grammar* g, const gm_vocab* v, int32_t key_begin, const int32_t* key_list,
+                             int32_t n, int32_t* acc_rows, int32_t* dep_rows, void* stream) {
   if (!g || !v) return fail(GM_ERR_INVALID, "null grammar/vocab");
-  if (key_begin < 0 || n < 0 || key_begin + n > g->dev.n_keys) return fail(GM_ERR_INVALID, "key range out of bounds");
+  if (n < 0) return fail(GM_ERR_INVALID, "negative key count");
+  if (key_list) {
+    for (int32_t k = 0; k < n; ++k)
+      if (key_list[k] < 0 || key_list[k] >= g->dev.n_keys) return fail(GM_ERR_INVALID, "key index out of bounds");
+  } else if (key_begin < 0 || key_begin + n > g->dev.n_keys) {
+    return fail(GM_ERR_INVALID, "key range out of bounds");
+  }
   if (n == 0) return GM_OK;
   cudaStream_t s = as_stream(stream);
   const size_t bytes = (size_t)n * v->dev.W * 4;
@@ -485,14 +493,34 @@ gm_status gm_cache_build_rows(const gm_grammar* g, const gm_vocab* v, int32_t ke
   BuildScratch* B;
   gm_status st = build_scratch(&B, s);
   if (st) return st;
-  st = launch_cache_build(g->dev, v->dev, B->arena, B->ovf, key_begin, n, reinterpret_cast<uint32_t*>(acc_rows),
-                          reinterpret_cast<uint32_t*>(dep_rows), B->arena.err, s);
+  int32_t* d_keys = nullptr;
+  if (key_list) {
+    GM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_keys), (size_t)n * 4, s));
+    GM_CUDA_TRY(cudaMemcpyAsync(d_keys, key_list, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+  }
+  st = launch_cache_build(g->dev, v->dev, B->arena, B->ovf, key_begin, d_keys, n,
+                          reinterpret_cast<uint32_t*>(acc_rows), reinterpret_cast<uint32_t*>(dep_rows),
+                          B->arena.err, s);
+  if (d_keys) cudaFreeAsync(d_keys, s);
   if (st) return st;
   uint32_t bits = 0;
   GM_CUDA_TRY(cudaMemcpyAsync(&bits, B->arena.err, 4, cudaMemcpyDeviceToHost, s));
   GM_CUDA_TRY(cudaStreamSynchronize(s));
   return err_bits_to_status(bits, "cache build");
 }
+
+gm_status gm_cache_build_rows(const gm_grammar* g, const gm_vocab* v, int32_t key_begin, int32_t n,
+                              int32_t* acc_rows, int32_t* dep_rows, void* stream) {
+  return cache_build(g, v, key_begin, nullptr, n, acc_rows, dep_rows, stream);
+}
+
+gm_status gm_cache_build_keys(const gm_grammar* g, const gm_vocab* v, const int32_t* key_list, int32_t n,
+                              int32_t* acc_rows, int32_t* dep_rows, void* stream) {
+  if (n > 0 && !key_list) return fail(GM_ERR_INVALID, "null key list");
+  return cache_build(g, v, 0, key_list, n, acc_rows, dep_rows, stream);
+}
+
+int32_t gm_grammar_num_keys(const gm_grammar* g) { return g ? g->dev.n_keys : 0; }
 
 gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t* acc_rows,
                           const int32_t* dep_rows, gm_cache** out, gm_cache_stats* stats, void* stream) {

@@ -26,12 +26,12 @@ constexpr int kBuildF = 96;   // walker-local frames
 
 __global__ void __launch_bounds__(128)
 cache_build_kernel(DevGrammar G, DevVocab Vc, DevArena A, DevOverflow O, int32_t key_begin,
-                   uint32_t* __restrict__ acc_rows, uint32_t* __restrict__ dep_rows,
-                   uint32_t* __restrict__ err_out) {
+                   const int32_t* __restrict__ key_list, uint32_t* __restrict__ acc_rows,
+                   uint32_t* __restrict__ dep_rows, uint32_t* __restrict__ err_out) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= Vc.n_sorted) return;
-  const int32_t k = blockIdx.y;
-  const int32_t key_node = G.cache_keys[key_begin + k];
+  const int32_t k = blockIdx.y;  // row k: key key_list[k] (position sharding) or key_begin + k
+  const int32_t key_node = G.cache_keys[key_list ? __ldg(key_list + k) : key_begin + k];
   const int32_t tid = __ldg(Vc.sorted_ids + j);
   const int32_t o0 = __ldg(Vc.off + tid);
   const int len = __ldg(Vc.off + tid + 1) - o0;
@@ -271,14 +271,15 @@ using namespace gm;
 
 namespace gm {
 gm_status launch_cache_build(const DevGrammar& G, const DevVocab& V, const DevArena& A, const DevOverflow& O,
-                             int32_t key_begin, int32_t n, uint32_t* acc, uint32_t* dep,
+                             int32_t key_begin, const int32_t* key_list, int32_t n, uint32_t* acc, uint32_t* dep,
                              uint32_t* err, cudaStream_t s) {
   if (n <= 0 || V.n_sorted == 0) return GM_OK;
   const int threads = 128;
   for (int32_t k0 = 0; k0 < n; k0 += 65535) {
     const int32_t kn = (n - k0) < 65535 ? (n - k0) : 65535;
     dim3 grid((unsigned)ceil_div(V.n_sorted, threads), (unsigned)kn);
-    cache_build_kernel<<<grid, threads, 0, s>>>(G, V, A, O, key_begin + k0, acc + (size_t)k0 * V.W,
+    cache_build_kernel<<<grid, threads, 0, s>>>(G, V, A, O, key_begin + k0, key_list ? key_list + k0 : nullptr,
+                                                acc + (size_t)k0 * V.W,
                                                 dep + (size_t)k0 * V.W, err);
     GM_LAUNCH_CHECK();
   }

@@ -180,37 +180,106 @@ def build_cache_rows(grammar: DeviceGrammar, dvocab: DeviceVocab, key_begin: int
     return acc, dep
 
 
+def build_cache_rows_keys(grammar: DeviceGrammar, dvocab: DeviceVocab, keys, stream=None):
+    """Rows of an arbitrary list of cache keys (position sharding)."""
+    lib = _lib.load()
+    keys = np.ascontiguousarray(np.asarray(keys, dtype=np.int32))
+    n = len(keys)
+    acc = torch.empty((n, dvocab.words), dtype=torch.int32, device=dvocab.device)
+    dep = torch.empty((n, dvocab.words), dtype=torch.int32, device=dvocab.device)
+    if n:
+        status = lib.gm_cache_build_keys(grammar.handle, dvocab.handle, keys.ctypes.data, n, acc.data_ptr(),
+                                         dep.data_ptr(), _lib.stream_ptr(stream))
+        if status == _lib.GM_ERR_STATE_CAP:
+            raise StateLimitError(lib.gm_last_error().decode())
+        _lib.check(status, "gm_cache_build_keys")
+    return acc, dep
+
+
 def shard_range(n_keys: int, world: int, rank: int):
-    """Contiguous block of cache keys owned by ``rank``."""
+    """Contiguous block of cache keys owned by ``rank`` (kept for callers
+    that want blocks; the build deals keys with ``shard_keys``)."""
     per = (n_keys + world - 1) // world if world else n_keys
     return min(rank * per, n_keys), min((rank + 1) * per, n_keys), per
 
 
-def sharded_rows(build, n_keys: int, words: int, device, group=None):
-    """Position-sharded cache rows: each rank builds its key block with
-    ``build(lo, n) -> (acc, dep)`` and one all-gather replicates the finished
-    rows to every rank (NCCL over NVLink on the GPU box; gloo in CPU tests).
-    Returns full (acc, dep) [n_keys, words] int32 identical on every rank."""
+def key_costs(tables: CompiledTables, vocab: Vocabulary) -> np.ndarray:
+    """Estimated K1 work per cache key: the token bytes whose
+    first byte the key's node can consume — a position inside a string walks
+    almost the whole sorted vocabulary, a structural one dies at byte 0 of
+    most tokens (SURVEY §7 hard part 3)."""
+    data, off = vocab.packed()
+    lens = np.diff(off)
+    nonempty = lens > 0
+    first = np.zeros(len(lens), dtype=np.int64)
+    first[nonempty] = data[off[:-1][nonempty]]
+    cls = np.asarray(tables.byte_class, dtype=np.int64)
+    C = int(tables.n_classes)
+    per_class = np.zeros(C, dtype=np.float64)
+    np.add.at(per_class, cls[first[nonempty]], lens[nonempty].astype(np.float64))
+    toff = np.asarray(tables.trans_off, dtype=np.int64)
+    keys = np.asarray(tables.cache_keys, dtype=np.int64)
+    out = np.empty(len(keys), dtype=np.float64)
+    for i, nd in enumerate(keys):
+        idx = nd * C + np.arange(C)
+        live = toff[idx + 1] > toff[idx]
+        out[i] = per_class[live].sum() + 1.0
+    return out
+
+
+def shard_keys(costs, world: int, rank: int) -> np.ndarray:
+    """Keys of ``rank``: all keys sorted by decreasing estimated cost (ties by
+    index), dealt round-robin over the ranks, so every rank gets
+    a share of the expensive string-interior positions."""
+    order = np.argsort(-np.asarray(costs, dtype=np.float64), kind="stable")
+    return order[rank::world].astype(np.int32)
+
+
+def _all_gather(out: torch.Tensor, inp: torch.Tensor, group):
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "gloo" and inp.is_cuda:  # gloo collectives run on host copies
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
+def sharded_rows(build, n_keys: int, words: int, device, group=None, costs=None):
+    """Position-sharded cache rows: each rank builds its keys with
+    ``build(keys) -> (acc, dep)`` (rows in ``keys`` order), one all-gather
+    replicates them and every rank puts them back in key order (NCCL over
+    NVLink on the GPU box; gloo in the CPU tests).  The result is identical
+    on every rank and bit-identical to the 1-rank build (REF SPEC.md:364).
+    Returns (acc, dep) [n_keys, words] int32."""
     world = 1
     if group is not None:
         import torch.distributed as dist
 
         world = dist.get_world_size(group)
+    if costs is None:
+        costs = np.zeros(n_keys)
     if world <= 1:
-        return build(0, n_keys)
+        return build(np.arange(n_keys, dtype=np.int32))
     import torch.distributed as dist
 
     rank = dist.get_rank(group)
-    lo, hi, per = shard_range(n_keys, world, rank)
-    acc_l, dep_l = build(lo, hi - lo)
+    per = (n_keys + world - 1) // world
+    mine = shard_keys(costs, world, rank)
+    acc_l, dep_l = build(mine)
     pad = torch.zeros((2, per, words), dtype=torch.int32, device=device)
-    pad[0, : hi - lo] = acc_l
-    pad[1, : hi - lo] = dep_l
+    pad[0, : len(mine)] = acc_l
+    pad[1, : len(mine)] = dep_l
     full = torch.empty((world * 2, per, words), dtype=torch.int32, device=device)
-    dist.all_gather_into_tensor(full, pad, group=group)
+    _all_gather(full, pad, group)
     full = full.view(world, 2, per, words)
-    acc = full[:, 0].reshape(world * per, words)[:n_keys].contiguous()
-    dep = full[:, 1].reshape(world * per, words)[:n_keys].contiguous()
+    acc = torch.empty((n_keys, words), dtype=torch.int32, device=device)
+    dep = torch.empty((n_keys, words), dtype=torch.int32, device=device)
+    for r in range(world):
+        keys_r = torch.from_numpy(shard_keys(costs, world, r).astype(np.int64)).to(device)
+        acc.index_copy_(0, keys_r, full[r, 0, : len(keys_r)])
+        dep.index_copy_(0, keys_r, full[r, 1, : len(keys_r)])
     return acc, dep
 
 
@@ -218,8 +287,9 @@ def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOp
                       root_rule_name: Optional[str] = None, group=None, stream=None,
                       uncached: bool = False) -> CompiledDeviceGrammar:
     """Front end + K1/K1b build.  With a torch.distributed ``group`` of size G
-    the cache keys are dealt round-robin-by-block across ranks and the rows
-    are replicated with one all-gather."""
+    the cache keys are dealt round-robin in decreasing order of estimated
+    cost (``key_costs``) and the rows replicated with one all-gather
+    (SURVEY §8e)."""
     t0 = time.perf_counter()
     tables = build_tables_native(parse_grammar(text, root_rule_name), opts)
     t1 = time.perf_counter()
@@ -234,8 +304,9 @@ def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOp
         acc = torch.zeros((n_keys, dvocab.words), dtype=torch.int32, device=dvocab.device)
         dep = torch.from_numpy(u.view(np.int32).copy()).to(dvocab.device).expand(n_keys, -1).contiguous()
     else:
-        acc, dep = sharded_rows(lambda lo, n: build_cache_rows(grammar, dvocab, lo, n, stream), n_keys,
-                                dvocab.words, dvocab.device, group)
+        costs = key_costs(tables, dvocab.vocab) if group is not None else None
+        acc, dep = sharded_rows(lambda keys: build_cache_rows_keys(grammar, dvocab, keys, stream), n_keys,
+                                dvocab.words, dvocab.device, group, costs)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     cache = DeviceCache(grammar, dvocab, acc, dep, stream)

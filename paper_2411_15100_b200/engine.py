@@ -26,7 +26,7 @@ from .grammar import parse_grammar
 from .vocab import Vocabulary
 
 __all__ = ["MatcherError", "RequestErrors", "DeviceVocab", "DeviceGrammar", "DeviceCache", "CompiledDeviceGrammar",
-           "MatcherPool", "compile_on_device", "get_pool"]
+           "MatcherPool", "compile_on_device", "compile_many_on_device", "get_pool"]
 
 
 class MatcherError(RuntimeError):
@@ -248,7 +248,8 @@ def _all_gather(out: torch.Tensor, inp: torch.Tensor, group):
 
 def sharded_rows(build, n_keys: int, words: int, device, group=None, costs=None):
     """Position-sharded cache rows: each rank builds its keys with
-    ``build(keys) -> (acc, dep)`` (rows in ``keys`` order), one all-gather
+    ``build(keys) -> (acc, dep)`` (rows in ``keys`` order; keys None = all,
+    in order, for a single rank), one all-gather
     replicates them and every rank puts them back in key order (NCCL over
     NVLink on the GPU box; gloo in the CPU tests).  The result is identical
     on every rank and bit-identical to the 1-rank build (REF SPEC.md:364).
@@ -261,7 +262,7 @@ def sharded_rows(build, n_keys: int, words: int, device, group=None, costs=None)
     if costs is None:
         costs = np.zeros(n_keys)
     if world <= 1:
-        return build(np.arange(n_keys, dtype=np.int32))
+        return build(None)
     import torch.distributed as dist
 
     rank = dist.get_rank(group)
@@ -305,8 +306,12 @@ def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOp
         dep = torch.from_numpy(u.view(np.int32).copy()).to(dvocab.device).expand(n_keys, -1).contiguous()
     else:
         costs = key_costs(tables, dvocab.vocab) if group is not None else None
-        acc, dep = sharded_rows(lambda keys: build_cache_rows_keys(grammar, dvocab, keys, stream), n_keys,
-                                dvocab.words, dvocab.device, group, costs)
+        def build(keys):  # None: every key (one contiguous range)
+            if keys is None:
+                return build_cache_rows(grammar, dvocab, 0, n_keys, stream)
+            return build_cache_rows_keys(grammar, dvocab, keys, stream)
+
+        acc, dep = sharded_rows(build, n_keys, dvocab.words, dvocab.device, group, costs)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     cache = DeviceCache(grammar, dvocab, acc, dep, stream)
@@ -314,6 +319,76 @@ def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOp
     timings = {"front_end": (t1 - t0) * 1e3, "cache_build": (t2 - t1) * 1e3, "assemble": (t3 - t2) * 1e3,
                "total": (t3 - t0) * 1e3}
     return CompiledDeviceGrammar(tables, grammar, cache, dvocab, timings)
+
+
+def compile_many_on_device(texts, dvocab: DeviceVocab, opts: Optional[AutomatonOptions] = None, *, group=None,
+                           stream=None):
+    """BASELINE config 5's build: every rank ends with ALL grammars compiled,
+    the work sharded by grammar position across the group ("all
+    positions of all schemas").  The host front end is dealt round-robin over
+    the ranks and the tables exchanged (all_gather_object); the (grammar,
+    key) pairs of all grammars are dealt round-robin in decreasing order of
+    estimated cost; one all-gather of the padded rows replicates them.
+    Returns (list of CompiledDeviceGrammar, stats with the per-rank bytes
+    moved and phase ms).  Compare: per-rank compile (each rank compiles only
+    the grammars of the requests it serves; no exchange)."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if group is not None else 1
+    rank = dist.get_rank(group) if group is not None else 0
+    t0 = time.perf_counter()
+    mine = {i: build_tables_native(parse_grammar(texts[i]), opts) for i in range(rank, len(texts), world)}
+    t1 = time.perf_counter()
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, mine, group=group)
+        tables = {}
+        for part in parts:
+            tables.update(part)
+    else:
+        tables = mine
+    t2 = time.perf_counter()
+    grammars = [DeviceGrammar(tables[i]) for i in range(len(texts))]
+    pairs, costs = [], []
+    for i in range(len(texts)):
+        c = key_costs(tables[i], dvocab.vocab)
+        pairs += [(i, k) for k in range(len(c))]
+        costs.append(c)
+    costs = np.concatenate(costs) if costs else np.zeros(0)
+    n = len(pairs)
+    W = dvocab.words
+
+    def build(sel):
+        if sel is None:
+            sel = np.arange(n)
+        acc = torch.empty((len(sel), W), dtype=torch.int32, device=dvocab.device)
+        dep = torch.empty((len(sel), W), dtype=torch.int32, device=dvocab.device)
+        by_g = {}
+        for j, p in enumerate(sel):
+            by_g.setdefault(pairs[p][0], []).append((j, pairs[p][1]))
+        for gi, lst in by_g.items():
+            a, d = build_cache_rows_keys(grammars[gi], dvocab, [k for _, k in lst], stream)
+            idx = torch.tensor([j for j, _ in lst], dtype=torch.int64, device=dvocab.device)
+            acc.index_copy_(0, idx, a)
+            dep.index_copy_(0, idx, d)
+        return acc, dep
+
+    acc, dep = sharded_rows(build, n, W, dvocab.device, group if world > 1 else None, costs)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    out, at = [], 0
+    for i, g in enumerate(grammars):
+        nk = g.n_keys
+        cache = DeviceCache(g, dvocab, acc[at:at + nk].contiguous(), dep[at:at + nk].contiguous(), stream)
+        out.append(CompiledDeviceGrammar(tables[i], g, cache, dvocab, {}))
+        at += nk
+    t4 = time.perf_counter()
+    per = (n + world - 1) // world
+    stats = {"grammars": len(texts), "positions": n, "world": world,
+             "front_end_ms": (t1 - t0) * 1e3, "tables_exchange_ms": (t2 - t1) * 1e3,
+             "cache_build_ms": (t3 - t2) * 1e3, "assemble_ms": (t4 - t3) * 1e3, "total_ms": (t4 - t0) * 1e3,
+             "allgather_bytes_in_per_rank": (world - 1) * per * 2 * W * 4 if world > 1 else 0}
+    return out, stats
 
 
 # ---------------------------------------------------------------------------

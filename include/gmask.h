@@ -377,8 +377,20 @@ gm_status gm_pool_check(gm_pool* p, int32_t* flags_out);
 gm_status gm_pool_errors(gm_pool* p, const int32_t* slots, int32_t n,
                          uint32_t* out, int32_t clear, void* stream);
 gm_status gm_status_of_error_bits(uint32_t bits);
-/* arena statistics: live entries */
+/* Arena statistics (syncs): live frames, tombstones, capacity (slots). */
+gm_status gm_pool_arena_stats(gm_pool* p, int64_t* live, int64_t* tombstones,
+                              int64_t* capacity);
+/* live frames (gm_pool_arena_stats), -1 on error */
 int64_t gm_pool_arena_used(gm_pool* p);
+/* Reclaim arena frames (REF pstack.py:85-111 decref / end_log: frames no
+ * live stack references are freed).  live_slots (HOST int32[n]) lists every
+ * slot whose state must survive; every other slot's history is dropped.
+ * Frames reachable from a top of a live slot's history-ring entries (the
+ * rollback window) are kept; the rest become free again.  Handles never
+ * move, so live state is untouched.  Stream-ordered: no step kernel on
+ * this pool may run concurrently on another stream. */
+gm_status gm_pool_collect(gm_pool* p, const int32_t* live_slots, int32_t n,
+                          void* stream);
 /* Diagnostics: phase timestamps (ns, %globaltimer) of CTA 0 of the last
  * accept (out[0..16)) and fill (out[16..32)) launches, then per-CTA
  * durations (fill: out[64 + 2i], accept: out[64 + 2*capacity + i]) when the

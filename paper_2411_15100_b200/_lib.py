@@ -126,6 +126,8 @@ _SIGNATURES = {
     "gm_pool_errors": ([_P, _P, _I32, _P, _I32, _P], _I32),
     "gm_status_of_error_bits": ([C.c_uint32], _I32),
     "gm_pool_arena_used": ([_P], _I64),
+    "gm_pool_arena_stats": ([_P, _P, _P, _P], _I32),
+    "gm_pool_collect": ([_P, _P, _I32, _P], _I32),
     "gm_pool_trace": ([_P, _P, _I64], _I32),
     "gm_front_end_build": ([_P, _I64, _I32, _I32, C.POINTER(gm_fe_options), C.POINTER(_P),
                             C.POINTER(gm_fe_tables)], _I32),

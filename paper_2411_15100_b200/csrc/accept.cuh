@@ -52,7 +52,7 @@ __device__ inline void chain_from_arena(const DevPool& P, int32_t h, Chain& c) {
   c.n = 0;
   while (h >= 0 && c.n < kChain) {
     const unsigned long long k = arena_load(P.arena, h);
-    if (k == kEmptyKey) break;
+    if (k >= kTombKey) break;
     c.h[c.n] = h;
     c.k[c.n] = k;
     ++c.n;

@@ -226,14 +226,36 @@ __device__ __forceinline__ int32_t key_parent(unsigned long long k) { return (in
 __device__ __forceinline__ int32_t key_node(unsigned long long k) { return (int32_t)((uint32_t)k >> 1); }
 __device__ __forceinline__ uint32_t key_term(unsigned long long k) { return (uint32_t)k & 1u; }
 
+// Tombstone: a slot whose frame was reclaimed by the pool's collector
+// (gm_pool_collect) while a live key further along the same probe chain
+// still needs the chain unbroken.  Never a valid key (parent+1 < 2^31).
+constexpr unsigned long long kTombKey = ~1ull;
+
 // Handle of `key`, inserting it if absent, probing linearly from `start`;
-// -1 + error bit when the table is full.
+// -1 + error bit when the table is full.  Keys are only ever inserted at
+// the first empty-or-tombstone slot of their probe chain, and the collector
+// keeps every slot between a live key's home and its position non-empty, so
+// reaching an EMPTY slot proves the key absent.  A tombstone is reused only
+// after the scan has proved the key absent; a lost race rescans (slots only
+// fill while kernels run, so two racing inserts of one key claim the same
+// first free slot).
 __device__ inline int32_t arena_probe(const DevArena& A, unsigned long long key, uint32_t start) {
-  uint32_t i = start & A.mask;
-  for (int probe = 0; probe < 8192; ++probe) {
-    const unsigned long long cur = atomicCAS(A.keys + i, kEmptyKey, key);
-    if (cur == kEmptyKey || cur == key) return (int32_t)i;
-    i = (i + 1) & A.mask;
+  for (int attempt = 0; attempt < 64; ++attempt) {
+    uint32_t i = start & A.mask;
+    int64_t tomb = -1;
+    int probe = 0;
+    for (; probe < 8192; ++probe) {
+      const unsigned long long cur = arena_load(A, (int32_t)i);
+      if (cur == key) return (int32_t)i;
+      if (cur == kEmptyKey) break;
+      if (cur == kTombKey && tomb < 0) tomb = i;
+      i = (i + 1) & A.mask;
+    }
+    if (probe == 8192 && tomb < 0) break;  // full
+    const uint32_t at = tomb >= 0 ? (uint32_t)tomb : i;
+    const unsigned long long expect = tomb >= 0 ? kTombKey : kEmptyKey;
+    const unsigned long long old = atomicCAS(A.keys + at, expect, key);
+    if (old == expect || old == key) return (int32_t)at;
   }
   if (A.err) atomicOr(A.err, kErrArena);
   return -1;
@@ -285,7 +307,7 @@ struct Walker {
   }
 
   __device__ __forceinline__ void know(int32_t h, unsigned long long key) {
-    if (h < 0 || key == kEmptyKey || nk == K) return;
+    if (h < 0 || key >= kTombKey || nk == K) return;
     for (int i = 0; i < nk; ++i)
       if (kh[i] == h) return;
     kh[nk] = h; kk[nk] = key; ++nk;
@@ -300,7 +322,7 @@ struct Walker {
       return k;
     }
     k = arena_load(A, h);
-    if (k == kEmptyKey) err |= kErrInvalid;  // dangling handle: report, never walk garbage
+    if (k >= kTombKey) err |= kErrInvalid;  // dangling handle: report, never walk garbage
     else know(h, k);
     return k;
   }
@@ -322,7 +344,7 @@ struct Walker {
   __device__ __forceinline__ void pop(const DevArena& A, int32_t r, int32_t& pr, int32_t& pn) {
     if (r >= 0) { pr = fpar[r]; pn = fnode[r]; return; }
     const unsigned long long k = key_of(A, -2 - r);
-    if (k == kEmptyKey) { pr = -1; pn = 0; return; }  // reported by key_of
+    if (k >= kTombKey) { pr = -1; pn = 0; return; }  // reported by key_of
     const int32_t p = key_parent(k);
     pr = p < 0 ? -1 : -2 - p;
     pn = key_node(k);
@@ -512,7 +534,7 @@ struct RWalker {
   __device__ __forceinline__ void pop(const DevArena& A, int32_t r, int32_t& pr, int32_t& pn) {
     if (r >= 0 && r < kChainRef) { pr = fpar[r]; pn = fnode[r]; return; }
     const unsigned long long k = global_key(A, r);
-    if (k == kEmptyKey) { err |= kErrInvalid; pr = -1; pn = 0; return; }
+    if (k >= kTombKey) { err |= kErrInvalid; pr = -1; pn = 0; return; }
     pn = key_node(k);
     if (r >= kChainRef && r - kChainRef + 1 < nx) { pr = r + 1; return; }
     const int32_t p = key_parent(k);
@@ -787,12 +809,12 @@ struct BigWalk {
   __device__ uint32_t term_of(const DevArena& A, int32_t h) {
     if (h < 0) return 1u;
     const unsigned long long k = arena_load(A, h);
-    if (k == kEmptyKey) { err |= kErrInvalid; return 0u; }
+    if (k >= kTombKey) { err |= kErrInvalid; return 0u; }
     return key_term(k);
   }
   __device__ void pop(const DevArena& A, int32_t h, int32_t& ph, int32_t& pn) {
     const unsigned long long k = arena_load(A, h);
-    if (k == kEmptyKey) { err |= kErrInvalid; ph = -1; pn = 0; return; }
+    if (k >= kTombKey) { err |= kErrInvalid; ph = -1; pn = 0; return; }
     ph = key_parent(k);
     pn = key_node(k);
   }

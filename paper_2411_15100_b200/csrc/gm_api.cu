@@ -26,6 +26,8 @@ gm_status fail(gm_status code, const std::string& msg) {
 gm_status launch_cache_build(const DevGrammar&, const DevVocab&, const DevArena&, const DevOverflow&, int32_t,
                              const int32_t*, int32_t, uint32_t*, uint32_t*, uint32_t*, cudaStream_t);
 gm_status launch_pool_errors(const DevPool&, const int32_t*, int32_t, uint32_t*, int32_t, cudaStream_t);
+gm_status launch_collect(const DevPool&, const int32_t*, int32_t, uint32_t*, uint32_t*, cudaStream_t);
+gm_status launch_arena_count(const DevArena&, unsigned long long*, cudaStream_t);
 gm_status launch_row_popcount(const uint32_t*, int32_t, int32_t, int64_t*, cudaStream_t);
 gm_status launch_dep_compact(const uint32_t*, int32_t, int32_t, const int32_t*, int32_t*, cudaStream_t);
 gm_status launch_dep_records(const int32_t*, int64_t, const int4*, int4*, cudaStream_t);
@@ -191,6 +193,9 @@ struct gm_pool {
   int64_t scratch_cap;
   int32_t* scratch_i32;    // probe outputs
   int32_t max_w;
+  uint32_t* gc_mark = nullptr;  // collector bitmaps (arena slots / 32 words each)
+  uint32_t* gc_need = nullptr;
+  unsigned long long* counts = nullptr;
 };
 
 // Pools that may hold bindings to a cache: gm_cache_release unbinds the
@@ -1133,14 +1138,41 @@ gm_status gm_pool_trace(gm_pool* p, uint64_t* out, int64_t n) {
   return GM_OK;
 }
 
+gm_status gm_pool_arena_stats(gm_pool* p, int64_t* live, int64_t* tombstones, int64_t* capacity) {
+  if (!p) return fail(GM_ERR_INVALID, "null pool");
+  gm_status st;
+  if (!p->counts && (st = p->mem.alloc(&p->counts, 2))) return st;
+  if ((st = launch_arena_count(p->dev.arena, p->counts, 0))) return st;
+  unsigned long long c[2];
+  GM_CUDA_TRY(cudaMemcpy(c, p->counts, 16, cudaMemcpyDeviceToHost));
+  if (live) *live = (int64_t)c[0];
+  if (tombstones) *tombstones = (int64_t)c[1];
+  if (capacity) *capacity = (int64_t)p->dev.arena.mask + 1;
+  return GM_OK;
+}
+
 int64_t gm_pool_arena_used(gm_pool* p) {
-  if (!p) return -1;
-  // counted on the host: cheap enough for diagnostics
-  std::vector<unsigned long long> keys((size_t)p->dev.arena.mask + 1);
-  if (cudaMemcpy(keys.data(), p->dev.arena.keys, keys.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  int64_t used = 0;
-  for (auto k : keys) used += (k != kEmptyKey);
-  return used;
+  int64_t live = -1;
+  if (gm_pool_arena_stats(p, &live, nullptr, nullptr)) return -1;
+  return live;
+}
+
+gm_status gm_pool_collect(gm_pool* p, const int32_t* live_slots, int32_t n, void* stream) {
+  if (!p || n < 0 || (n > 0 && !live_slots)) return fail(GM_ERR_INVALID, "bad collect arguments");
+  for (int32_t i = 0; i < n; ++i)
+    if (live_slots[i] < 0 || live_slots[i] >= p->dev.capacity) return fail(GM_ERR_INVALID, "slot out of range");
+  gm_status st;
+  const size_t words = ((size_t)p->dev.arena.mask + 1) / 32;
+  if (!p->gc_mark && ((st = p->mem.alloc(&p->gc_mark, words)) || (st = p->mem.alloc(&p->gc_need, words)))) return st;
+  cudaStream_t s = as_stream(stream);
+  int32_t* d_live = nullptr;
+  if (n > 0) {
+    GM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d_live), (size_t)n * 4, s));
+    GM_CUDA_TRY(cudaMemcpyAsync(d_live, live_slots, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+  }
+  st = launch_collect(p->dev, d_live, n, p->gc_mark, p->gc_need, s);
+  if (d_live) cudaFreeAsync(d_live, s);
+  return st;
 }
 
 }  // extern "C"

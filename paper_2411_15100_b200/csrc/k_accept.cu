@@ -207,6 +207,100 @@ __global__ void fork_kernel(DevPool P, int32_t src, int32_t dst) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Arena collection (REF pstack.py:85-111 reclaims frames by refcount; here a
+// mark / sweep over the live slots' histories, run between steps).
+//   mark:    every frame reachable from a top of a live slot's history ring
+//            entries (the rollback window, REF matcher.py:239-244, 310-326)
+//   sweep:   unmarked frames -> tombstones
+//   need:    every slot between a live key's home and its position
+//   compact: tombstones no live key's probe chain crosses -> empty
+// Handles are slots and never move, so nothing else is rewritten.
+__global__ void gc_mark_kernel(DevPool P, const int32_t* __restrict__ live, int32_t n, uint32_t* __restrict__ mark) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n * P.H) return;
+  const int32_t slot = live[t / P.H];
+  const int32_t k = (int32_t)(t % P.H);
+  if (slot < 0 || slot >= P.capacity || k > P.hist_len[slot]) return;
+  const int32_t h = ((P.head[slot] - k) % P.H + P.H) % P.H;
+  const int nt = P.meta[(size_t)slot * P.H + h] & 0xFFFF;
+  const int2* tops = ring_tops(P, slot, h, nt);
+  for (int s = 0; s < nt; ++s) {
+    int32_t hh = tops[s].x;
+    while (hh >= 0 && (uint32_t)hh <= P.arena.mask) {
+      const uint32_t bit = 1u << (hh & 31);
+      if (atomicOr(mark + (hh >> 5), bit) & bit) break;  // this frame's ancestors are marked already
+      const unsigned long long key = P.arena.keys[hh];
+      if (key >= kTombKey) break;
+      hh = key_parent(key);
+    }
+  }
+}
+
+__global__ void gc_sweep_kernel(DevArena A, const uint32_t* __restrict__ mark) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > A.mask) return;
+  const unsigned long long key = A.keys[i];
+  if (key < kTombKey && !(mark[i >> 5] & (1u << (i & 31)))) A.keys[i] = kTombKey;
+}
+
+__global__ void gc_need_kernel(DevArena A, uint32_t* __restrict__ need) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > A.mask) return;
+  const unsigned long long key = A.keys[i];
+  if (key >= kTombKey) return;
+  for (uint32_t q = mix64(key) & A.mask; q != i; q = (q + 1) & A.mask) atomicOr(need + (q >> 5), 1u << (q & 31));
+}
+
+__global__ void gc_compact_kernel(DevArena A, const uint32_t* __restrict__ need) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > A.mask) return;
+  if (A.keys[i] == kTombKey && !(need[i >> 5] & (1u << (i & 31)))) A.keys[i] = kEmptyKey;
+}
+
+// live frames / tombstones
+__global__ void arena_count_kernel(DevArena A, unsigned long long* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long live = 0, tomb = 0;
+  if (i <= A.mask) {
+    const unsigned long long key = A.keys[i];
+    live = key < kTombKey;
+    tomb = key == kTombKey;
+  }
+  live = __reduce_add_sync(0xFFFFFFFFu, (unsigned)live);
+  tomb = __reduce_add_sync(0xFFFFFFFFu, (unsigned)tomb);
+  if ((threadIdx.x & 31) == 0) {
+    if (live) atomicAdd(out, live);
+    if (tomb) atomicAdd(out + 1, tomb);
+  }
+}
+
+gm_status launch_collect(const DevPool& P, const int32_t* live, int32_t n, uint32_t* mark, uint32_t* need,
+                         cudaStream_t s) {
+  const size_t words = ((size_t)P.arena.mask + 1) / 32;
+  const unsigned blocks = (unsigned)ceil_div((int64_t)P.arena.mask + 1, 256);
+  GM_CUDA_TRY(cudaMemsetAsync(mark, 0, words * 4, s));
+  GM_CUDA_TRY(cudaMemsetAsync(need, 0, words * 4, s));
+  if (n > 0) {
+    gc_mark_kernel<<<(unsigned)ceil_div((int64_t)n * P.H, 128), 128, 0, s>>>(P, live, n, mark);
+    GM_LAUNCH_CHECK();
+  }
+  gc_sweep_kernel<<<blocks, 256, 0, s>>>(P.arena, mark);
+  GM_LAUNCH_CHECK();
+  gc_need_kernel<<<blocks, 256, 0, s>>>(P.arena, need);
+  GM_LAUNCH_CHECK();
+  gc_compact_kernel<<<blocks, 256, 0, s>>>(P.arena, need);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+
+gm_status launch_arena_count(const DevArena& A, unsigned long long* out, cudaStream_t s) {
+  GM_CUDA_TRY(cudaMemsetAsync(out, 0, 16, s));
+  arena_count_kernel<<<(unsigned)ceil_div((int64_t)A.mask + 1, 256), 256, 0, s>>>(A, out);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+
 // Per-slot error words of `slots` (gathered; cleared with `clear`).
 __global__ void pool_errors_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ out,
                                    int32_t clear) {

@@ -118,7 +118,7 @@ __device__ __forceinline__ void context_of(const DevPool& P, const SlotHdr& hd, 
   cj = -1;
   const bool on_chain = hd.nchain > 0 && hd.chain_h[0] == t.x;
   const unsigned long long pk = on_chain ? hd.chain_k[0] : arena_load(P.arena, t.x);
-  if (pk == kEmptyKey) return;
+  if (pk >= kTombKey) return;
   const int32_t pn = key_node(pk);
   const int32_t* cr = G.callers + (size_t)G.node_rule[t.y] * kMaxCallers;
   for (int j = 0; j < kRootCaller; ++j) {
@@ -134,7 +134,7 @@ __device__ __forceinline__ void context_of(const DevPool& P, const SlotHdr& hd, 
   }
   const unsigned long long k2 =
       (on_chain && hd.nchain > 1 && hd.chain_h[1] == h2) ? hd.chain_k[1] : arena_load(P.arena, h2);
-  if (k2 == kEmptyKey) return;
+  if (k2 >= kTombKey) return;
   const int32_t pn2 = key_node(k2);
   const int32_t* cr2 = G.callers + (size_t)G.node_rule[pn] * kMaxCallers;
   for (int j = 0; j < kRootCaller; ++j) {

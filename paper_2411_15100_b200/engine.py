@@ -457,6 +457,38 @@ class MatcherPool:
             raise exc
         raise RequestErrors(bad)
 
+    def live_slots(self) -> list:
+        """Slots currently handed out to matchers."""
+        with self._lock:
+            free = set(self._free)
+        return [s for s in range(self.capacity) if s not in free]
+
+    def arena_stats(self) -> dict:
+        """Frames in the device arena (syncs): live, tombstones, capacity."""
+        live, tomb, cap = C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.check(_lib.load().gm_pool_arena_stats(self.handle, C.byref(live), C.byref(tomb), C.byref(cap)),
+                   "gm_pool_arena_stats")
+        return {"live": live.value, "tombstones": tomb.value, "capacity": cap.value,
+                "occupancy": (live.value + tomb.value) / max(cap.value, 1)}
+
+    def collect(self, stream=None, live_slots=None) -> None:
+        """Reclaim the arena frames no live matcher references (REF
+        pstack.py:85-111).  Stream-ordered; no step on this pool may run on
+        another stream meanwhile.  ``live_slots`` defaults to every slot
+        handed out."""
+        live = np.ascontiguousarray(np.asarray(self.live_slots() if live_slots is None else live_slots,
+                                               dtype=np.int32))
+        _lib.check(_lib.load().gm_pool_collect(self.handle, live.ctypes.data if len(live) else None, len(live),
+                                               _lib.stream_ptr(stream)), "gm_pool_collect")
+
+    def maybe_collect(self, threshold: float = 0.5, stream=None) -> bool:
+        """Collect when live + tombstoned frames exceed ``threshold`` of the
+        arena (syncs for the count)."""
+        if self.arena_stats()["occupancy"] <= threshold:
+            return False
+        self.collect(stream)
+        return True
+
     def __del__(self):
         if getattr(self, "handle", None) is not None and _lib._lib is not None:
             _lib._lib.gm_pool_release(self.handle)

@@ -133,7 +133,11 @@ class DecodeLoop:
     """
 
     def __init__(self, matchers: Sequence[GrammarMatcher], bitmask, logits: Sequence[torch.Tensor],
-                 recycle: bool = True, stream: Optional[torch.cuda.Stream] = None):
+                 recycle: bool = True, stream: Optional[torch.cuda.Stream] = None, collect_every: int = 0,
+                 collect_threshold: float = 0.5):
+        """``collect_every`` > 0: every that many steps, reclaim arena frames
+        no live matcher references once the arena is more than
+        ``collect_threshold`` full (MatcherPool.maybe_collect; syncs)."""
         import ctypes as C
 
         from . import _lib
@@ -170,6 +174,10 @@ class DecodeLoop:
         self._sptr = int(self.stream.cuda_stream)
         self._tok = np.zeros(self.B, dtype=np.int32)
         self._flags = np.zeros(self.B, dtype=np.uint8)
+        self.collect_every = collect_every
+        self.collect_threshold = collect_threshold
+        self._steps = 0
+        self.collections = 0
 
     def step(self, tokens, i: int = 0) -> None:
         """Issue one decode step on buffer i (tokens: host ints, or None for
@@ -183,6 +191,10 @@ class DecodeLoop:
         st = self._lib.gm_decoder_step(self._h, i, ptr, self._sptr)
         if st:
             self._check(st, "gm_decoder_step")
+        self._steps += 1
+        if self.collect_every and self._steps % self.collect_every == 0:
+            with torch.cuda.stream(self.stream):  # stream-ordered after this step's K5
+                self.collections += self._pool.maybe_collect(self.collect_threshold, self.stream)
 
     def flags(self, i: int = 0, out: Optional[np.ndarray] = None, wait: bool = True,
               raise_errors: bool = True) -> np.ndarray:

@@ -226,6 +226,11 @@ std::vector<int> eps_close(const Nfa& a, std::vector<int> states, std::vector<ch
   return states;
 }
 
+// subset construction over max_states states (caught: eps_free fallback)
+struct DfaLimit : GrammarFail {
+  using GrammarFail::GrammarFail;
+};
+
 Dfa determinize(const Nfa& a, int n_classes, int max_states) {
   std::vector<char> mark(a.byte.size(), 0), is_final(a.byte.size(), 0);
   for (int f : a.finals) is_final[f] = 1;
@@ -257,8 +262,8 @@ Dfa determinize(const Nfa& a, int n_classes, int max_states) {
       ids.emplace(T, id);
       order.push_back(std::move(T));
       if ((int)order.size() > max_states)
-        throw GrammarFail("rule automaton exceeds " + std::to_string(max_states) +
-                          " states after determinisation");
+        throw DfaLimit("rule automaton exceeds " + std::to_string(max_states) +
+                       " states after determinisation");
       return id;
     };
     std::vector<std::pair<int, int>> row, crow;
@@ -280,6 +285,57 @@ Dfa determinize(const Nfa& a, int n_classes, int max_states) {
     d.finals.push_back(fin);
   }
   return d;
+}
+
+// Fallback when the subset construction of a rule would exceed
+// max_dfa_states (e.g. `[ab]* "a" [ab]{20}`, 2^21 subsets): the rule keeps
+// an epsilon-free NFA instead.  A node per NFA state reached by a byte or
+// call edge (plus the start); its moves are the edges of every state of its
+// epsilon closure, so a (node, class) may lead to several targets and the
+// walkers carry one stack per live target — what the reference's Thompson
+// automaton does at run time (REF pda.py:246-329), bounded by the same
+// 4096-stack cap.  The language is unchanged, so masks are too.
+Dfa eps_free(const Nfa& a, int n_classes) {
+  std::vector<char> mark(a.byte.size(), 0), is_final(a.byte.size(), 0);
+  for (int f : a.finals) is_final[f] = 1;
+  std::vector<int> id(a.byte.size(), -1), order{a.start};
+  id[a.start] = 0;
+  auto node = [&](int v) {
+    if (id[v] < 0) {
+      id[v] = (int)order.size();
+      order.push_back(v);
+    }
+    return id[v];
+  };
+  Dfa d;
+  for (size_t i = 0; i < order.size(); ++i) {
+    const std::vector<int> C = eps_close(a, {order[i]}, mark);
+    std::vector<std::pair<int, int>> row, crow;
+    bool fin = false;
+    for (int u : C) {
+      fin |= is_final[u];
+      for (auto& e : a.byte[u])
+        for (int c = 0; c < n_classes; ++c)
+          if (e.first.test(c)) row.push_back({c, node(e.second)});
+      for (auto& e : a.call[u]) crow.push_back({e.first, node(e.second)});
+    }
+    std::sort(row.begin(), row.end());
+    row.erase(std::unique(row.begin(), row.end()), row.end());
+    std::sort(crow.begin(), crow.end());
+    crow.erase(std::unique(crow.begin(), crow.end()), crow.end());
+    d.trans.push_back(std::move(row));
+    d.calls.push_back(std::move(crow));
+    d.finals.push_back(fin);
+  }
+  return d;
+}
+
+Dfa det_or_nfa(const Nfa& a, int n_classes, int max_states) {
+  try {
+    return determinize(a, n_classes, max_states);
+  } catch (const DfaLimit&) {
+    return eps_free(a, n_classes);
+  }
 }
 
 Dfa minimize(const Dfa& d) {
@@ -459,7 +515,7 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
     Builder bld(ir, R.byte_class.data());
     bld.a.start = bld.a.add();
     bld.a.finals = {bld.emit(body[r], bld.a.start)};
-    dfas[r] = minimize(determinize(bld.a, n_classes, o.max_dfa_states));
+    dfas[r] = minimize(det_or_nfa(bld.a, n_classes, o.max_dfa_states));
   }
   if (o.inline_rules) {
     for (int pass = 0; pass < 64; ++pass) {
@@ -500,7 +556,12 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
           for (auto& e : cs)
             if (inl[e.first] && e.first != host) targets[e.first] = &snap[e.first];
         if (targets.empty()) continue;
-        Dfa nd = minimize(determinize(inline_into(dfas[host], targets), n_classes, o.max_dfa_states));
+        Dfa nd;
+        try {
+          nd = minimize(determinize(inline_into(dfas[host], targets), n_classes, o.max_dfa_states));
+        } catch (const DfaLimit&) {
+          continue;  // inlining here would blow the subset construction up: keep the calls
+        }
         if (nd.size() > o.inline_max_result_states) continue;
         dfas[host] = std::move(nd);
         changed = true;

@@ -167,3 +167,25 @@ def test_native_front_end_errors():
 
     with pytest.raises(StateLimitError):
         build_tables_native(parse_grammar('root ::= root "a" | "b"'))
+
+
+def test_dfa_limit_falls_back_to_nfa():
+    """A rule whose subset construction would exceed max_dfa_states (2^18
+    subsets here) keeps an epsilon-free NFA (front_end.cpp eps_free): same
+    language, several targets per (node, class)."""
+    import random
+    import re
+
+    import numpy as np
+
+    from paper_2411_15100_b200.automaton import AutomatonOptions, build_tables_native
+    from paper_2411_15100_b200.grammar import parse_grammar
+
+    t = build_tables_native(parse_grammar('root ::= [ab]* "a" [ab]{17} "."'), AutomatonOptions())
+    assert np.diff(t.trans_off).max() >= 2 and t.n_nodes < 100
+    sim = TableSim(t)
+    rx = re.compile(rb"[ab]*a[ab]{17}\.")
+    rng = random.Random(3)
+    for _ in range(300):
+        s = bytes(rng.choice(b"ab") for _ in range(rng.randrange(15, 26))) + (b"." if rng.random() < 0.8 else b"")
+        assert sim.accepts(s) == bool(rx.fullmatch(s)), s

@@ -8,6 +8,9 @@ grammask).
   the batched wide fill must reproduce the reference's masks bit for bit,
   through the grammask API (K2 + K4), the batched XGrammar API and the fused
   K5 step.
+* ``dfa_blowup`` (``[ab]* "a" [ab]{17} "."``): over the front end's 200k
+  DFA-state limit, so the rule stays an epsilon-free NFA (front_end.cpp
+  eps_free) with up to 18 live stacks — same masks as the reference.
 * ``ambig_over_cap`` (4200 alternatives): the reference's compile raises
   StateLimitError (REF cache.py:58, 137-138); so does ours.
 * errors are attributed to the request that caused them (per-slot error
@@ -40,7 +43,7 @@ def caps_vocab():
     return vocab_from_tokens(toks, eos_id=len(toks) - 1, special=[len(toks) - 1])
 
 
-CASES = ["ambig40", "ambig300", "deep_ambig"]
+CASES = ["ambig40", "ambig300", "deep_ambig", "dfa_blowup"]
 
 
 @pytest.mark.parametrize("case", CASES)

@@ -14,6 +14,9 @@ Writes tests/golden/caps.json.gz:
   cache build raises StateLimitError (cap 4096, REF cache.py:58, 137-138) —
   so must ours (more than kWideCap = 4096 stacks).
 * ``ambig300``: 300 alternatives (wide ring entries and batched fills).
+* ``dfa_blowup``: ``[ab]* "a" [ab]{17} "."`` — its subset construction
+  would need 2^18 states (over the front end's 200k limit), so the rule keeps
+  an epsilon-free NFA and the walkers carry up to 18 stacks.
 * ``deep_ambig``: nested ambiguity (two alternatives per level and 12
   levels of nesting: a ::= "(" a ")" | "(" b ")" ...), masks after every
   prefix.
@@ -52,7 +55,8 @@ q ::= "(" item ")" | "(" "b" ")" | "b"
 
 
 def caps_vocab():
-    toks = [b"x", b"y", b"z", b"xx", b"xxx", b"yy", b"yyy", b"(", b")", b"((", b"))", b"a", b"b", b"(a", b"b)"]
+    toks = [b"x", b"y", b"z", b"xx", b"xxx", b"yy", b"yyy", b"(", b")", b"((", b"))", b"a", b"b", b"(a", b"b)",
+            b"ab", b"ba", b"aa", b"bb", b"aab", b"bab", b"abba", b".", b"a."]
     toks += [str(d).encode() for d in range(10)]
     toks += [f"z{i}".encode() for i in range(1, 41)] + [f"{i}y".encode() for i in range(1, 41)]
     seen, out = set(), []
@@ -109,6 +113,12 @@ def main():
     trajs = record(b, vocab, 6, 40, 12, lambda s: (b"(",) if s < 14 else (b")", b"a", b"b"))
     doc["cases"]["deep_ambig"] = {"grammar": gdeep, "trajectories": trajs}
     print("deep", max(max(t["ref_stacks"]) for t in trajs), "stacks max", f"{time.time() - t0:.1f}s", flush=True)
+
+    gdfa = 'root ::= [ab]* "a" [ab]{17} "."\n'
+    b = compile_bundle(gdfa, vocab)
+    trajs = record(b, vocab, 6, 40, 14, lambda s: (b"a", b"b"))
+    doc["cases"]["dfa_blowup"] = {"grammar": gdfa, "trajectories": trajs}
+    print("dfa_blowup", max(max(t["ref_stacks"]) for t in trajs), "stacks max", f"{time.time() - t0:.1f}s", flush=True)
 
     gbig = ambig_grammar(4200)
     try:

@@ -66,6 +66,13 @@ gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_rows,
                            const int32_t* bitmask, int64_t bitmask_stride,
                            const int32_t* indices, void* stream);
 
+/* K0's policy for 16-byte chunks that mix allowed and masked logits: a
+ * warp whose store round has at least min_lanes mixed chunks loads them,
+ * blends in -inf and writes each with one full store; otherwise (or with
+ * min_lanes = 0) it writes only the masked elements.  Returns the previous
+ * value.  Default: GMASK_APPLY_BLEND at load, else the build's default. */
+int32_t gm_apply_set_blend(int32_t min_lanes);
+
 /* ------------------------------------------------------------------------ */
 /* Vocabulary                                                                */
 /* ------------------------------------------------------------------------ */

@@ -92,6 +92,7 @@ _SIGNATURES = {
     "gm_last_error": ([], C.c_char_p),
     "gm_version": ([], C.c_char_p),
     "gm_apply_inplace": ([_P, _I32, _I64, _I64, _I64, _P, _I64, _P, _P], _I32),
+    "gm_apply_set_blend": ([_I32], _I32),
     "gm_vocab_create": ([_P, _P, _I32, _P, _I32, _I32, C.POINTER(_P)], _I32),
     "gm_vocab_release": ([_P], None),
     "gm_vocab_size": ([_P], _I32),
@@ -160,6 +161,8 @@ def load() -> C.CDLL:
         fn.argtypes = args
         fn.restype = res
     _lib = lib
+    if os.environ.get("GMASK_APPLY_BLEND") and hasattr(lib, "gm_apply_set_blend"):
+        lib.gm_apply_set_blend(int(os.environ["GMASK_APPLY_BLEND"]))  # K0 and the fused apply
     return lib
 
 

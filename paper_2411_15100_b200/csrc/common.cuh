@@ -110,21 +110,8 @@ __device__ __forceinline__ void st_cs_u16(void* p, uint32_t v) {
 // bit-identical; one full-sector store replaces up to 8 byte-masked partial
 // stores, which the memory system would otherwise merge sector by sector
 // (SQL-like masks: K5 48.2 -> 39.4 us/step).
-// Used when at least kBlendMinLanes of a warp's 32 consecutive chunks are
-// mixed (sector-dense partial writes, e.g. identifier-class masks); a few
-// mixed chunks among full ones (JSON's bimodal masks) keep the fire-and-forget
-// element stores, which add no load latency to the step (a threshold on the
-// warp's masked-element count via __reduce_add_sync measured 0.7 us slower).
-// Opt-in (-DGM_BLEND=1, GMASK_NVCC_EXTRA): measured K5 SQL 48.2 -> 39.4 us/step
-// but XML_TOY 16.3 -> 31.0 (its load latency sits on the apply's critical
-// path) and JSON +0.1; the default keeps the element stores.
-#ifndef GM_BLEND
-#define GM_BLEND 0
-#endif
-#ifndef GM_BLEND_MIN_LANES
-#define GM_BLEND_MIN_LANES 8
-#endif
-constexpr int kBlendMinLanes = GM_BLEND_MIN_LANES;
+// Used by K0 (per tile) and the fused apply (per warp round) when the
+// mixed chunks are dense and heavily masked (gm_apply_set_blend).
 template <int EB>
 __device__ __forceinline__ void blend_chunk(void* p, uint32_t keep, uint32_t neg) {
   uint32_t v0, v1, v2, v3;

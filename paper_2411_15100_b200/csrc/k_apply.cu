@@ -30,19 +30,58 @@ __device__ __forceinline__ void st_v4(void* p, uint32_t v) {
 constexpr int kTileTok = 1024;  // tokens per warp tile (32 words)
 constexpr int kApplyWarps = 8;  // warps per CTA
 constexpr int kApplyCtasPerSm = 8;
+#ifndef GM_APPLY_BLEND_DEFAULT
+#define GM_APPLY_BLEND_DEFAULT 528  // >= 16 mixed chunks per tile averaging >= 2 masked elements (tools/apply_compare.py sweep)
+#endif
 
 // EB = bytes per element.  Persistent grid (8 CTAs of 8 warps per SM): warp
 // w of N handles tiles w, w + N, ... of the row-major (row, tile) space, so
 // the batch is one wave and consecutive warps write consecutive spans.
 // (Measured and rejected: TPW tiles per warp with all mask loads issued
 // first, contiguous or strided — 0.2-0.3 us slower per 128-row step.)
+// Mixed 16-byte chunks (some logits kept, some masked) of one mask word:
+// (chunks, masked elements in them).
+template <int EB>
+__device__ __forceinline__ uint2 mixed_of_word(uint32_t w) {
+  constexpr int VEC = 16 / EB, CPW = 32 / VEC;
+  constexpr uint32_t FULL = (1u << VEC) - 1u;
+  uint32_t n = 0, el = 0;
+#pragma unroll
+  for (int k = 0; k < CPW; ++k) {
+    const uint32_t c = (w >> (k * VEC)) & FULL;
+    const bool mixed = c != 0 && c != FULL;
+    n += mixed;
+    el += mixed ? (uint32_t)__popc(~c & FULL) : 0u;
+  }
+  return make_uint2(n, el);
+}
+
 template <int EB>
 __device__ __forceinline__ void apply_tile(char* __restrict__ tp, int64_t tok_base, int64_t vocab, uint32_t w, int lane,
-                                           uint32_t neg) {
+                                           uint32_t neg, int blend_min) {
   constexpr int VEC = 16 / EB;                 // tokens per 16-byte chunk
   constexpr int ROUNDS = kTileTok / VEC / 32;  // store rounds per tile
   constexpr int CPW = 32 / VEC;                // chunks per mask word
   constexpr uint32_t FULL = (1u << VEC) - 1u;
+  // Mixed-chunk policy, decided once per tile from its 32 mask words: when
+  // the tile has at least (blend_min & 0xFF) mixed chunks averaging at
+  // least (blend_min >> 8) masked elements (identifier-class masks: SQL),
+  // each mixed chunk is loaded, blended with -inf and written with one full
+  // 16-byte store, instead of up to 8 byte-masked element stores; sparse or
+  // lightly masked mixed chunks (JSON's bimodal masks, XML) keep the element
+  // stores, which add no load latency.  blend_min 0 = never (runtime
+  // switch: gm_apply_set_blend / GMASK_APPLY_BLEND).
+  bool blend = false;
+  // words that are all-allowed or all-masked hold no mixed chunk (JSON's
+  // bimodal masks): one vote skips the policy
+  if (blend_min > 0 && __any_sync(0xFFFFFFFFu, w != 0u && w != 0xFFFFFFFFu)) {
+    const uint2 m = mixed_of_word<EB>(w);
+    const uint32_t nmix = __reduce_add_sync(0xFFFFFFFFu, m.x);
+    if (nmix >= (uint32_t)(blend_min & 0xFF) && nmix > 0) {
+      const uint32_t nel = __reduce_add_sync(0xFFFFFFFFu, m.y);
+      blend = nel >= (uint32_t)((blend_min >> 8) & 0xFF) * nmix;
+    }
+  }
 #pragma unroll
   for (int r = 0; r < ROUNDS; ++r) {
     const int c = r * 32 + lane;  // chunk within the tile
@@ -54,11 +93,7 @@ __device__ __forceinline__ void apply_tile(char* __restrict__ tp, int64_t tok_ba
       const int64_t nvalid = vocab - tok0;
       keep |= nvalid <= 0 ? FULL : (FULL & ~((1u << nvalid) - 1u));
     }
-#if GM_BLEND
-    const bool dense_mixed = __popc(__ballot_sync(0xFFFFFFFFu, keep != 0 && keep != FULL)) >= kBlendMinLanes;
-#else
-    constexpr bool dense_mixed = false;
-#endif
+    const bool dense_mixed = blend;
     if (keep == FULL) continue;
     char* p = tp + c * 16;
     if (keep == 0) {
@@ -81,7 +116,7 @@ template <int EB>
 __global__ void __launch_bounds__(32 * kApplyWarps)
 apply_tile_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab, int64_t lstride_bytes,
                   const int32_t* __restrict__ bitmask, int64_t bstride, const int32_t* __restrict__ indices,
-                  uint32_t neg, int64_t tiles_per_row) {
+                  uint32_t neg, int64_t tiles_per_row, int blend_min) {
   pdl_trigger();
   pdl_wait();
   const int lane = threadIdx.x & 31;
@@ -94,7 +129,7 @@ apply_tile_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab, int6
     const int64_t word = tile * 32 + lane;
     const uint32_t w = word < words_row ? (uint32_t)__ldg(bitmask + row * bstride + word) : 0xFFFFFFFFu;
     if (__all_sync(0xFFFFFFFFu, w == 0xFFFFFFFFu)) continue;  // whole tile allowed
-    apply_tile<EB>(logits + row * lstride_bytes + tile * kTileTok * EB, tile * kTileTok, vocab, w, lane, neg);
+    apply_tile<EB>(logits + row * lstride_bytes + tile * kTileTok * EB, tile * kTileTok, vocab, w, lane, neg, blend_min);
   }
 }
 
@@ -129,6 +164,13 @@ __global__ void l2_touch_kernel(const uint4* __restrict__ p, int64_t lines, uint
 }
 
 }  // namespace
+
+// K0's mixed-chunk policy (see apply_tile); GMASK_APPLY_BLEND overrides the
+// default at load, gm_apply_set_blend at run time.
+static int g_apply_blend = [] {
+  const char* e = std::getenv("GMASK_APPLY_BLEND");
+  return e && *e ? std::atoi(e) : GM_APPLY_BLEND_DEFAULT;
+}();
 
 gm_status launch_l2_touch(void* base, size_t bytes, const L2Window& win) {
   const int64_t lines = (int64_t)(bytes / 128);
@@ -168,10 +210,10 @@ extern "C" gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_row
     const dim3 grid((unsigned)ctas), block(32 * kApplyWarps);
     if (eb == 4)
       GM_CUDA_TRY(launch_pdl(apply_tile_kernel<4>, grid, block, 0, s, lp, n_rows, vocab_size, lstride_bytes, bitmask,
-                             bitmask_stride, indices, neg, tiles_per_row));
+                             bitmask_stride, indices, neg, tiles_per_row, g_apply_blend));
     else
       GM_CUDA_TRY(launch_pdl(apply_tile_kernel<2>, grid, block, 0, s, lp, n_rows, vocab_size, lstride_bytes, bitmask,
-                             bitmask_stride, indices, neg, tiles_per_row));
+                             bitmask_stride, indices, neg, tiles_per_row, g_apply_blend));
   } else {
     int64_t gx = ceil_div(vocab_size, 256);
     if (gx > 65535) gx = 65535;
@@ -185,4 +227,15 @@ extern "C" gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_row
   }
   GM_LAUNCH_CHECK();
   return GM_OK;
+}
+
+namespace gm {
+gm_status set_fill_blend(int32_t policy);
+}
+
+extern "C" int32_t gm_apply_set_blend(int32_t min_lanes) {
+  const int32_t old = gm::g_apply_blend;
+  gm::g_apply_blend = min_lanes < 0 ? 0 : min_lanes;
+  gm::set_fill_blend(gm::g_apply_blend);  // the fused apply (K3/K5) follows
+  return old;
 }

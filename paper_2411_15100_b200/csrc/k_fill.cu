@@ -29,6 +29,16 @@
 namespace gm {
 
 constexpr int kFillThreads = 512;
+// The fused apply's mixed-chunk blend (K0's policy) is compiled in only with
+// -DGM_FILL_BLEND=1: measured K5 SQL 43.9 -> 37.9 us/step but XML 19.7 ->
+// 23.0 and JSON +0.7 (the policy check alone), so the fused apply keeps the
+// element stores; K0 applies the policy (per tile, default 528).
+#ifndef GM_FILL_BLEND
+#define GM_FILL_BLEND 0
+#endif
+#ifndef GM_FILL_BLEND_DEFAULT
+#define GM_FILL_BLEND_DEFAULT 528
+#endif
 constexpr int kTmaRows = 4;     // tops whose rows are TMA-staged (more: direct loads)
 constexpr int kDepS = 16;
 constexpr int kDepF = 64;
@@ -57,6 +67,11 @@ constexpr bool kTimeline = true;
 constexpr bool kTimeline = false;
 #endif
 
+// Mixed-chunk policy of the fused apply (same encoding as K0's, whose
+// setter gm_apply_set_blend also updates this copy); read at run time, so a
+// captured graph follows the switch.
+__device__ int g_fill_blend = GM_FILL_BLEND_DEFAULT;
+
 // K3/K5 tail: mask one logits row in place from the finished mask words in
 // shared memory (coalesced 16-byte chunks, -inf only where masked, logits
 // never read; mixed chunks store just their masked elements).  EB = bytes
@@ -77,10 +92,21 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
     uint32_t keep = (words[t0 >> 5] >> (t0 & 31)) & full;
     const bool tail = t0 + vec > lim;
     if (tail) keep |= full & ~((1u << (lim - t0)) - 1u);
-#if GM_BLEND
-    const bool dense_mixed = __popc(__ballot_sync(__activemask(), keep != 0 && keep != full)) >= kBlendMinLanes;
-#else
-    constexpr bool dense_mixed = false;
+    // the K0 mixed-chunk policy (k_apply.cu apply_tile), per 32-chunk round
+    // of the warp: blend when at least (policy & 0xFF) / 2 of its chunks are
+    // mixed with at least (policy >> 8) masked elements each on average
+    bool dense_mixed = false;
+#if GM_FILL_BLEND
+    const int policy = g_fill_blend;
+    const unsigned am = __activemask();
+    const bool mixed = keep != 0 && keep != full;
+    if (policy > 0 && __any_sync(am, mixed)) {
+      const int nmix = __popc(__ballot_sync(am, mixed));
+      if (2 * nmix >= (policy & 0xFF)) {
+        const int nel = (int)__reduce_add_sync(am, mixed ? (unsigned)__popc(~keep & full) : 0u);
+        dense_mixed = nel >= ((policy >> 8) & 0xFF) * nmix;
+      }
+    }
 #endif
     if (keep == full) continue;
     char* p = base + t0 * EB;
@@ -1061,4 +1087,11 @@ gm_status launch_step_ptok(const DevPool& P, const int32_t* slots, int32_t n, co
   return GM_OK;
 }
 
+}  // namespace gm
+
+namespace gm {
+gm_status set_fill_blend(int32_t policy) {
+  GM_CUDA_TRY(cudaMemcpyToSymbol(g_fill_blend, &policy, sizeof(policy)));
+  return GM_OK;
+}
 }  // namespace gm

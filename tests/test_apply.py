@@ -59,3 +59,34 @@ def test_apply_rejects_cpu():
 
     with pytest.raises(RuntimeError):
         apply_token_bitmask_inplace(torch.zeros(1, 32), torch.zeros(1, 1, dtype=torch.int32))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("policy", [0, 1, 528, 0x0F10])
+def test_apply_mixed_chunk_policy_exact(dtype, policy):
+    """K0's runtime mixed-chunk policy (gm_apply_set_blend): element stores,
+    blend always, the default and a strict threshold give the same exact
+    result on masks with dense, sparse and heavily masked mixed chunks;
+    logits past the vocabulary and rows not listed stay untouched."""
+    from paper_2411_15100_b200 import _lib, apply_token_bitmask_inplace
+
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(policy + 1)
+    B, vocab = 9, 128256
+    W = (vocab + 31) // 32
+    logits = torch.randn(B, vocab + 8, device="cuda", generator=g).to(dtype)
+    bm = torch.randint(-2**31, 2**31 - 1, (B, W), device="cuda", dtype=torch.int32, generator=g)  # dense mixed
+    bm[1] = bm[1] | 0x7F7F7F7F        # mixed chunks with one masked element
+    bm[2] = bm[2] & 0x01010101        # heavily masked mixed chunks
+    bm[3, ::2] = -1                   # bimodal words
+    bm[3, 1::2] = 0
+    bm[4] = -1
+    bm[5] = 0
+    want = _expect(logits, bm, vocab, rows=[0, 1, 2, 3, 4, 5, 7])
+    old = lib.gm_apply_set_blend(policy)
+    try:
+        y = logits.clone()
+        apply_token_bitmask_inplace(y, bm, vocab_size=vocab, indices=[0, 1, 2, 3, 4, 5, 7])
+    finally:
+        lib.gm_apply_set_blend(old)
+    assert torch.equal(y.view(torch.int8), want.view(torch.int8))

@@ -106,6 +106,7 @@ def main():
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--out", default=None)
+    ap.add_argument("--blend", type=int, nargs="*", default=[], help="also time K0 with these blend thresholds")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     import paper_2411_15100_b200 as gm
@@ -120,7 +121,22 @@ def main():
     ring = [torch.randn(args.batch, V, device="cuda").to(dtype) for _ in range(8)]
     peak, peak_kind = bench.measured_peak_hbm()
 
-    impls = {"k0_ours": lambda lg, bm: gm.apply_token_bitmask_inplace(lg, bm)}
+    from paper_2411_15100_b200 import _lib
+
+    lib = _lib.load()
+    default_blend = lib.gm_apply_set_blend(0)
+    lib.gm_apply_set_blend(default_blend)
+
+    def k0(blend):
+        def fn(lg, bm):  # the policy is a launch parameter: captured with the graph
+            old = lib.gm_apply_set_blend(blend)
+            gm.apply_token_bitmask_inplace(lg, bm)
+            lib.gm_apply_set_blend(old)
+        return fn
+
+    impls = {"k0_ours": k0(default_blend)}
+    for n in args.blend:
+        impls[f"k0_blend{n}"] = k0(n)
     errors = {}
     try:
         from xgrammar.kernels.apply_token_bitmask_inplace_triton import apply_token_bitmask_inplace_triton
@@ -134,7 +150,7 @@ def main():
         impls["xgrammar_cuda"] = lambda lg, bm: apply_token_bitmask_inplace_cuda(lg, bm)
     except Exception as exc:  # noqa: BLE001
         errors["xgrammar_cuda"] = repr(exc)[:300]
-    res = {"grammar": args.grammar, "batch": args.batch, "V": V, "steps": args.steps, "dtype": args.dtype,
+    res = {"grammar": args.grammar, "k0_default_blend": default_blend, "batch": args.batch, "V": V, "steps": args.steps, "dtype": args.dtype,
            "allowed_fraction": allowed_frac, "algorithmic_bytes_per_step": algo, "peak_gbs": peak,
            "peak_source": peak_kind, "errors": errors, "impls": {}}
     for name, fn in impls.items():

@@ -218,8 +218,9 @@ def profiled_traffic(kernel_tag: str):
         except Exception:
             continue
         for k, v in d.items():
-            if k.endswith(kernel_tag):
-                return {"bytes": float(v), "source": os.path.relpath(path, ROOT)}
+            if k.endswith(kernel_tag) and isinstance(v, (int, float)):
+                how = (d.get("how") or {}).get(k, "dram read+write per launch, one ncu --set full replay")
+                return {"bytes": float(v), "source": os.path.relpath(path, ROOT), "how": how}
     return None
 
 
@@ -1009,8 +1010,7 @@ def main():
                          "achieved": achieved, "peak": peak, "peak_source": peak_kind, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": traffic["bytes"] if traffic else None,
-                         "traffic_source": (traffic["source"] + " (dram read+write per launch, one ncu --set full "
-                                            "replay)") if traffic else None,
+                         "traffic_source": (traffic["source"] + ": " + traffic["how"]) if traffic else None,
                          "algorithmic_bytes_per_launch": algo_bytes},
             "e2e": {"value": r["e2e_us"], "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": B,
                     "path": "DecodeLoop.step per decode step (native gm_decoder_step: host token ids passed to K5 "

@@ -6,7 +6,8 @@ import json
 
 import pytest
 
-from paper_2411_15100_b200.automaton import StateLimitError, build_tables
+from automaton_spec import build_tables
+from paper_2411_15100_b200.automaton import StateLimitError
 from paper_2411_15100_b200.grammar import GrammarError, parse_grammar
 from paper_2411_15100_b200.schema import SchemaError, schema_to_grammar_text
 from tablesim import TableSim
@@ -136,7 +137,7 @@ def _schema_variants(n):
 
 def test_native_front_end_tables_identical():
     """The C++ front end (gm_front_end_build, §8f rank 2) builds exactly the
-    tables of the Python specification (automaton.build_tables), array for
+    tables of the Python specification (tests/automaton_spec.py build_tables), array for
     array, for every reference grammar and 24 schema grammars; host only."""
     import numpy as np
 

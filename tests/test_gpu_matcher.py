@@ -305,9 +305,10 @@ def test_guided_generation_is_in_language():  # REF test_matcher.py:376-386
                                              ("sql", "bfloat16", 6), ("sql", "float32", 6)])
 def test_fused_fill_apply_equals_separate(grammar, dtype, B):
     """K3 (one kernel) == K2 fill then K0 apply == torch.where(bit, x, -inf),
-    bit for bit, along a trajectory (B = 100: one CTA per request with the
-    cross-CTA apply queue; the SQL grammar's identifier-class masks take the
-    load-blend-store path for dense mixed chunks)."""
+    bit for bit, along a trajectory (B = 6: several CTAs per request, each
+    with its word range; B = 100: one CTA per request; the SQL grammar's
+    identifier-class masks take K0's load-blend-store path for dense mixed
+    chunks while the fused apply stores only the masked elements)."""
     import torch
 
     import paper_2411_15100_b200 as gm

@@ -623,9 +623,15 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
     return bail(st);
   // records gathered from the vocabulary's token records (their byte offsets
   // point into the vocabulary buffer), then the one-level context classes
+  // GMASK_CTX_CLASSES=0 (diagnostics): no context classes, the fill walks
+  // every dependent (with an uncached compile: every token, REF
+  // matcher.py:446-460 brute force)
+  const char* cc = getenv("GMASK_CTX_CLASSES");
+  const bool ctx_classes = !(cc && cc[0] == '0');
   if ((st = launch_dep_records(dep_ids, dep_total, v->dev.tokrec, rec, s)) ||
-      (st = launch_dep_context(g->dev, dep_off, n, dep_total, rec, reinterpret_cast<const uint8_t*>(v->dev.tokrec),
-                               s)) ||
+      (ctx_classes &&
+       (st = launch_dep_context(g->dev, dep_off, n, dep_total, rec, reinterpret_cast<const uint8_t*>(v->dev.tokrec),
+                                s))) ||
       (two_level &&
        (st = launch_dep_context2(g->dev, dep_off, n, dep_total, rec, reinterpret_cast<const uint8_t*>(v->dev.tokrec),
                                  ctx2, s))))

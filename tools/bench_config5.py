@@ -10,7 +10,8 @@ the replicated-cache path with the NCCL all-gather is bench.py's config 3).
 
 Reports: compile ms per schema (front end + K1 cache build + assembly, one
 GPU, sequential), the fill+apply step (K3) over the mixed-grammar batch, the
-K5 decode step, oracle parity on sampled requests, and the oracle's compile
+K5 decode step, parity with the reference (grammask, baseline/_ref) on sampled
+requests over all steps, and the reference's compile
 time for a sample of schemas (CPU reference, extrapolated to 1,024).
 
     python tools/bench_config5.py [--schemas 1024] [--per-gpu 128] [--steps 60]
@@ -180,27 +181,52 @@ def main():
     k5_mism = int((masks_t != masks_all).any(dim=2).sum())
     k5_acc = bool(acc_t[:S - 1].bool().all())
 
-    # oracle parity on the sampled rows (their own schemas) + oracle compile time
-    from oracle import compile_oracle_bundle
-    from oracle.matcher import OracleMatcher
-    from paper_2411_15100_b200.schema import schema_to_grammar_text
-
+    # parity on the sampled rows (their own schemas) against the REFERENCE
+    # itself (grammask from baseline/_ref: its schema lowering, compile and
+    # Matcher), + its compile time; the oracle port only if it is missing
     toks_h = toks_hist.cpu().numpy()
     keep_h = keep.cpu().numpy()
     mism, checked, ocomp = 0, 0, []
+    gmk = bench._grammask()
+    kind = "reference" if gmk is not None else "port"
     for r in range(min(sample_rows, args.oracle_schemas)):
-        t1 = time.perf_counter()
-        ob = compile_oracle_bundle(schema_to_grammar_text(json.dumps(mine[r])), vocab)
-        ocomp.append(time.perf_counter() - t1)
-        m = OracleMatcher(ob, history_window=1)
-        for s in range(min(S, 24)):
+        if gmk is not None:
+            from grammask.bundle import compile_bundle as ref_compile
+            from grammask.matcher import Matcher as RefMatcher, TokenMask as RefMask
+            from grammask.schema import schema_to_grammar_text as ref_schema
+            from grammask.synthvocab import synth_vocab as ref_synth
+
+            rv = ref_synth(V)
+            t1 = time.perf_counter()
+            ob = ref_compile(ref_schema(json.dumps(mine[r])), rv)
+            ocomp.append(time.perf_counter() - t1)
+            new_m = lambda: RefMatcher(ob, rv, history_window=1)  # noqa: E731
+            mk = RefMask(V)
+
+            def fill(m):
+                m.fill_next_token_mask(mk)
+                return np.frombuffer(mk.to_bytes(), dtype=np.int32)
+        else:
+            from oracle import compile_oracle_bundle
+            from oracle.matcher import OracleMatcher
+            from paper_2411_15100_b200.schema import schema_to_grammar_text
+
+            t1 = time.perf_counter()
+            ob = compile_oracle_bundle(schema_to_grammar_text(json.dumps(mine[r])), vocab)
+            ocomp.append(time.perf_counter() - t1)
+            new_m = lambda: OracleMatcher(ob, history_window=1)  # noqa: E731
+
+            def fill(m):
+                return m.fill().view(np.int32)
+        m = new_m()
+        for s in range(S):
             checked += 1
-            if not np.array_equal(m.fill().view(np.int32), keep_h[s, r]):
+            if not np.array_equal(fill(m), keep_h[s, r]):
                 mism += 1
             t = int(toks_h[s, r])
             assert m.accept_token(t)
             if t == vocab.eos_id:
-                m = OracleMatcher(ob, history_window=1)
+                m = new_m()
     out = {
         "config": "SURVEY §8d config 5: distinct JSON schemas, synth_vocab(%d), %d requests/GPU" % (V, B),
         "schemas_total": args.schemas, "rank": rank, "world": world,
@@ -213,8 +239,8 @@ def main():
         "k5_all_accepted": k5_acc,
         "fill_apply_us_per_step_l2_flushed": step_us, "accept_recycle_us_per_step_l2_flushed": acc_us,
         "masked_fraction": float(masked[args.warmup:].double().mean().item()) / (B * V),
-        "oracle_parity": {"requests": min(sample_rows, args.oracle_schemas), "steps_checked": checked,
-                          "mismatches": mism},
+        "cpu_parity": {"kind": kind, "requests": min(sample_rows, args.oracle_schemas), "steps_checked": checked,
+                       "mismatches": mism},
         "cpu_reference_compile_s_per_schema": statistics.fmean(ocomp) if ocomp else None,
         "cpu_reference_compile_s_1024_extrapolated_1core": (statistics.fmean(ocomp) * args.schemas) if ocomp else None,
         "cpu": bench._cpu_name(),

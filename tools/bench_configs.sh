@@ -9,7 +9,7 @@ OUT=gpurun_out/configs_${TAG}.jsonl
 : > $OUT
 for spec in "schema 64" "xml 128" "arithmetic 128" "json 128"; do
   set -- $spec
-  timeout 900 python bench.py --grammar $1 --batch $2 --steps 100 --warmup 5 --cpu-steps 12 --cpu-budget-s 15 \
+  timeout 900 python bench.py --grammar $1 --batch $2 --steps 100 --warmup 5 --cpu-budget-s 20 \
       >> $OUT 2> gpurun_out/configs_${TAG}_$1.err || echo "{\"grammar\": \"$1\", \"failed\": true}" >> $OUT
 done
 cat $OUT | cut -c1-400

@@ -28,7 +28,7 @@ __device__ __forceinline__ void st_v4(void* p, uint32_t v) {
 }
 
 constexpr int kTileTok = 1024;  // tokens per warp tile (32 words)
-constexpr int kApplyWarps = 8;  // warps per CTA
+constexpr int kApplyWarps = 8;  // warps per CTA (measured: 16 x 4, 4 x 16, 8 x 4, 8 x 2 per SM all slower)
 constexpr int kApplyCtasPerSm = 8;
 #ifndef GM_APPLY_BLEND_DEFAULT
 #define GM_APPLY_BLEND_DEFAULT 528  // >= 16 mixed chunks per tile averaging >= 2 masked elements (tools/apply_compare.py sweep)
@@ -123,25 +123,13 @@ apply_tile_kernel(char* __restrict__ logits, int64_t n_rows, int64_t vocab, int6
   const int64_t words_row = (vocab + 31) >> 5;
   const int64_t n_tiles = n_rows * tiles_per_row;
   const int64_t n_warps = (int64_t)gridDim.x * kApplyWarps;
-  // software-pipelined: the next tile's mask word is loaded before this
-  // tile's stores are issued, so its HBM latency overlaps them
-  auto load_word = [&](int64_t t, int64_t& row, int64_t& tile) -> uint32_t {
-    const int64_t i = t / tiles_per_row;
-    tile = t - i * tiles_per_row;
-    row = indices ? (int64_t)__ldg(indices + i) : i;
+  for (int64_t t = (int64_t)blockIdx.x * kApplyWarps + (threadIdx.x >> 5); t < n_tiles; t += n_warps) {
+    const int64_t i = t / tiles_per_row, tile = t - i * tiles_per_row;
+    const int64_t row = indices ? (int64_t)__ldg(indices + i) : i;
     const int64_t word = tile * 32 + lane;
-    return word < words_row ? (uint32_t)__ldg(bitmask + row * bstride + word) : 0xFFFFFFFFu;
-  };
-  int64_t t = (int64_t)blockIdx.x * kApplyWarps + (threadIdx.x >> 5);
-  int64_t row = 0, tile = 0;
-  uint32_t w = t < n_tiles ? load_word(t, row, tile) : 0xFFFFFFFFu;
-  for (; t < n_tiles; t += n_warps) {
-    const int64_t cur_row = row, cur_tile = tile;
-    const uint32_t cur_w = w;
-    if (t + n_warps < n_tiles) w = load_word(t + n_warps, row, tile);
-    if (__all_sync(0xFFFFFFFFu, cur_w == 0xFFFFFFFFu)) continue;  // whole tile allowed
-    apply_tile<EB>(logits + cur_row * lstride_bytes + cur_tile * kTileTok * EB, cur_tile * kTileTok, vocab, cur_w, lane,
-                   neg, blend_min);
+    const uint32_t w = word < words_row ? (uint32_t)__ldg(bitmask + row * bstride + word) : 0xFFFFFFFFu;
+    if (__all_sync(0xFFFFFFFFu, w == 0xFFFFFFFFu)) continue;  // whole tile allowed
+    apply_tile<EB>(logits + row * lstride_bytes + tile * kTileTok * EB, tile * kTileTok, vocab, w, lane, neg, blend_min);
   }
 }
 

@@ -493,6 +493,14 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     torch.cuda.synchronize()
     k0_b2b_ms = t_ev[2].elapsed_time(t_ev[3]) / (S - W0)
 
+    # the same apply through XGrammar 0.2.0's GPU kernels (its
+    # Triton kernel is XGrammar's default and the bar; its CUDA kernel is
+    # JIT-built for this device), same masks, same logits ring, same graph
+    # bracket; each output checked against torch.where on a few steps
+    xgr = {}
+    if not args.no_xgrammar:
+        xgr = time_xgrammar_apply(masks_all, ring, W0, S, V, stream, cap_stream, sync_ranks, k0_b2b_ms)
+
     # pass E2E — `e2e`: the same decode steps through the public serving API
     # with host buffers, back to back in one bracket: per step one
     # DecodeLoop.step (native gm_decoder_step: host ids -> pinned staging ->
@@ -587,6 +595,7 @@ def run_ours(args, rank: int, world: int, group) -> dict:
         "k5_b2b_us": mx(k5_b2b_ms * 1e3),
         "k5_b2b_reps_us": [x * 1e3 for x in k5_rep_ms],
         "k0_b2b_us": mx(k0_b2b_ms * 1e3),
+        "xgrammar_apply": xgr,
         "e2e_us": mx(e2e_ms * 1e3),
         "e2e_host_us": e2e_host_us,
         "step_us": mx(statistics.fmean(step_ms) * 1e3),
@@ -646,6 +655,52 @@ def _reference_bundle(gmk, grammar: str, vocab_size: int):
     t0 = time.perf_counter()
     b = compile_bundle(text, vocab)
     return vocab, b, time.perf_counter() - t0
+
+
+def time_xgrammar_apply(masks_all, ring, W0, S, V, stream, cap_stream, sync_ranks, k0_ms) -> dict:
+    """XGrammar 0.2.0's Triton and CUDA apply kernels (xgrammar/kernels/
+    apply_token_bitmask_inplace_{triton,cuda}.py) over the same masks and
+    logits ring as K0's back-to-back pass; us/step, mismatching elements."""
+    out = {"k0_us": k0_ms * 1e3}
+    impls = {}
+    try:
+        from xgrammar.kernels.apply_token_bitmask_inplace_triton import apply_token_bitmask_inplace_triton
+
+        impls["triton"] = apply_token_bitmask_inplace_triton
+    except Exception as exc:  # noqa: BLE001
+        out["triton_error"] = repr(exc)[:200]
+    try:
+        from xgrammar.kernels.apply_token_bitmask_inplace_cuda import apply_token_bitmask_inplace_cuda
+
+        impls["cuda"] = apply_token_bitmask_inplace_cuda
+    except Exception as exc:  # noqa: BLE001
+        out["cuda_error"] = repr(exc)[:200]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    gen = torch.Generator(device=masks_all.device).manual_seed(3)
+    for name, fn in impls.items():
+        try:
+            bad = 0
+            for s in range(W0, min(S, W0 + 3)):  # exactness (also JIT / autotune outside the capture)
+                x = torch.randn(masks_all.shape[1], V, device=masks_all.device, generator=gen).to(ring[0].dtype)
+                want = torch.where(unpack_allowed(masks_all[s], V), x, torch.full_like(x, float("-inf")))
+                fn(x, masks_all[s])
+                bad += int((x.view(torch.int16) != want.view(torch.int16)).sum())
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=cap_stream):
+                for s in range(W0, S):
+                    fn(ring[s % len(ring)], masks_all[s])
+            g.replay()
+            sync_ranks()
+            ev[0].record(stream)
+            g.replay()
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+            us = ev[0].elapsed_time(ev[1]) / (S - W0) * 1e3
+            out[name] = {"us": us, "k0_speedup": us / (k0_ms * 1e3), "mismatching_elements": bad}
+        except Exception as exc:  # noqa: BLE001
+            out[name + "_error"] = repr(exc)[:200]
+    return out
 
 
 def cpu_baseline(args, ours: dict) -> dict:
@@ -938,6 +993,7 @@ def main():
     ap.add_argument("--repeats", type=int, default=7, help="K-step brackets of the value pass (median)")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-xgrammar", action="store_true", help="skip timing XGrammar's apply kernels")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic only: keep L2 warm between steps")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -999,6 +1055,7 @@ def main():
                 "k2_then_k0_us": r["separate_us"], "k4_accept_recycle_us": r["accept_us"],
                 "e2e_graph_step_us": r["e2e_latency_us"],
             },
+            "apply_vs_xgrammar": r["xgrammar_apply"],
             "k0_apply_b2b_us": r["k0_b2b_us"],
             "k0_apply_b2b_gbs": k0_bytes / (r["k0_b2b_us"] * 1e-6) / 1e9,
             "k0_apply_b2b_frac": k0_bytes / (r["k0_b2b_us"] * 1e-6) / 1e9 / peak,

@@ -926,6 +926,7 @@ struct DevPool {
   DevOverflow ovf;            // overflow-walker scratch lanes
   SlotHdr* hdr;               // [capacity]
   unsigned long long* trace;  // optional phase timestamps (GMASK_TRACE=1), else null
+  int32_t trace_ring;         // GMASK_TRACE=2: launches kept per CTA (back-to-back timelines), else 0
   // launch hint: the binding every bound slot shares (host bookkeeping,
   // gm_pool_reset / fork), or null.  Grammar blobs and token records are
   // immutable, so a step kernel may start staging them before its

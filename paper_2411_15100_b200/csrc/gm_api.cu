@@ -731,9 +731,11 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   GM_CUDA_TRY(cudaMemset(hdr, 0, sizeof(SlotHdr) * (size_t)capacity));
   unsigned long long* trace = nullptr;
   const char* tr = getenv("GMASK_TRACE");
-  if (tr && tr[0] == '1') {
-    if ((st = p->mem.alloc(&trace, 64 + 16 * (size_t)capacity))) return bail(st);
-    GM_CUDA_TRY(cudaMemset(trace, 0, (64 + 16 * (size_t)capacity) * 8));
+  const int32_t trace_ring = (tr && tr[0] == '2') ? 16 : 0;
+  if (tr && (tr[0] == '1' || tr[0] == '2')) {
+    const size_t n = 64 + 16 * (size_t)capacity * (1 + trace_ring) + (size_t)capacity;
+    if ((st = p->mem.alloc(&trace, n))) return bail(st);
+    GM_CUDA_TRY(cudaMemset(trace, 0, n * 8));
   }
   p->dev = DevPool{};
   p->dev.capacity = capacity;
@@ -754,6 +756,7 @@ gm_status gm_pool_create(int32_t capacity, int32_t max_stacks, int32_t max_windo
   p->dev.ovf = ovf;
   p->dev.hdr = hdr;
   p->dev.trace = trace;
+  p->dev.trace_ring = trace_ring;
   // opt-in L2 persistence for the arena (GMASK_L2_PERSIST=1): a device-wide
   // persisting carve-out + a persisting access-policy window on the step
   // launches; measured no gain on the JSON bench (the contended arena lines
@@ -1137,7 +1140,7 @@ gm_status gm_pool_materialize(gm_pool* p, int32_t handle, int32_t* out, int32_t 
 
 gm_status gm_pool_trace(gm_pool* p, uint64_t* out, int64_t n) {
   if (!p || !p->dev.trace) return fail(GM_ERR_INVALID, "pool created without GMASK_TRACE=1");
-  const int64_t cap = 64 + 3 * (int64_t)p->dev.capacity;
+  const int64_t cap = 64 + 16 * (int64_t)p->dev.capacity * (1 + p->dev.trace_ring) + (int64_t)p->dev.capacity;
   if (n > cap) n = cap;
   GM_CUDA_TRY(cudaDeviceSynchronize());
   GM_CUDA_TRY(cudaMemcpy(out, p->dev.trace, n * 8, cudaMemcpyDeviceToHost));

@@ -312,6 +312,7 @@ class Matcher:
             raise MatcherError("matcher is terminated")
         self._core.fill_row(self._row, 0, need_apply=False)
         out.words[:] = self._row[0].cpu().numpy().view(np.uint32)
+        self._core.check()  # this request's device error (e.g. over the 4096-stack cap), REF matcher.py:188-189
 
     def fill_device_row(self, bitmask: torch.Tensor, index: int = 0):
         """Fill bitmask[index] in HBM without the host copy."""

@@ -311,6 +311,10 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
       return kAccOk;
     }
   }
+#ifdef GM_DIAG_NO_GENERAL  // diagnostics: code-size experiment (multi-stack requests then fail)
+  slot_error(P, slot, kErrCap);
+  return kAccErr;
+#endif
   // general path: up to kAccS stacks, local frames
   Walker<kAccS, kAccF> w;
   w.reset();

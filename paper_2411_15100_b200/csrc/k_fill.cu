@@ -275,7 +275,12 @@ __device__ __forceinline__ void dep_walk(const DevPool& P, int32_t slot, const S
     err = rw.err;
     ok = rw.n > 0;
   } else {
+#ifdef GM_DIAG_NO_GENERAL
+    err = kErrCap;
+    ok = false;
+#else
     ok = walk_dep_general(&P, slot, &hd, &G, t.x, t.y, e, inl, far, spec, &err);
+#endif
   }
   if (err) {
     slot_error(P, slot, err);

@@ -1008,8 +1008,15 @@ def main():
     group = None
     if world > 1:
         local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        n_dev = torch.cuda.device_count()
+        torch.cuda.set_device(local % n_dev)
+        # one GPU per rank: NCCL over NVLink.  More ranks than GPUs (a
+        # functional check of the multi-rank path on a small box): gloo
+        backend = os.environ.get("GMASK_DIST_BACKEND") or ("nccl" if world <= n_dev else "gloo")
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local % n_dev))
+        else:
+            torch.distributed.init_process_group(backend)
         group = torch.distributed.group.WORLD
     else:
         torch.cuda.set_device(0)

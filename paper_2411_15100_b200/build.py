@@ -58,6 +58,19 @@ def build(force: bool = False, verbose: bool = False, out: Path = None) -> Path:
             OUT = saved
     if not force and not _stale():
         return OUT
+    # several processes (torchrun ranks) may find the library stale at once:
+    # one builds, the others wait on the lock and then see it fresh
+    import fcntl
+
+    BUILD.mkdir(exist_ok=True)
+    with open(BUILD / ".build.lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and not _stale():
+            return OUT
+        return _build_locked(verbose)
+
+
+def _build_locked(verbose: bool) -> Path:
     nvcc = _nvcc()
     BUILD.mkdir(exist_ok=True)
     include = ["-I", str(ROOT / "include"), "-I", str(CSRC)]

@@ -15,6 +15,8 @@ import json
 import threading
 from typing import Dict, List, Optional, Sequence, Union
 
+import torch
+
 from .automaton import AutomatonOptions
 from .engine import CompiledDeviceGrammar, DeviceVocab, compile_on_device
 from .schema import schema_to_grammar_text
@@ -160,7 +162,7 @@ class GrammarCompiler:
         options: Optional[AutomatonOptions] = None,
         group=None,
     ) -> None:
-        del max_threads  # the cache build runs on the GPU
+        self._threads = max(1, int(max_threads)) if isinstance(max_threads, int) else 8  # batch compiles
         self.tokenizer_info = tokenizer_info
         self._cache_enabled = cache_enabled
         self._cache_limit = cache_limit_bytes
@@ -169,7 +171,7 @@ class GrammarCompiler:
         self._memo: Dict[tuple, CompiledGrammar] = {}
         self._lock = threading.Lock()
 
-    def _compile(self, text: str, root_rule_name: Optional[str] = None) -> CompiledGrammar:
+    def _compile(self, text: str, root_rule_name: Optional[str] = None, parsed=None) -> CompiledGrammar:
         key = (text, root_rule_name)
         if self._cache_enabled:
             with self._lock:
@@ -177,7 +179,7 @@ class GrammarCompiler:
             if hit is not None:
                 return hit
         dev = compile_on_device(text, self.tokenizer_info.device_vocab, self._options,
-                                root_rule_name=root_rule_name, group=self._group)
+                                root_rule_name=root_rule_name, group=self._group, parsed=parsed)
         cg = CompiledGrammar(dev, self.tokenizer_info, text)
         if self._cache_enabled:
             with self._lock:
@@ -190,10 +192,15 @@ class GrammarCompiler:
     def compile_grammar(self, grammar: str, *, root_rule_name: str = "root") -> CompiledGrammar:
         """EBNF text -> CompiledGrammar.  The root is ``root_rule_name`` if that
         rule exists, else the grammask default (first rule)."""
+        import dataclasses
+
         from .grammar import parse_grammar
 
-        names = parse_grammar(grammar).bodies
-        return self._compile(grammar, root_rule_name if root_rule_name in names else None)
+        g = parse_grammar(grammar)  # parsed once: the root is chosen on the parse result
+        root = root_rule_name if root_rule_name in g.bodies else None
+        if root is not None and g.root != root:
+            g = dataclasses.replace(g, root=root)
+        return self._compile(grammar, root, parsed=g)
 
     def compile_json_schema(
         self,
@@ -213,6 +220,25 @@ class GrammarCompiler:
         if isinstance(schema, dict):
             schema = json.dumps(schema)
         return self._compile(schema_to_grammar_text(schema, whitespace=any_whitespace))
+
+    def compile_json_schemas(self, schemas, *, any_whitespace: bool = True, max_workers: Optional[int] = None):
+        """Compile many JSON schemas (e.g. BASELINE config 5: one per request)
+        on ``max_workers`` host threads (default: the compiler's
+        ``max_threads``): the native front end and the device build release
+        the GIL, so schemas overlap; results in input order."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        n = max_workers or self._threads
+        if n <= 1 or len(schemas) <= 1:
+            return [self.compile_json_schema(s, any_whitespace=any_whitespace) for s in schemas]
+        dev = torch.cuda.current_device()
+
+        def one(sch):
+            torch.cuda.set_device(dev)
+            return self.compile_json_schema(sch, any_whitespace=any_whitespace)
+
+        with ThreadPoolExecutor(max_workers=n) as ex:
+            return list(ex.map(one, schemas))
 
     def compile_builtin_json_grammar(self) -> CompiledGrammar:
         return self._compile(BUILTIN_JSON_GRAMMAR)

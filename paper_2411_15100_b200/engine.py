@@ -286,13 +286,13 @@ def sharded_rows(build, n_keys: int, words: int, device, group=None, costs=None)
 
 def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOptions] = None, *,
                       root_rule_name: Optional[str] = None, group=None, stream=None,
-                      uncached: bool = False) -> CompiledDeviceGrammar:
+                      uncached: bool = False, parsed=None) -> CompiledDeviceGrammar:
     """Front end + K1/K1b build.  With a torch.distributed ``group`` of size G
     the cache keys are dealt round-robin in decreasing order of estimated
     cost (``key_costs``) and the rows replicated with one all-gather
     (SURVEY §8e)."""
     t0 = time.perf_counter()
-    tables = build_tables_native(parse_grammar(text, root_rule_name), opts)
+    tables = build_tables_native(parsed if parsed is not None else parse_grammar(text, root_rule_name), opts)
     t1 = time.perf_counter()
     grammar = DeviceGrammar(tables)
     n_keys = grammar.n_keys

@@ -101,6 +101,19 @@ def main():
     split = {k: statistics.fmean(c.compile_ms[k] for c in compiled) for k in compiled[0].compile_ms}
     keys = [c.stats.get("keys", 0) for c in compiled]
     compile_total_ms = (time.perf_counter() - t0) * 1e3
+    # the same schemas compiled on host threads (GrammarCompiler.
+    # compile_json_schemas: native front end + device build release the GIL)
+    threaded = {}
+    for nt in (4, 8):
+        tc = gm.GrammarCompiler(info, cache_enabled=False, max_threads=nt)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        again = tc.compile_json_schemas([json.dumps(sc) for sc in mine])
+        torch.cuda.synchronize()
+        threaded[nt] = (time.perf_counter() - t1) * 1e3
+        a0, b0 = compiled[0]._dev.cache.export(), again[0]._dev.cache.export()
+        assert torch.equal(a0[0], b0[0]) and (a0[2] == b0[2]).all()
+        del again
 
     pool = get_pool()
     matchers = [gm.GrammarMatcher(c, max_rollback_tokens=1) for c in compiled]
@@ -233,6 +246,7 @@ def main():
         "compile_ms_per_schema": {"mean": statistics.fmean(per_ms), "median": statistics.median(per_ms),
                                   "max": max(per_ms)},
         "compile_ms_rank_total": compile_total_ms,
+        "compile_ms_rank_total_threads": threaded,
         "compile_split_ms_mean": split,
         "cache_keys_per_schema": {"mean": statistics.fmean(keys), "max": max(keys)},
         "k5_step_us_back_to_back": k5_b2b_us, "k5_mask_mismatches_vs_flushed_pass": k5_mism,

@@ -79,6 +79,10 @@ WORKLOADS = {
     "xml": dict(config=4, structural=frozenset(b"<>/ab"), force=None, desc="XML_TOY recursive grammar"),
     "arithmetic": dict(config=4, structural=frozenset(b"()+-*/0123456789"), force=(b"(", 40),
                        desc="ARITHMETIC grammar, 40 forced '(' per request (nesting depth >= 32)"),
+    "json_nested": dict(config=4, structural=frozenset(b'[]{},:"'), force=(b"[", 12),
+                        desc="builtin JSON grammar, nesting-biased trajectories (12 forced '[' then structural "
+                             "tokens only: arrays / objects / strings nest and close in every order, so "
+                             "multi-level dependents such as '\"}]' need the request's deeper stack)"),
     "sql": dict(config=4, structural=frozenset(b"(),.;=<>*' "), force=None,
                 desc="SQL-like query grammar (paper_2411_15100_b200/grammars/sql.gbnf: joins, nested conditions, "
                      "subqueries)"),
@@ -88,7 +92,7 @@ WORKLOADS = {
 def grammar_text(name: str) -> str:
     import paper_2411_15100_b200 as gm
 
-    if name == "json":
+    if name in ("json", "json_nested"):
         return gm.BUILTIN_JSON_GRAMMAR
     if name == "schema":
         from paper_2411_15100_b200.schema import schema_to_grammar_text
@@ -649,7 +653,7 @@ def _reference_bundle(gmk, grammar: str, vocab_size: int):
     from grammask import grammars as rg
     from grammask.schema import schema_to_grammar_text as ref_schema
 
-    text = {"json": rg.JSON_ECMA404, "xml": rg.XML_TOY, "arithmetic": rg.ARITHMETIC,
+    text = {"json": rg.JSON_ECMA404, "json_nested": rg.JSON_ECMA404, "xml": rg.XML_TOY, "arithmetic": rg.ARITHMETIC,
             "schema": ref_schema(rg.SAMPLE_SCHEMA)}.get(grammar) or grammar_text(grammar)
     vocab = synth_vocab(vocab_size)
     t0 = time.perf_counter()

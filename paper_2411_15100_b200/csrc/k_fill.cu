@@ -404,6 +404,8 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     mbar_init(&blob_bar, (uint32_t)P.hint_blob_bytes);
     bulk_g2s(tables, P.hint_blob, (uint32_t)P.hint_blob_bytes, &blob_bar);
   }
+  unsigned long long t_launch = 0;  // diagnostics: CTA resident (before the grid-dependency wait)
+  if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_launch));
   pdl_wait();
   const int32_t i = blockIdx.x;
   if (i >= n) return;
@@ -910,6 +912,12 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
     const int64_t c = (int64_t)i * n_split + split;
     if (16 * c + 16 <= 16 * (int64_t)P.capacity) {  // per-CTA timeline (absolute %globaltimer stamps)
       unsigned long long* tr = P.trace + 64 + 16 * c;
+      if (P.trace_ring > 0) {  // GMASK_TRACE=2: ring of the last trace_ring launches (back-to-back analysis)
+        unsigned long long* cnt = P.trace + 64 + 16 * (int64_t)P.capacity * (1 + P.trace_ring) + c;
+        const unsigned long long k = (*cnt)++;
+        tr = P.trace + 64 + 16 * (int64_t)P.capacity * (1 + (int64_t)(k % P.trace_ring)) + 16 * c;
+        t_pref = t_launch;
+      }
       tr[0] = t_start; tr[1] = t_hdr; tr[2] = t_acc; tr[3] = t_setup;
       tr[4] = t_ctx; tr[5] = t_walks; tr[6] = t_merge; tr[7] = t1;
       tr[8] = t_walk;                // accept: register walk done (0: no walk / general path)

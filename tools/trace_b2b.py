@@ -39,6 +39,7 @@ def main(S=48, grammar="json"):
     slots = torch.tensor([m.slot for m in ms], dtype=torch.int32, device=dev)
     rows = torch.arange(B, device=dev)
     structural = torch.from_numpy(bench.structural_flags(vocab, bench.WORKLOADS[grammar]["structural"])).to(dev)
+    force = bench.forced_token(vocab, grammar)
     W = (V + 31) // 32
     masks = torch.empty((S, B, W), dtype=torch.int32, device=dev)
     toks = torch.empty((S, B), dtype=torch.int32, device=dev)
@@ -47,7 +48,7 @@ def main(S=48, grammar="json"):
     for s in range(S):
         batch_step(pool, slots, toks[s - 1] if s else None, acc[s - 1] if s else None, masks[s], ring[s % 8],
                    recycle=True)
-        toks[s] = bench.sample_tokens(bench.unpack_allowed(masks[s], V), structural, s, rows).to(torch.int32)
+        toks[s] = bench.sample_tokens(bench.unpack_allowed(masks[s], V), structural, s, rows, force=force).to(torch.int32)
     torch.cuda.synchronize()
     for m in ms:
         m.reset()
@@ -100,6 +101,8 @@ def main(S=48, grammar="json"):
             row["accept_by_kind"].setdefault(key, []).append(round(t, 2))
         ends = sorted((x[7] - t0) / 1e3 for x in recs)
         row["cta_end_p50_max"] = (round(ends[len(ends) // 2], 2), round(ends[-1], 2))
+        walked = [(x[10] >> 40) & 0xFFFF for x in recs]
+        row["deps_walked_mean_max"] = (round(sum(walked) / len(walked), 1), max(walked))
         out.append(row)
     keys = ["span_us", "gap_to_next_us", "launch_to_first_start_us", "next_resident_before_end_us"] + PH
     summ = {}
@@ -115,4 +118,5 @@ def main(S=48, grammar="json"):
 
 
 if __name__ == "__main__":
-    main()
+    g = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--grammar=")), "json")
+    main(grammar=g)

@@ -371,9 +371,14 @@ def run_ours(args, rank: int, world: int, group) -> dict:
     masks_t = torch.empty_like(masks_all)
     acc_t = torch.zeros((S, B), dtype=torch.uint8, device=dev)
 
+    # slot ids by value in the launch parameters (the serving loop knows its
+    # requests' slots on the host): the header load is the kernel's first
+    # global access.  --device-slots: read them from a device array instead
+    host_slots = None if args.device_slots else [m.slot for m in matchers]
+
     def k5(s):
         batch_step(pool, slots, tok_dev[s - 1] if s > 0 else None, acc_t[s - 1] if s > 0 else None, masks_t[s],
-                   ring[s % n_ring], recycle=True)
+                   ring[s % n_ring], recycle=True, host_slots=host_slots)
 
     # Launched from Python each K5 call costs ~10 us of host time, more than
     # the kernel, so a plain loop would time the host.  The W warm-up steps
@@ -998,6 +1003,7 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-xgrammar", action="store_true", help="skip timing XGrammar's apply kernels")
+    ap.add_argument("--device-slots", action="store_true", help="diagnostic: K5 reads slot ids from device memory")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic only: keep L2 warm between steps")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -313,6 +313,17 @@ gm_status gm_step_tokens(gm_pool* p, const int32_t* slots, int32_t n,
                          void* logits, int32_t dtype, int64_t vocab_size,
                          int64_t logits_stride, void* stream);
 
+/* gm_step_tokens with the slot ids passed by value from HOST memory
+ * (host_slots[0..n), n <= 512, rows = i): the step kernel's first global
+ * access is then the slot header itself, one round trip fewer.  Token ids
+ * (device, nullable: first step), outputs and semantics as gm_step_tokens. */
+gm_status gm_step_tokens_host_slots(gm_pool* p, const int32_t* host_slots, int32_t n,
+                                    const int32_t* token_ids, uint8_t* accepted_out,
+                                    int32_t recycle_terminated, int32_t* bitmask,
+                                    int64_t bitmask_stride, void* logits, int32_t dtype,
+                                    int64_t vocab_size, int64_t logits_stride,
+                                    void* stream);
+
 /* Native decode loop over gm_step_tokens with host buffers (the serving
  * form of the reference's per-token accept_token -> fill_next_token_mask
  * loop, REF matcher.py:273, 377, driven from the host as in REF bench.py:

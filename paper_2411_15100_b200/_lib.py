@@ -116,6 +116,7 @@ _SIGNATURES = {
     "gm_fill_apply_tokens": ([_P, _P, _I32, _P, _I64, _P, _P, _I32, _I64, _I64, _P], _I32),
     "gm_pool_recycle": ([_P, _P, _I32, _P], _I32),
     "gm_step_tokens": ([_P, _P, _I32, _P, _P, _I32, _P, _I64, _P, _P, _I32, _I64, _I64, _P], _I32),
+    "gm_step_tokens_host_slots": ([_P, _P, _I32, _P, _P, _I32, _P, _I64, _P, _I32, _I64, _I64, _P], _I32),
     "gm_decoder_create": ([_P, _P, _I32, _I32, _P, _I64, _P, _I32, _I64, _I64, _I32, C.POINTER(_P)], _I32),
     "gm_decoder_step": ([_P, _I32, _P, _P], _I32),
     "gm_decoder_flags": ([_P, _I32, _P, _I32], _I32),

@@ -39,8 +39,8 @@ gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t
 gm_status launch_fill_apply(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*, int32_t,
                             void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_l2_touch(void* base, size_t bytes, const L2Window& win);
-gm_status launch_step_ptok(const DevPool&, const int32_t*, int32_t, const int32_t*, uint8_t*, int32_t, int32_t*, int64_t,
-                           int32_t, void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
+gm_status launch_step_ptok(const DevPool&, const int32_t*, int32_t, const int32_t*, const int32_t*, uint8_t*, int32_t,
+                           int32_t*, int64_t, int32_t, void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_step(const DevPool&, const int32_t*, int32_t, const int32_t*, uint8_t*, int32_t, int32_t*, int64_t,
                       const int32_t*, int32_t, void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_accept_tokens(const DevPool&, const int32_t*, const int32_t*, int32_t, uint8_t*, cudaStream_t);
@@ -912,6 +912,32 @@ gm_status gm_step_tokens(gm_pool* p, const int32_t* slots, int32_t n, const int3
                      p->max_w, logits, eb, neg, vocab_size, logits_stride * eb, as_stream(stream));
 }
 
+gm_status gm_step_tokens_host_slots(gm_pool* p, const int32_t* host_slots, int32_t n, const int32_t* token_ids,
+                                    uint8_t* accepted_out, int32_t recycle_terminated, int32_t* bitmask,
+                                    int64_t bitmask_stride, void* logits, int32_t dtype, int64_t vocab_size,
+                                    int64_t logits_stride, void* stream) {
+  if (!p || (n > 0 && !host_slots)) return fail(GM_ERR_INVALID, "null pool / slots");
+  if (token_ids && !accepted_out) return fail(GM_ERR_INVALID, "accepted_out is required with token_ids");
+  if (!bitmask && !logits) return fail(GM_ERR_INVALID, "need a bitmask and/or logits");
+  for (int32_t i = 0; i < n; ++i)
+    if (host_slots[i] < 0 || host_slots[i] >= p->dev.capacity) return fail(GM_ERR_INVALID, "slot out of range");
+  int32_t eb = 2;
+  uint32_t neg = 0;
+  if (logits) {
+    switch (dtype) {
+      case GM_DTYPE_F32: eb = 4; neg = 0xFF800000u; break;
+      case GM_DTYPE_F16: eb = 2; neg = 0xFC00FC00u; break;
+      case GM_DTYPE_BF16: eb = 2; neg = 0xFF80FF80u; break;
+      default: return fail(GM_ERR_INVALID, "unknown dtype");
+    }
+    if (reinterpret_cast<uintptr_t>(logits) % 16 || (logits_stride * eb) % 16)
+      return fail(GM_ERR_INVALID, "fused step+apply needs 16-byte aligned logits rows");
+  }
+  return launch_step_ptok(p->dev, host_slots, n, nullptr, token_ids, accepted_out, recycle_terminated, bitmask,
+                          bitmask_stride, p->max_w, logits, eb, neg, vocab_size, logits_stride * eb,
+                          as_stream(stream));
+}
+
 // ---------------------------------------------------------------------------
 // Native decode loop (gm_decoder_*): per step one host memcpy into pinned
 // staging, H2D on an input copy stream, K5 on the caller's stream, D2H of
@@ -929,6 +955,7 @@ struct gm_decoder {
   std::vector<uint8_t*> acc_host, acc_dev;
   std::vector<cudaEvent_t> h2d, k5, done;
   std::vector<int> issued;
+  std::vector<int32_t> host_slots;  // the slot ids, passed by value to K5
   bool no_ptok = false;             // GMASK_DECODER_COPY=1: token ids via the H2D copy path
   cudaStream_t copy = nullptr;      // H2D of token ids
   cudaStream_t copy_out = nullptr;  // D2H of accepted flags (separate: the next H2D must not queue behind it)
@@ -973,6 +1000,11 @@ gm_status gm_decoder_create(gm_pool* p, const int32_t* slots, int32_t n, int32_t
     decoder_free(d);
     return fail(GM_ERR_CUDA, std::string("gm_decoder_create: ") + cudaGetErrorString(e));
   };
+  d->host_slots.resize(n);
+  {
+    const cudaError_t e0 = cudaMemcpy(d->host_slots.data(), slots, (size_t)n * 4, cudaMemcpyDeviceToHost);
+    if (e0 != cudaSuccess) return bail(e0);
+  }
   cudaError_t e = cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking);
   if (e != cudaSuccess) return bail(e);
   if ((e = cudaStreamCreateWithFlags(&d->copy_out, cudaStreamNonBlocking)) != cudaSuccess) return bail(e);
@@ -1016,9 +1048,9 @@ gm_status gm_decoder_step(gm_decoder* d, int32_t buf, const int32_t* host_tokens
       case GM_DTYPE_F16: eb = 2; neg = 0xFC00FC00u; break;
       default: eb = 2; neg = 0xFF80FF80u; break;
     }
-    gm_status st = launch_step_ptok(d->pool->dev, d->slots, n, host_tokens, d->acc_dev[buf], d->recycle,
-                                    d->bitmask[buf], d->bstride, d->pool->max_w, d->logits[buf], eb, neg, d->vocab,
-                                    d->lstride * eb, s);
+    gm_status st = launch_step_ptok(d->pool->dev, d->host_slots.data(), n, host_tokens, nullptr, d->acc_dev[buf],
+                                    d->recycle, d->bitmask[buf], d->bstride, d->pool->max_w, d->logits[buf], eb, neg,
+                                    d->vocab, d->lstride * eb, s);
     if (st) return st;
     GM_CUDA_TRY(cudaEventRecord(d->k5[buf], s));
     GM_CUDA_TRY(cudaStreamWaitEvent(d->copy_out, d->k5[buf], 0));

@@ -374,7 +374,9 @@ struct StepArgs {
 // the host's sampled ids by value: no H2D copy on the step's path).
 constexpr int kParamTokens = 512;
 struct TokParams {
-  int32_t v[kParamTokens];
+  int32_t v[kParamTokens];     // token ids (when has_tok)
+  int32_t slot[kParamTokens];  // slot ids: the header load needs no global round trip first
+  int32_t has_tok;
 };
 
 template <bool APPLY, bool ACCEPT>
@@ -382,7 +384,7 @@ __device__ __forceinline__ void
 fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
           int64_t bstride, const int32_t* __restrict__ rows, uint8_t* __restrict__ need_apply, int32_t Wp,
           char* __restrict__ logits, int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg,
-          StepArgs SA, const int32_t* ptok) {
+          StepArgs SA, const int32_t* ptok, const int32_t* pslot = nullptr) {
   extern __shared__ __align__(16) uint8_t smem[];
   const size_t part_bytes = ((size_t)Wp * 4 + 15) & ~(size_t)15;
   uint32_t* dep_acc = reinterpret_cast<uint32_t*>(smem);  // [Wp] this CTA's words
@@ -415,7 +417,7 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   unsigned long long acc_ts[4] = {0, 0, 0, 0};  // accept: commit start, frames interned, ring written
   unsigned long long t_pref = 0, t_pre = 0;  // accept: frames interned, header state built
   if (kTimeline && P.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-  const int32_t slot = __ldg(slots + i);
+  const int32_t slot = pslot ? pslot[i] : __ldg(slots + i);
   const int64_t row = rows ? (int64_t)__ldg(rows + i) : (int64_t)i;
   __shared__ RingPos rp;
   __shared__ int4 s_rec[2];
@@ -953,7 +955,7 @@ step_ptok_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32
                  int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg, StepArgs SA,
                  const __grid_constant__ TokParams tp) {
   fill_body<APPLY, true>(P, slots, n, bitmask, bstride, rows, nullptr, Wp, logits, lstride_bytes, ap_vocab, ap_eb,
-                         ap_neg, SA, tp.v);
+                         ap_neg, SA, tp.has_tok ? tp.v : nullptr, tp.slot);
 }
 
 template <bool APPLY, bool ACCEPT>
@@ -1071,17 +1073,24 @@ static gm_status ptok_attrs() {
   return GM_OK;
 }
 
-gm_status launch_step_ptok(const DevPool& P, const int32_t* slots, int32_t n, const int32_t* host_tokens,
-                           uint8_t* accepted, int32_t recycle, int32_t* bitmask, int64_t bstride, int32_t Wmax,
-                           void* logits, int32_t eb, uint32_t neg, int64_t vocab, int64_t lstride_bytes,
-                           cudaStream_t s) {
+// K5 with the slot ids (and, when host_tokens is non-null, the token ids)
+// by value in the launch parameters; with host_tokens null the tokens come
+// from device_tokens (nullable: no accept, first step).
+gm_status launch_step_ptok(const DevPool& P, const int32_t* host_slots, int32_t n, const int32_t* host_tokens,
+                           const int32_t* device_tokens, uint8_t* accepted, int32_t recycle, int32_t* bitmask,
+                           int64_t bstride, int32_t Wmax, void* logits, int32_t eb, uint32_t neg, int64_t vocab,
+                           int64_t lstride_bytes, cudaStream_t s) {
   if (n <= 0) return GM_OK;
-  if (n > kParamTokens) return fail(GM_ERR_INVALID, "batch too large for parameter-passed token ids");
+  if (n > kParamTokens) return fail(GM_ERR_INVALID, "batch too large for parameter-passed slot / token ids");
   const size_t smem = fill_smem(split_words(Wmax, 1));
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
   TokParams tp;
-  std::memcpy(tp.v, host_tokens, (size_t)n * 4);
-  const StepArgs sa{nullptr, accepted, recycle};
+  std::memset(&tp, 0, sizeof(tp));
+  if (host_tokens) std::memcpy(tp.v, host_tokens, (size_t)n * 4);
+  std::memcpy(tp.slot, host_slots, (size_t)n * 4);
+  tp.has_tok = host_tokens != nullptr;
+  const int32_t* slots = nullptr;  // the kernel reads tp.slot
+  const StepArgs sa{host_tokens ? nullptr : device_tokens, accepted, recycle};
   const L2Window win{P.l2_base, P.l2_bytes, P.l2_hit};
   uint32_t* bm = reinterpret_cast<uint32_t*>(bitmask);
   if (logits) {

@@ -324,7 +324,7 @@ class BatchGrammarMatcher:
         if tokens is not None and accepted is None:
             accepted = torch.empty(len(matchers), dtype=torch.uint8, device=slots.device)
         batch_step(get_pool(), slots, tokens, accepted if tokens is not None else None, bitmask, logits,
-                   recycle=recycle)
+                   recycle=recycle, host_slots=[m.slot for m in matchers])
         return accepted if tokens is not None else None
 
     @staticmethod
@@ -368,7 +368,7 @@ def batch_fill_apply(pool: MatcherPool, slots: torch.Tensor, logits: torch.Tenso
 def batch_step(pool: MatcherPool, slots: torch.Tensor, tokens: Optional[torch.Tensor], accepted: Optional[torch.Tensor],
                bitmask: Optional[torch.Tensor] = None, logits: Optional[torch.Tensor] = None,
                rows: Optional[torch.Tensor] = None, recycle: bool = False, vocab_size: Optional[int] = None,
-               stream=None) -> None:
+               stream=None, host_slots: Optional[Sequence[int]] = None) -> None:
     """K5, one launch per decode step: accept ``tokens`` (int32 CUDA or pinned
     host, or None for the first step) into ``accepted`` (uint8 CUDA or pinned
     host; host buffers are read/written by the kernel directly), optionally restart
@@ -384,6 +384,16 @@ def batch_step(pool: MatcherPool, slots: torch.Tensor, tokens: Optional[torch.Te
         if t is not None and t.device.type == "cpu" and not t.is_pinned():
             raise ValueError("tokens / accepted must be CUDA tensors or pinned host tensors")
     v = (logits.shape[1] if vocab_size is None else vocab_size) if logits is not None else 0
+    if host_slots is not None and rows is None and len(host_slots) <= 512 and (tokens is None or tokens.is_cuda):
+        # slot ids by value in the launch parameters (host copy of ``slots``)
+        hs = np.ascontiguousarray(np.asarray(host_slots, dtype=np.int32))
+        _lib.check(_lib.load().gm_step_tokens_host_slots(
+            pool.handle, hs.ctypes.data, len(hs), tokens.data_ptr() if tokens is not None else None,
+            accepted.data_ptr() if accepted is not None else None, 1 if recycle else 0,
+            bitmask.data_ptr() if bitmask is not None else None, bitmask.stride(0) if bitmask is not None else 0,
+            logits.data_ptr() if logits is not None else None, _DTYPES[logits.dtype] if logits is not None else 0, v,
+            logits.stride(0) if logits is not None else 0, _lib.stream_ptr(stream)), "gm_step_tokens_host_slots")
+        return
     _lib.check(_lib.load().gm_step_tokens(
         pool.handle, slots.data_ptr(), slots.numel(), tokens.data_ptr() if tokens is not None else None,
         accepted.data_ptr() if accepted is not None else None, 1 if recycle else 0,

@@ -175,6 +175,30 @@ typedef struct gm_fe_tables {
   const int32_t* rule_start;   /* [n_rules]     */
 } gm_fe_tables;
 
+/* Native grammar parser (the rest of SURVEY §8f rank 2): EBNF text (UTF-8,
+ * len bytes) -> the prefix IR gm_front_end_build takes, with the rule names
+ * ('\0'-separated, name i = names + name_off[i]) and the root rule index
+ * (root_rule_name, nullable: `root` if defined, else the first rule).
+ * Surface semantics and every error message / position are those of REF
+ * grammar.py (restated in paper_2411_15100_b200/grammar.py, which the tests
+ * compare it with).  On GM_ERR_GRAMMAR the view's error / err_line /
+ * err_col describe the GrammarError (line 0: no position) and *out must
+ * still be released.  Host only. */
+typedef struct gm_parsed gm_parsed;
+typedef struct gm_parse_view {
+  const int32_t* ir;
+  int64_t ir_len;
+  int32_t n_rules;
+  int32_t root_rule;
+  const char* names;
+  const int64_t* name_off;   /* [n_rules + 1] */
+  const char* error;
+  int32_t err_line, err_col;
+} gm_parse_view;
+gm_status gm_grammar_parse(const uint8_t* text, int64_t len, const char* root_rule_name,
+                           gm_parsed** out, gm_parse_view* view);
+void gm_grammar_parse_release(gm_parsed* g);
+
 typedef struct gm_front_end gm_front_end;
 gm_status gm_front_end_build(const int32_t* ir, int64_t ir_len, int32_t n_rules,
                              int32_t root_rule, const gm_fe_options* opts,

@@ -74,6 +74,12 @@ class gm_fe_tables(C.Structure):
         ("n_raw", C.c_int32), ("finals", C.c_void_p), ("rule_start", C.c_void_p)]
 
 
+class gm_parse_view(C.Structure):
+    _fields_ = [("ir", C.c_void_p), ("ir_len", C.c_int64), ("n_rules", C.c_int32), ("root_rule", C.c_int32),
+                ("names", C.c_void_p), ("name_off", C.c_void_p), ("error", C.c_char_p), ("err_line", C.c_int32),
+                ("err_col", C.c_int32)]
+
+
 class gm_cache_stats(C.Structure):
     _fields_ = [
         ("n_keys", C.c_int32),
@@ -134,6 +140,8 @@ _SIGNATURES = {
     "gm_front_end_build": ([_P, _I64, _I32, _I32, C.POINTER(gm_fe_options), C.POINTER(_P),
                             C.POINTER(gm_fe_tables)], _I32),
     "gm_front_end_release": ([_P], None),
+    "gm_grammar_parse": ([_P, _I64, C.c_char_p, C.POINTER(_P), C.POINTER(gm_parse_view)], _I32),
+    "gm_grammar_parse_release": ([_P], None),
 }
 
 _lib = None

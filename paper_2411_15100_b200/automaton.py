@@ -34,7 +34,8 @@ import numpy as np
 
 from .grammar import Alt, Bytes, Eps, GrammarError, Lit, ParsedGrammar, Ref, Rep, Seq
 
-__all__ = ["StateLimitError", "CompiledTables", "AutomatonOptions", "build_tables_native", "encode_ir"]
+__all__ = ["StateLimitError", "CompiledTables", "AutomatonOptions", "NativeParsed", "build_tables_native",
+           "encode_ir", "parse_grammar_native"]
 
 DEFAULT_STATE_CAP = 4096  # REF pda.py:53
 _FOLLOW_DEAD, _FOLLOW_ANY = -1, -2
@@ -130,7 +131,51 @@ def encode_ir(g: ParsedGrammar) -> Tuple[np.ndarray, Dict[str, int]]:
     return arr.astype(np.uint32).view(np.int32) if arr.size else arr.astype(np.int32), rid_of
 
 
-def build_tables_native(g: ParsedGrammar, opts: Optional[AutomatonOptions] = None) -> CompiledTables:
+@dataclass
+class NativeParsed:
+    """A grammar parsed by the native parser (gm_grammar_parse): rule names in
+    source order, the root, and the prefix IR the front end takes."""
+
+    names: List[str]
+    root: str
+    ir: np.ndarray
+
+    @property
+    def bodies(self) -> Dict[str, None]:  # membership tests (compile_grammar's root choice)
+        return dict.fromkeys(self.names)
+
+
+def parse_grammar_native(text: str, root_rule_name: Optional[str] = None) -> NativeParsed:
+    """EBNF text -> NativeParsed through libgmask's C++ parser: the same IR,
+    names, root and GrammarError (message, line, column) as
+    grammar.parse_grammar + encode_ir (tests/test_frontend.py)."""
+    import ctypes as C
+
+    from . import _lib
+
+    lib = _lib.load()
+    data = text.encode("utf-8", "surrogatepass")
+    view = _lib.gm_parse_view()
+    h = C.c_void_p()
+    st = lib.gm_grammar_parse(data, len(data), root_rule_name.encode() if root_rule_name is not None else None,
+                              C.byref(h), C.byref(view))
+    try:
+        if st == _lib.GM_ERR_GRAMMAR:
+            raise GrammarError(view.error.decode("utf-8", "replace"), view.err_line or None, view.err_col or None)
+        _lib.check(st, "gm_grammar_parse")
+        n = view.n_rules
+        off = np.ctypeslib.as_array(C.cast(view.name_off, C.POINTER(C.c_int64)), shape=(n + 1,))
+        blob = C.string_at(view.names, int(off[-1]))
+        names = [blob[off[i]:off[i + 1] - 1].decode() for i in range(n)]
+        ir = (np.ctypeslib.as_array(C.cast(view.ir, C.POINTER(C.c_int32)), shape=(view.ir_len,)).copy()
+              if view.ir_len else np.zeros(0, np.int32))
+        return NativeParsed(names, names[view.root_rule], ir)
+    finally:
+        if h:
+            lib.gm_grammar_parse_release(h)
+
+
+def build_tables_native(g, opts: Optional[AutomatonOptions] = None) -> CompiledTables:
     """build_tables through libgmask's C++ front end (gm_front_end_build):
     identical tables (tests/test_frontend.py compares them array for array),
     a fraction of the host time."""
@@ -141,7 +186,10 @@ def build_tables_native(g: ParsedGrammar, opts: Optional[AutomatonOptions] = Non
     opts = opts or AutomatonOptions()
     if not opts.determinize:
         raise NotImplementedError("determinize=False is not supported by the device tables")
-    ir, rid_of = encode_ir(g)
+    if isinstance(g, NativeParsed):
+        ir, rid_of = g.ir, {nm: i for i, nm in enumerate(g.names)}
+    else:
+        ir, rid_of = encode_ir(g)
     ir = np.ascontiguousarray(ir)
     fo = _lib.gm_fe_options(1, int(opts.inline), int(opts.ctx_expansion), opts.inline_max_rule_states,
                             opts.inline_max_result_states, opts.max_dfa_states, opts.max_follow_states,

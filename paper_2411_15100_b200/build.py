@@ -21,7 +21,7 @@ OUT = PKG / "libgmask.so"
 BUILD = PKG / "_build"
 
 SOURCES = ["gm_api.cu", "k_apply.cu", "k_cache.cu", "k_fill.cu", "k_accept.cu"]
-HOST_SOURCES = ["front_end.cpp"]  # host-only C++ (g++)
+HOST_SOURCES = ["front_end.cpp", "grammar_parse.cpp"]  # host-only C++ (g++)
 HEADERS = ["common.cuh", "device.cuh", "accept.cuh"]
 
 NVCC_FLAGS = [

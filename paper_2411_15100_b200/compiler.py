@@ -194,10 +194,10 @@ class GrammarCompiler:
         rule exists, else the grammask default (first rule)."""
         import dataclasses
 
-        from .grammar import parse_grammar
+        from .automaton import parse_grammar_native
 
-        g = parse_grammar(grammar)  # parsed once: the root is chosen on the parse result
-        root = root_rule_name if root_rule_name in g.bodies else None
+        g = parse_grammar_native(grammar)  # parsed once (native): the root is chosen on the result
+        root = root_rule_name if root_rule_name in g.names else None
         if root is not None and g.root != root:
             g = dataclasses.replace(g, root=root)
         return self._compile(grammar, root, parsed=g)

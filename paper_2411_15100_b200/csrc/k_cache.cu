@@ -117,29 +117,41 @@ __global__ void row_popcount_kernel(const uint32_t* __restrict__ rows, int32_t W
 }
 
 // Sorted id lists of the dependent rows (REF cache.py:400-402 sorts them).
-// One warp per key walks the row in order; ballot + prefix keeps it ordered.
-__global__ void dep_compact_kernel(const uint32_t* __restrict__ rows, int32_t W, int32_t n,
-                                   const int32_t* __restrict__ dep_off, int32_t* __restrict__ dep_ids) {
+// One CTA per key: every thread counts the set bits of a contiguous run of
+// words, a block-wide exclusive scan gives each run its output offset, and
+// the run is written in order — one pass over the row instead of a serial
+// warp walk (82 us -> a few us for JSON at 128k).
+constexpr int kCompactThreads = 256;
+__global__ void __launch_bounds__(kCompactThreads)
+dep_compact_kernel(const uint32_t* __restrict__ rows, int32_t W, int32_t n, const int32_t* __restrict__ dep_off,
+                   int32_t* __restrict__ dep_ids) {
   const int32_t k = blockIdx.x;
-  if (k >= n || threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  int32_t base = dep_off[k];
-  for (int32_t w0 = 0; w0 < W; w0 += 32) {
-    const int32_t w = w0 + lane;
-    uint32_t bits = w < W ? rows[(size_t)k * W + w] : 0u;
-    const int cnt = __popc(bits);
-    int incl = cnt;
-    for (int o = 1; o < 32; o <<= 1) {
-      int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    int pos = base + incl - cnt;
+  if (k >= n) return;
+  const uint32_t* row = rows + (size_t)k * W;
+  const int32_t per = (W + kCompactThreads - 1) / kCompactThreads;
+  const int32_t w0 = min(W, (int32_t)threadIdx.x * per), w1 = min(W, w0 + per);
+  int cnt = 0;
+  for (int32_t w = w0; w < w1; ++w) cnt += __popc(__ldg(row + w));
+  // block exclusive scan of cnt
+  __shared__ int warp_sum[kCompactThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = cnt;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_sum[warp] = incl;
+  __syncthreads();
+  int before = 0;
+  for (int j = 0; j < warp; ++j) before += warp_sum[j];
+  int pos = dep_off[k] + before + incl - cnt;
+  for (int32_t w = w0; w < w1; ++w) {
+    uint32_t bits = __ldg(row + w);
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
       dep_ids[pos++] = w * 32 + b;
     }
-    base += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 
@@ -314,7 +326,7 @@ gm_status launch_dep_context2(const DevGrammar& G, const int32_t* dep_off, int32
 gm_status launch_dep_compact(const uint32_t* rows, int32_t W, int32_t n, const int32_t* off,
                              int32_t* ids, cudaStream_t s) {
   if (n <= 0) return GM_OK;
-  dep_compact_kernel<<<n, 32, 0, s>>>(rows, W, n, off, ids);
+  dep_compact_kernel<<<n, kCompactThreads, 0, s>>>(rows, W, n, off, ids);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

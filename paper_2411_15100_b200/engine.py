@@ -21,8 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .automaton import AutomatonOptions, CompiledTables, StateLimitError, build_tables_native
-from .grammar import parse_grammar
+from .automaton import AutomatonOptions, CompiledTables, StateLimitError, build_tables_native, parse_grammar_native
 from .vocab import Vocabulary
 
 __all__ = ["MatcherError", "RequestErrors", "DeviceVocab", "DeviceGrammar", "DeviceCache", "CompiledDeviceGrammar",
@@ -292,7 +291,7 @@ def compile_on_device(text: str, dvocab: DeviceVocab, opts: Optional[AutomatonOp
     cost (``key_costs``) and the rows replicated with one all-gather
     (SURVEY §8e)."""
     t0 = time.perf_counter()
-    tables = build_tables_native(parsed if parsed is not None else parse_grammar(text, root_rule_name), opts)
+    tables = build_tables_native(parsed if parsed is not None else parse_grammar_native(text, root_rule_name), opts)
     t1 = time.perf_counter()
     grammar = DeviceGrammar(tables)
     n_keys = grammar.n_keys
@@ -337,7 +336,7 @@ def compile_many_on_device(texts, dvocab: DeviceVocab, opts: Optional[AutomatonO
     world = dist.get_world_size(group) if group is not None else 1
     rank = dist.get_rank(group) if group is not None else 0
     t0 = time.perf_counter()
-    mine = {i: build_tables_native(parse_grammar(texts[i]), opts) for i in range(rank, len(texts), world)}
+    mine = {i: build_tables_native(parse_grammar_native(texts[i]), opts) for i in range(rank, len(texts), world)}
     t1 = time.perf_counter()
     if world > 1:
         parts = [None] * world

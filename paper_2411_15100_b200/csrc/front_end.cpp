@@ -518,9 +518,15 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
     dfas[r] = minimize(det_or_nfa(bld.a, n_classes, o.max_dfa_states));
   }
   if (o.inline_rules) {
+    // a host whose inlining was refused (too many states / DFA limit) is not
+    // retried while neither it nor any of its targets has changed (version
+    // counters): the retry would refuse again
+    std::vector<int64_t> version(n_rules_in, 0);
+    std::vector<std::vector<int64_t>> refused(n_rules_in);
     for (int pass = 0; pass < 64; ++pass) {
       std::vector<char> inl(n_rules_in, 0);
       std::vector<Dfa> snap(n_rules_in);
+      const std::vector<int64_t> snap_version = version;
       for (int r = 0; r < n_rules_in; ++r)
         if (!has_calls(dfas[r]) && dfas[r].size() <= o.inline_max_rule_states) {
           inl[r] = 1;
@@ -556,14 +562,25 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
           for (auto& e : cs)
             if (inl[e.first] && e.first != host) targets[e.first] = &snap[e.first];
         if (targets.empty()) continue;
+        std::vector<int64_t> sig{version[host]};
+        for (auto& kv : targets) {
+          sig.push_back(kv.first);
+          sig.push_back(snap_version[kv.first]);
+        }
+        if (sig == refused[host]) continue;
         Dfa nd;
         try {
           nd = minimize(determinize(inline_into(dfas[host], targets), n_classes, o.max_dfa_states));
         } catch (const DfaLimit&) {
+          refused[host] = sig;
           continue;  // inlining here would blow the subset construction up: keep the calls
         }
-        if (nd.size() > o.inline_max_result_states) continue;
+        if (nd.size() > o.inline_max_result_states) {
+          refused[host] = sig;
+          continue;
+        }
         dfas[host] = std::move(nd);
+        ++version[host];
         changed = true;
       }
       if (!changed) break;
@@ -628,6 +645,7 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
   std::vector<char> is_key(n_nodes, 0);
   is_key[start_node] = 1;
   typedef std::pair<std::vector<int>, int> St;
+  std::vector<std::vector<St>> per_class(n_classes);
   for (int u = 0; u < n_nodes; ++u) {
     std::map<St, char> seen;  // ordered: sorted(seen)
     std::vector<St> wk;
@@ -659,7 +677,7 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
             throw CapFail("branch set exceeded cap of " + std::to_string(o.state_cap));
         }
     }
-    std::vector<std::vector<St>> per_class(n_classes);
+    for (auto& v : per_class) v.clear();  // reused across nodes (no per-node allocation)
     for (auto& kv : seen) {
       const std::vector<int>& P = kv.first.first;
       const int m = kv.first.second;
@@ -678,7 +696,8 @@ void build(const Ir& ir, int32_t n_rules_in, int32_t root_in, const gm_fe_option
     for (int c = 0; c < n_classes; ++c) {
       trans_off[(size_t)u * n_classes + c] = (int64_t)trans_flat.size() / 2;
       auto& lst = per_class[c];
-      std::sort(lst.begin(), lst.end(), [](const St& a, const St& b) {
+      if (lst.size() > 1)
+        std::sort(lst.begin(), lst.end(), [](const St& a, const St& b) {
         if (a.second != b.second) return a.second < b.second;
         return a.first < b.first;
       });

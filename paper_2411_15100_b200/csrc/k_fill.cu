@@ -372,10 +372,14 @@ struct StepArgs {
 
 // Token ids carried in the launch parameters (the native decode loop passes
 // the host's sampled ids by value: no H2D copy on the step's path).
+// Sized to the batch (64 / 128 / 256 / 512 requests): the launch's
+// parameter block stays small — above 4 KB of parameters the driver takes a
+// slower path (measured: host issue +3 us per step with 512-entry arrays).
 constexpr int kParamTokens = 512;
+template <int N>
 struct TokParams {
-  int32_t v[kParamTokens];     // token ids (when has_tok)
-  int32_t slot[kParamTokens];  // slot ids: the header load needs no global round trip first
+  int32_t v[N];     // token ids (when has_tok)
+  int32_t slot[N];  // slot ids: the header load needs no global round trip first
   int32_t has_tok;
 };
 
@@ -948,12 +952,12 @@ fill_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* _
 
 // K5 with the token ids in the launch parameters (__grid_constant__: read
 // in place from the parameter bank)
-template <bool APPLY>
+template <bool APPLY, int N>
 __global__ void __maxnreg__(128)
 step_ptok_kernel(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __restrict__ bitmask,
                  int64_t bstride, const int32_t* __restrict__ rows, int32_t Wp, char* __restrict__ logits,
                  int64_t lstride_bytes, int64_t ap_vocab, int ap_eb, uint32_t ap_neg, StepArgs SA,
-                 const __grid_constant__ TokParams tp) {
+                 const __grid_constant__ TokParams<N> tp) {
   fill_body<APPLY, true>(P, slots, n, bitmask, bstride, rows, nullptr, Wp, logits, lstride_bytes, ap_vocab, ap_eb,
                          ap_neg, SA, tp.has_tok ? tp.v : nullptr, tp.slot);
 }
@@ -1066,10 +1070,40 @@ gm_status launch_step(const DevPool& P, const int32_t* slots, int32_t n, const i
 }
 
 // K5 from the native decode loop: token ids by value (n <= kParamTokens).
-template <bool APPLY>
+template <bool APPLY, int N>
 static gm_status ptok_attrs() {
-  GM_CUDA_TRY(cudaFuncSetAttribute(step_ptok_kernel<APPLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  GM_CUDA_TRY(cudaFuncSetAttribute(step_ptok_kernel<APPLY>, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
+  GM_CUDA_TRY(cudaFuncSetAttribute(step_ptok_kernel<APPLY, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  GM_CUDA_TRY(cudaFuncSetAttribute(step_ptok_kernel<APPLY, N>, cudaFuncAttributePreferredSharedMemoryCarveout, 25));
+  return GM_OK;
+}
+
+template <int N>
+static gm_status launch_step_ptok_n(const DevPool& P, const int32_t* host_slots, int32_t n, const int32_t* host_tokens,
+                                    const int32_t* device_tokens, uint8_t* accepted, int32_t recycle, int32_t* bitmask,
+                                    int64_t bstride, int32_t Wmax, void* logits, int32_t eb, uint32_t neg,
+                                    int64_t vocab, int64_t lstride_bytes, size_t smem, cudaStream_t s) {
+  TokParams<N> tp;
+  std::memset(&tp, 0, sizeof(tp));
+  if (host_tokens) std::memcpy(tp.v, host_tokens, (size_t)n * 4);
+  std::memcpy(tp.slot, host_slots, (size_t)n * 4);
+  tp.has_tok = host_tokens != nullptr;
+  const int32_t* slots = nullptr;  // the kernel reads tp.slot
+  const StepArgs sa{host_tokens ? nullptr : device_tokens, accepted, recycle};
+  const L2Window win{P.l2_base, P.l2_bytes, P.l2_hit};
+  uint32_t* bm = reinterpret_cast<uint32_t*>(bitmask);
+  if (logits) {
+    static gm_status attrs = ptok_attrs<true, N>();
+    if (attrs) return attrs;
+    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<true, N>, dim3(n, 1), dim3(fill_threads(1)), smem, s, P, slots, n,
+                             bm, bstride, (const int32_t*)nullptr, split_words(Wmax, 1), static_cast<char*>(logits),
+                             lstride_bytes, vocab, (int)eb, neg, sa, tp));
+  } else {
+    static gm_status attrs = ptok_attrs<false, N>();
+    if (attrs) return attrs;
+    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<false, N>, dim3(n, 1), dim3(fill_threads(1)), smem, s, P, slots, n,
+                             bm, bstride, (const int32_t*)nullptr, split_words(Wmax, 1), (char*)nullptr, (int64_t)0,
+                             (int64_t)0, 2, 0u, sa, tp));
+  }
   return GM_OK;
 }
 
@@ -1084,29 +1118,14 @@ gm_status launch_step_ptok(const DevPool& P, const int32_t* host_slots, int32_t 
   if (n > kParamTokens) return fail(GM_ERR_INVALID, "batch too large for parameter-passed slot / token ids");
   const size_t smem = fill_smem(split_words(Wmax, 1));
   if (smem > 220 * 1024) return fail(GM_ERR_INVALID, "vocabulary too large for the fill kernel");
-  TokParams tp;
-  std::memset(&tp, 0, sizeof(tp));
-  if (host_tokens) std::memcpy(tp.v, host_tokens, (size_t)n * 4);
-  std::memcpy(tp.slot, host_slots, (size_t)n * 4);
-  tp.has_tok = host_tokens != nullptr;
-  const int32_t* slots = nullptr;  // the kernel reads tp.slot
-  const StepArgs sa{host_tokens ? nullptr : device_tokens, accepted, recycle};
-  const L2Window win{P.l2_base, P.l2_bytes, P.l2_hit};
-  uint32_t* bm = reinterpret_cast<uint32_t*>(bitmask);
-  if (logits) {
-    static gm_status attrs = ptok_attrs<true>();
-    if (attrs) return attrs;
-    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<true>, dim3(n, 1), dim3(fill_threads(1)), smem, s, P, slots, n, bm,
-                             bstride, (const int32_t*)nullptr, split_words(Wmax, 1), static_cast<char*>(logits),
-                             lstride_bytes, vocab, (int)eb, neg, sa, tp));
-  } else {
-    static gm_status attrs = ptok_attrs<false>();
-    if (attrs) return attrs;
-    GM_CUDA_TRY(launch_pdl_w(&win, step_ptok_kernel<false>, dim3(n, 1), dim3(fill_threads(1)), smem, s, P, slots, n, bm,
-                             bstride, (const int32_t*)nullptr, split_words(Wmax, 1), (char*)nullptr, (int64_t)0,
-                             (int64_t)0, 2, 0u, sa, tp));
-  }
-  return GM_OK;
+#define GM_PTOK(N)                                                                                                  \
+  return launch_step_ptok_n<N>(P, host_slots, n, host_tokens, device_tokens, accepted, recycle, bitmask, bstride, \
+                               Wmax, logits, eb, neg, vocab, lstride_bytes, smem, s)
+  if (n <= 64) GM_PTOK(64);
+  if (n <= 128) GM_PTOK(128);
+  if (n <= 256) GM_PTOK(256);
+  GM_PTOK(kParamTokens);
+#undef GM_PTOK
 }
 
 }  // namespace gm

@@ -63,18 +63,21 @@ def test_apply_rejects_cpu():
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("policy", [0, 1, 528, 0x0F10])
-def test_apply_mixed_chunk_policy_exact(dtype, policy):
+@pytest.mark.parametrize("vocab", [128256, 32011])
+def test_apply_mixed_chunk_policy_exact(dtype, policy, vocab):
     """K0's runtime mixed-chunk policy (gm_apply_set_blend): element stores,
     blend always, the default and a strict threshold give the same exact
-    result on masks with dense, sparse and heavily masked mixed chunks;
-    logits past the vocabulary and rows not listed stay untouched."""
+    result on masks with dense, sparse and heavily masked mixed chunks, also
+    with a ragged last word; logits past the vocabulary and rows not listed
+    stay untouched."""
     from paper_2411_15100_b200 import _lib, apply_token_bitmask_inplace
 
     lib = _lib.load()
-    g = torch.Generator(device="cuda").manual_seed(policy + 1)
-    B, vocab = 9, 128256
+    g = torch.Generator(device="cuda").manual_seed(policy + vocab)
+    B = 9
     W = (vocab + 31) // 32
-    logits = torch.randn(B, vocab + 8, device="cuda", generator=g).to(dtype)
+    width = (vocab + 7) // 8 * 8 + 8  # 16-byte aligned rows (the tiled kernel), columns past the vocabulary
+    logits = torch.randn(B, width, device="cuda", generator=g).to(dtype)
     bm = torch.randint(-2**31, 2**31 - 1, (B, W), device="cuda", dtype=torch.int32, generator=g)  # dense mixed
     bm[1] = bm[1] | 0x7F7F7F7F        # mixed chunks with one masked element
     bm[2] = bm[2] & 0x01010101        # heavily masked mixed chunks

@@ -229,6 +229,31 @@ def profiled_traffic(kernel_tag: str):
     return None
 
 
+def physical_apply_bytes(masks, V: int, es: int = 2) -> float:
+    """Mean bytes per step an apply must move at 32-byte sector granularity
+    over masks [S, B, W] (int32 bitmask words): the mask words, a write of
+    every fully masked sector, a read + write of every mixed sector (some
+    logits kept, some masked: the memory system merges a partial write with
+    the sector's old bytes, or the kernel blends them itself); fully allowed
+    sectors move nothing.  The algorithmic count (mask + es B per masked
+    logit) is the lower bound for bimodal masks; this one is the bound for
+    masks whose allowed tokens are interleaved with masked ones (XML, SQL)."""
+    S, B, W = masks.shape
+    tps = 32 // es  # tokens per 32-byte sector: 16 (2-byte logits) or 8 (fp32)
+    full = (1 << tps) - 1
+    # sectors past the vocabulary (last word) are bitmask padding: dropped
+    pad_sectors = W * 32 // tps - (V + tps - 1) // tps
+    n_full_masked = n_mixed = 0
+    for s in range(S):  # one step at a time: small temporaries
+        m = masks[s].to(torch.int64) & 0xFFFFFFFF
+        parts = torch.stack([(m >> (k * tps)) & full for k in range(32 // tps)], dim=-1)  # [B, W, sectors]
+        if pad_sectors > 0:
+            parts[:, -1, (32 // tps) - pad_sectors:] = full
+        n_full_masked += int((parts == 0).sum())
+        n_mixed += int(((parts != 0) & (parts != full)).sum())
+    return (S * B * W * 4 + 32 * n_full_masked + 64 * n_mixed) / S
+
+
 def measure_write_ceiling(dev) -> float:
     """Store-only bandwidth of this GPU, measured live: torch's fill_ of a
     256 MiB buffer (twice the L2), 10 launches back to back in one event
@@ -653,6 +678,7 @@ def run_ours(args, rank: int, world: int, group) -> dict:
         "compile_ms": mx(statistics.median(compile_ms)),
         "compile_split_ms": compile_split,
         "masked_mean": float(masked_h.mean()),
+        "physical_apply_bytes": physical_apply_bytes(masks_all[W0:], V),
         "V": V, "W": W, "B": B,
         "clocks": clocks.summary(),
         "clocks_value": clocks_t.summary(),
@@ -1110,6 +1136,9 @@ def main():
             "k0_apply_b2b_gbs": k0_bytes / (r["k0_b2b_us"] * 1e-6) / 1e9,
             "k0_apply_b2b_frac": k0_bytes / (r["k0_b2b_us"] * 1e-6) / 1e9 / peak,
             "k0_apply_b2b_frac_of_write_ceiling": k0_bytes / (r["k0_b2b_us"] * 1e-6) / 1e9 / r["write_ceiling_gbs"],
+            # at sector granularity (bench.physical_apply_bytes): mixed sectors are read and written
+            "k0_apply_physical_bytes_per_step": r["physical_apply_bytes"],
+            "k0_apply_b2b_physical_frac": r["physical_apply_bytes"] / (r["k0_b2b_us"] * 1e-6) / 1e9 / peak,
             "compile_ms": r["compile_ms"],
             "compile_split_ms": r["compile_split_ms"],
             "masked_fraction": r["masked_mean"] / (B * V),

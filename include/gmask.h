@@ -70,7 +70,10 @@ gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_rows,
  * warp whose store round has at least min_lanes mixed chunks loads them,
  * blends in -inf and writes each with one full store; otherwise (or with
  * min_lanes = 0) it writes only the masked elements.  Returns the previous
- * value.  Default: GMASK_APPLY_BLEND at load, else the build's default. */
+ * value.  Default: GMASK_APPLY_BLEND at load, else the build's default.
+ * The fused apply (K3/K5) blends the rows of the cache keys whose accepted
+ * row meets the same thresholds (scaled to the row), decided when the cache
+ * is built (gm_cache_create) with the policy in force then. */
 int32_t gm_apply_set_blend(int32_t min_lanes);
 
 /* ------------------------------------------------------------------------ */
@@ -251,6 +254,7 @@ typedef struct gm_cache_stats {
   int64_t dependent_total;
   int64_t rejected_total;
   int64_t row_bytes;        /* dense rows resident in HBM */
+  int32_t blend_keys;       /* keys whose rows the fused apply blends (gm_apply_set_blend) */
 } gm_cache_stats;
 gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v,
                           const int32_t* acc_rows, const int32_t* dep_rows,

@@ -87,6 +87,7 @@ class gm_cache_stats(C.Structure):
         ("dependent_total", C.c_int64),
         ("rejected_total", C.c_int64),
         ("row_bytes", C.c_int64),
+        ("blend_keys", C.c_int32),
     ]
 
 

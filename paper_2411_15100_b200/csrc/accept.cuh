@@ -254,7 +254,7 @@ __device__ inline int accept_one(const DevPool& P, int32_t slot, const RingPos& 
       h.dep_hi[0] = ni.z;
       h.top[0] = t;
       h.ntops = 1;
-      h.flags = term ? 2 : 0;
+      h.flags = (term ? 2 : 0) | ((ni.w >> 28) & 4);  // 4: the fused apply blends this key's row
       if (spec) spec->n = 0;
       return kAccOk;
     }

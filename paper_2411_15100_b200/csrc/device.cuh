@@ -1059,7 +1059,7 @@ __device__ inline void build_chain(Chain& c, int32_t cur, const int32_t* fh, con
 // Only the EOS fact may need an arena load (a top whose frame is unknown).
 __device__ inline void header_state(const DevPool& P, SlotHdr& h, const DevGrammar& G, const int2* tops, int n,
                                     int terminated, const Chain* chain) {
-  int term = 0;
+  int term = 0, blend = 0;
   for (int s = 0; s < n; ++s) {
     const int2 t = tops[s];
     if (!terminated && !term && (G.node_flags[t.y] & GM_NODE_POP)) {
@@ -1077,6 +1077,7 @@ __device__ inline void header_state(const DevPool& P, SlotHdr& h, const DevGramm
       h.dep_lo[s] = ni.y;
       h.dep_hi[s] = ni.z;
       h.top[s] = t;
+      blend |= (ni.w >> 28) & 4;
     }
   }
   const int nc = (chain && n > 0) ? chain->n : 0;
@@ -1086,7 +1087,7 @@ __device__ inline void header_state(const DevPool& P, SlotHdr& h, const DevGramm
   }
   h.nchain = nc;
   h.ntops = n <= kHdrTops ? n : -1;
-  h.flags = (terminated ? 1 : 0) | (term ? 2 : 0);
+  h.flags = (terminated ? 1 : 0) | (term ? 2 : 0) | blend;  // 4: a top's row is applied blended
 }
 
 // rwalker_commit for the fused step kernel: interns exactly like
@@ -1232,7 +1233,7 @@ static_assert(offsetof(SlotHdr, ntops) >= kHdrStateVec * 16, "header state offse
 // fields, no chain copy.
 __device__ inline void header_state_inplace(const DevPool& P, SlotHdr& h, const DevGrammar& G, const int2* tops, int n,
                                             int terminated) {
-  int term = 0;
+  int term = 0, blend = 0;
   for (int s = 0; s < n; ++s) {
     const int2 t = tops[s];
     if (!terminated && !term && (G.node_flags[t.y] & GM_NODE_POP)) {
@@ -1249,11 +1250,12 @@ __device__ inline void header_state_inplace(const DevPool& P, SlotHdr& h, const 
       h.dep_lo[s] = ni.y;
       h.dep_hi[s] = ni.z;
       h.top[s] = t;
+      blend |= (ni.w >> 28) & 4;
     }
   }
   if (n == 0) h.nchain = 0;
   h.ntops = n <= kHdrTops ? n : -1;
-  h.flags = (terminated ? 1 : 0) | (term ? 2 : 0);
+  h.flags = (terminated ? 1 : 0) | (term ? 2 : 0) | blend;  // 4: a top's row is applied blended
 }
 
 // Publish the state part of a shared-memory header with the lanes of one

@@ -39,6 +39,8 @@ gm_status launch_fill(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t
 gm_status launch_fill_apply(const DevPool&, const int32_t*, int32_t, int32_t*, int64_t, const int32_t*, int32_t,
                             void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_l2_touch(void* base, size_t bytes, const L2Window& win);
+int32_t apply_blend_policy();
+gm_status launch_row_mixstats(const uint32_t*, int32_t, int32_t, int64_t*, cudaStream_t);
 gm_status launch_step_ptok(const DevPool&, const int32_t*, int32_t, const int32_t*, const int32_t*, uint8_t*, int32_t,
                            int32_t*, int64_t, int32_t, void*, int32_t, uint32_t, int64_t, int64_t, cudaStream_t);
 gm_status launch_step(const DevPool&, const int32_t*, int32_t, const int32_t*, uint8_t*, int32_t, int32_t*, int64_t,
@@ -182,6 +184,7 @@ struct gm_cache {
   DevBinding host_binding;
   DevBinding* binding;  // device copy
   int32_t n_keys;
+  int32_t n_blend_keys = 0;  // keys whose rows the fused apply blends (policy at build)
 };
 
 struct gm_pool {
@@ -549,15 +552,16 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
   const size_t rows_bytes = (size_t)n * W * 4;
   const size_t off_counts = (rows_bytes + 15) & ~size_t(15);
   uint8_t* buf1;
-  if ((st = c->mem.alloc(&buf1, off_counts + (size_t)(2 * n + 1) * 8))) return bail(st);
+  if ((st = c->mem.alloc(&buf1, off_counts + (size_t)(3 * n + 1) * 8))) return bail(st);
   uint32_t* acc = reinterpret_cast<uint32_t*>(buf1);
   int64_t* counts = reinterpret_cast<int64_t*>(buf1 + off_counts);
-  std::vector<int64_t> cnt(2 * (size_t)n);
+  std::vector<int64_t> cnt(3 * (size_t)n);
   if (n) {
     GM_CUDA_TRY(cudaMemcpyAsync(acc, acc_rows, rows_bytes, cudaMemcpyDeviceToDevice, s));
     if ((st = launch_row_popcount(reinterpret_cast<const uint32_t*>(dep_rows), W, n, counts, s))) return bail(st);
     if ((st = launch_row_popcount(acc, W, n, counts + n, s))) return bail(st);
-    GM_CUDA_TRY(cudaMemcpyAsync(cnt.data(), counts, (size_t)2 * n * 8, cudaMemcpyDeviceToHost, s));
+    if ((st = launch_row_mixstats(acc, W, n, counts + 2 * n, s))) return bail(st);
+    GM_CUDA_TRY(cudaMemcpyAsync(cnt.data(), counts, (size_t)3 * n * 8, cudaMemcpyDeviceToHost, s));
     GM_CUDA_TRY(cudaStreamSynchronize(s));
   }
   std::vector<int32_t> off(n + 1, 0);
@@ -568,13 +572,32 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
     if (dep_total > INT32_MAX) return bail(fail(GM_ERR_INVALID, "too many dependent tokens"));
     off[k + 1] = (int32_t)dep_total;
   }
-  // binding blob: grammar blob + node_info (key, dep_lo, dep_hi, rule) per node
+  // Fused-apply policy per key (2-byte logits): a row whose 16-byte chunks
+  // are densely mixed and heavily masked (SQL identifier classes) is applied
+  // with loaded + blended full-chunk stores instead of element stores.  The
+  // thresholds are K0's (gm_apply_set_blend at build time) scaled from its
+  // 1,024-token tile to the row; decided here from the accepted row so the
+  // step kernels pay nothing per step (per-step statistics measured +0.3 us
+  // on JSON).  A step blends when a top's key has the flag (header flag 4)
+  // and the runtime policy is non-zero.
+  const int32_t policy = apply_blend_policy();
+  std::vector<uint8_t> blend_key(n, 0);
+  for (int32_t k = 0; k < n && policy > 0; ++k) {
+    const int64_t mix = (int64_t)((uint64_t)cnt[2 * (size_t)n + k] >> 32);
+    const int64_t nel = (int64_t)((uint64_t)cnt[2 * (size_t)n + k] & 0xFFFFFFFFu);
+    blend_key[k] = mix > 0 && 128 * mix >= (int64_t)(policy & 0xFF) * (int64_t)W * 4 &&
+                   nel >= (int64_t)((policy >> 8) & 0xFF) * mix;
+  }
+  c->n_blend_keys = 0;
+  for (int32_t k = 0; k < n; ++k) c->n_blend_keys += blend_key[k];
+  // binding blob: grammar blob + node_info (key, dep_lo, dep_hi, rule | blend << 30) per node
   std::vector<uint8_t> bblob = g->blob_host;
   const size_t o_ninfo = (bblob.size() + 15) & ~size_t(15);
   bblob.resize(o_ninfo + (size_t)g->dev.n_nodes * 16, 0);
   for (int32_t nd = 0; nd < g->dev.n_nodes; ++nd) {
     const int32_t k = g->key_of_node[nd];
-    int32_t ni[4] = {k, k >= 0 ? off[k] : 0, k >= 0 ? off[k + 1] : 0, g->node_rule[nd]};
+    int32_t ni[4] = {k, k >= 0 ? off[k] : 0, k >= 0 ? off[k + 1] : 0,
+                     g->node_rule[nd] | ((k >= 0 && blend_key[k]) ? (1 << 30) : 0)};
     std::memcpy(bblob.data() + o_ninfo + (size_t)nd * 16, ni, 16);
   }
   BlobHdr bh;
@@ -646,6 +669,7 @@ gm_status gm_cache_create(const gm_grammar* g, const gm_vocab* v, const int32_t*
     stats->dependent_total = dep_total;
     stats->rejected_total = (int64_t)n * n_univ - acc_total - dep_total;
     stats->row_bytes = (int64_t)n * W * 4;
+    stats->blend_keys = c->n_blend_keys;
   }
   *out = c;
   return GM_OK;

@@ -230,12 +230,12 @@ extern "C" gm_status gm_apply_inplace(void* logits, int32_t dtype, int64_t n_row
 }
 
 namespace gm {
-gm_status set_fill_blend(int32_t policy);
-}
+// caches built from now on decide their fused-apply keys with this policy
+int32_t apply_blend_policy() { return g_apply_blend; }
+}  // namespace gm
 
 extern "C" int32_t gm_apply_set_blend(int32_t min_lanes) {
   const int32_t old = gm::g_apply_blend;
   gm::g_apply_blend = min_lanes < 0 ? 0 : min_lanes;
-  gm::set_fill_blend(gm::g_apply_blend);  // the fused apply (K3/K5) follows
   return old;
 }

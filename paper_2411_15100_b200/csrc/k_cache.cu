@@ -116,6 +116,37 @@ __global__ void row_popcount_kernel(const uint32_t* __restrict__ rows, int32_t W
   }
 }
 
+// Mixed-chunk statistics of each accepted row for 2-byte logits (16-byte
+// chunk = 8 tokens = one byte of a mask word): out[k] = mixed chunks << 32 |
+// their masked elements.  The fused apply's per-key policy (node_info.w bit
+// 30, header flag 4) is decided from it on the host.
+__global__ void row_mixstats_kernel(const uint32_t* __restrict__ rows, int32_t W, int32_t n,
+                                    int64_t* __restrict__ out) {
+  const int32_t k = blockIdx.x;
+  if (k >= n) return;
+  unsigned long long mix = 0, nel = 0;
+  for (int32_t w = threadIdx.x; w < W; w += blockDim.x) {
+    const uint32_t x = rows[(size_t)k * W + w];
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t c = (x >> (8 * b)) & 0xFFu;
+      if (c != 0u && c != 0xFFu) {
+        ++mix;
+        nel += 8 - __popc(c);
+      }
+    }
+  }
+  unsigned long long v = (mix << 32) | nel;
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __shared__ unsigned long long part[32];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += part[i];
+    out[k] = (int64_t)t;
+  }
+}
+
 // Sorted id lists of the dependent rows (REF cache.py:400-402 sorts them).
 // One CTA per key: every thread counts the set bits of a contiguous run of
 // words, a block-wide exclusive scan gives each run its output offset, and
@@ -300,6 +331,12 @@ gm_status launch_cache_build(const DevGrammar& G, const DevVocab& V, const DevAr
 gm_status launch_row_popcount(const uint32_t* rows, int32_t W, int32_t n, int64_t* out, cudaStream_t s) {
   if (n <= 0) return GM_OK;
   row_popcount_kernel<<<n, 256, 0, s>>>(rows, W, n, out);
+  GM_LAUNCH_CHECK();
+  return GM_OK;
+}
+gm_status launch_row_mixstats(const uint32_t* rows, int32_t W, int32_t n, int64_t* out, cudaStream_t s) {
+  if (n <= 0) return GM_OK;
+  row_mixstats_kernel<<<n, 256, 0, s>>>(rows, W, n, out);
   GM_LAUNCH_CHECK();
   return GM_OK;
 }

@@ -29,16 +29,13 @@
 namespace gm {
 
 constexpr int kFillThreads = 512;
-// The fused apply's mixed-chunk blend (K0's policy) is compiled in only with
-// -DGM_FILL_BLEND=1: measured K5 SQL 43.9 -> 37.9 us/step but XML 19.7 ->
-// 23.0 and JSON +0.7 (the policy check alone), so the fused apply keeps the
-// element stores; K0 applies the policy (per tile, default 528).
-#ifndef GM_FILL_BLEND
-#define GM_FILL_BLEND 0
-#endif
-#ifndef GM_FILL_BLEND_DEFAULT
-#define GM_FILL_BLEND_DEFAULT 528
-#endif
+// The fused apply's mixed-chunk policy is decided per cache key at build
+// (gm_cache_create: K0's thresholds, gm_apply_set_blend, over the key's
+// accepted row) and rides in the slot header (flag 4).
+// (Measured and rejected: a per-warp-round decision inside the apply loop,
+// K5 SQL 43.9 -> 37.9 us/step but XML 19.7 -> 23.0 and JSON +0.7 from the
+// per-round ballots; per-row statistics gathered by the merge, +0.3-0.6 us
+// on JSON even sampled 1 word in 8.)
 constexpr int kTmaRows = 4;     // tops whose rows are TMA-staged (more: direct loads)
 constexpr int kDepS = 16;
 constexpr int kDepF = 64;
@@ -67,18 +64,16 @@ constexpr bool kTimeline = true;
 constexpr bool kTimeline = false;
 #endif
 
-// Mixed-chunk policy of the fused apply (same encoding as K0's, whose
-// setter gm_apply_set_blend also updates this copy); read at run time, so a
-// captured graph follows the switch.
-__device__ int g_fill_blend = GM_FILL_BLEND_DEFAULT;
 
 // K3/K5 tail: mask one logits row in place from the finished mask words in
 // shared memory (coalesced 16-byte chunks, -inf only where masked, logits
-// never read; mixed chunks store just their masked elements).  EB = bytes
-// per logit as a template parameter: the chunk arithmetic is shifts and
-// masks.  (Measured and rejected: K0's warp-tile scheme here, 0.3 us/step
-// slower — the block-contiguous chunk order streams better from one SM.)
-template <int EB>
+// never read; mixed chunks store just their masked elements, or — `blend`,
+// decided per row from its mask statistics — are loaded, blended and stored
+// whole).  EB = bytes per logit as a template parameter: the chunk arithmetic
+// is shifts and masks.  (Measured and rejected: K0's warp-tile scheme here,
+// 0.3 us/step slower — the block-contiguous chunk order streams better from
+// one SM.)
+template <int EB, bool BLEND>
 __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint32_t* __restrict__ words,
                                             int64_t tok_lo, int64_t tok_hi, uint32_t neg) {
   // words[] holds the mask from token tok_lo (a multiple of 128) on
@@ -92,29 +87,13 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
     uint32_t keep = (words[t0 >> 5] >> (t0 & 31)) & full;
     const bool tail = t0 + vec > lim;
     if (tail) keep |= full & ~((1u << (lim - t0)) - 1u);
-    // the K0 mixed-chunk policy (k_apply.cu apply_tile), per 32-chunk round
-    // of the warp: blend when at least (policy & 0xFF) / 2 of its chunks are
-    // mixed with at least (policy >> 8) masked elements each on average
-    bool dense_mixed = false;
-#if GM_FILL_BLEND
-    const int policy = g_fill_blend;
-    const unsigned am = __activemask();
-    const bool mixed = keep != 0 && keep != full;
-    if (policy > 0 && __any_sync(am, mixed)) {
-      const int nmix = __popc(__ballot_sync(am, mixed));
-      if (2 * nmix >= (policy & 0xFF)) {
-        const int nel = (int)__reduce_add_sync(am, mixed ? (unsigned)__popc(~keep & full) : 0u);
-        dense_mixed = nel >= ((policy >> 8) & 0xFF) * nmix;
-      }
-    }
-#endif
     if (keep == full) continue;
     char* p = base + t0 * EB;
     if (keep == 0) {
       st_cs_v4(p, neg);
-    } else if (!tail && dense_mixed) {  // many mixed chunks here: load, blend, one full store each
+    } else if (BLEND && !tail) {  // dense, heavily masked mixed chunks: load, blend, one full store
       blend_chunk<EB>(p, keep, neg);
-    } else {  // the span's last chunk: element stores, nothing past its end
+    } else {  // element stores, nothing past the span's end
       uint32_t m = ~keep & full;
       while (m) {
         const int j = __ffs(m) - 1;
@@ -126,10 +105,20 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
   }
 }
 
+// the blend instantiation out of line: only rows the policy picks call it,
+// and the inline element-store path keeps its code layout
+__device__ __noinline__ void apply_row_blend2(char* rowp, const uint32_t* words, int64_t tok_lo, int64_t tok_hi,
+                                              uint32_t neg) {
+  apply_row_t<2, true>(rowp, words, tok_lo, tok_hi, neg);
+}
+
 __device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_t* __restrict__ words, int64_t tok_lo,
-                                          int64_t tok_hi, int eb, uint32_t neg) {
-  if (eb == 4) apply_row_t<4>(rowp, words, tok_lo, tok_hi, neg);
-  else apply_row_t<2>(rowp, words, tok_lo, tok_hi, neg);
+                                          int64_t tok_hi, int eb, uint32_t neg, bool blend = false) {
+  // one instantiation per policy: the element-store loop stays as tight as
+  // without the blend path (measured +0.3 us/step on JSON with a runtime flag)
+  if (eb == 4) apply_row_t<4, false>(rowp, words, tok_lo, tok_hi, neg);
+  else if (blend) apply_row_blend2(rowp, words, tok_lo, tok_hi, neg);
+  else apply_row_t<2, false>(rowp, words, tok_lo, tok_hi, neg);
 }
 
 // Caller index of a top's parent frame within the callers of the top's
@@ -905,7 +894,9 @@ fill_body(DevPool P, const int32_t* __restrict__ slots, int32_t n, uint32_t* __r
   // row still masks logits columns in [V, vocab) (their bits are zero, as
   // gm_apply_inplace treats them)
   if (APPLY && !overlap && (s_partial || ap_vocab > (int64_t)hd.V)) {
-    if (t_hi > t_lo) apply_row(logits + row * lstride_bytes, dep_acc, t_lo, t_hi, ap_eb, ap_neg);
+    // the per-key mixed-chunk policy (header flag 4, decided at cache build)
+    const bool blend = hd.flags & 4;
+    if (t_hi > t_lo) apply_row(logits + row * lstride_bytes, dep_acc, t_lo, t_hi, ap_eb, ap_neg, blend);
   }
   if (do_acc && threadIdx.x >= 64 && threadIdx.x < 96 && s_spec.n > 0) {  // warp 2: verify the deferred commit
     const bool bad = spec_mine && spec_old != kEmptyKey && spec_old != s_spec.key[spec_lane];
@@ -1128,11 +1119,4 @@ gm_status launch_step_ptok(const DevPool& P, const int32_t* host_slots, int32_t 
 #undef GM_PTOK
 }
 
-}  // namespace gm
-
-namespace gm {
-gm_status set_fill_blend(int32_t policy) {
-  GM_CUDA_TRY(cudaMemcpyToSymbol(g_fill_blend, &policy, sizeof(policy)));
-  return GM_OK;
-}
 }  // namespace gm

@@ -132,6 +132,7 @@ class DeviceCache:
             "dependent_total": stats.dependent_total,
             "rejected_total": stats.rejected_total,
             "row_bytes": stats.row_bytes,
+            "blend_keys": stats.blend_keys,  # rows the fused apply blends (mixed-chunk policy)
         }
 
     def export(self):

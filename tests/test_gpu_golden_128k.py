@@ -78,6 +78,10 @@ def test_k5_batch32_matches_reference(grammar):
     compiled = gm.GrammarCompiler(info).compile_grammar(fx["grammars"][grammar]["text"])
     trajs = fx["grammars"][grammar]["trajectories"]
     assert len(trajs) == 32
+    # the fused apply's per-key mixed-chunk policy: SQL's identifier-class
+    # rows are applied blended, so the logits check below covers that path
+    if grammar == "sql":
+        assert compiled._dev.cache.stats["blend_keys"] > 0
     n = replay_k5([compiled] * len(trajs), trajs, logits=grammar in ("json", "sql"))
     assert n == sum(len(t["masks"]) for t in trajs)
 

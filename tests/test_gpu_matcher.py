@@ -308,7 +308,8 @@ def test_fused_fill_apply_equals_separate(grammar, dtype, B):
     bit for bit, along a trajectory (B = 6: several CTAs per request, each
     with its word range; B = 100: one CTA per request; the SQL grammar's
     identifier-class masks take K0's load-blend-store path for dense mixed
-    chunks while the fused apply stores only the masked elements)."""
+    chunks, and the fused apply blends the rows of the keys its per-key
+    policy flagged at build)."""
     import torch
 
     import paper_2411_15100_b200 as gm

@@ -101,17 +101,23 @@ def main(S=48, grammar="json"):
             row["accept_by_kind"].setdefault(key, []).append(round(t, 2))
         ends = sorted((x[7] - t0) / 1e3 for x in recs)
         row["cta_end_p50_max"] = (round(ends[len(ends) // 2], 2), round(ends[-1], 2))
+        # when each CTA's apply can start (its merged words are final)
+        ready = sorted((x[6] - t0) / 1e3 for x in recs if x[6])
+        if ready:
+            row["apply_start_p10_p50_p90_max"] = tuple(round(ready[min(len(ready) - 1, int(q * len(ready)))], 2)
+                                                       for q in (0.1, 0.5, 0.9, 1.0))
         walked = [(x[10] >> 40) & 0xFFFF for x in recs]
         row["deps_walked_mean_max"] = (round(sum(walked) / len(walked), 1), max(walked))
         out.append(row)
-    keys = ["span_us", "gap_to_next_us", "launch_to_first_start_us", "next_resident_before_end_us"] + PH
+    keys = ["span_us", "gap_to_next_us", "launch_to_first_start_us", "next_resident_before_end_us"] + PH + [
+        "cta_end_p50_max", "apply_start_p10_p50_p90_max"]
     summ = {}
     for k in keys:
         vals = [r[k] for r in out if k in r]
         if not vals:
             continue
         if isinstance(vals[0], tuple):
-            summ[k] = (round(statistics.median(v[0] for v in vals), 2), round(statistics.median(v[1] for v in vals), 2))
+            summ[k] = tuple(round(statistics.median(v[j] for v in vals), 2) for j in range(len(vals[0])))
         else:
             summ[k] = round(statistics.median(vals), 2)
     print(json.dumps({"launches": len(out), "median_over_launches": summ, "per_launch": out}))

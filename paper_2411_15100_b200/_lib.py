@@ -172,7 +172,7 @@ def load() -> C.CDLL:
         fn.restype = res
     _lib = lib
     if os.environ.get("GMASK_APPLY_BLEND") and hasattr(lib, "gm_apply_set_blend"):
-        lib.gm_apply_set_blend(int(os.environ["GMASK_APPLY_BLEND"]))  # K0 and the fused apply
+        lib.gm_apply_set_blend(int(os.environ["GMASK_APPLY_BLEND"]))  # K0, and the fused apply of caches built later
     return lib
 
 

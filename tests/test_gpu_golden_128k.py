@@ -86,6 +86,28 @@ def test_k5_batch32_matches_reference(grammar):
     assert n == sum(len(t["masks"]) for t in trajs)
 
 
+def test_k5_sql_fused_apply_policy_off():
+    """The fused apply's per-key policy follows gm_apply_set_blend at cache
+    build: with the policy off no SQL key is blended and the element-store
+    apply of the same golden trajectories is exact too."""
+    import paper_2411_15100_b200 as gm
+    from paper_2411_15100_b200 import _lib
+
+    fx = fixture()
+    vocab = vocab_by_name(fx["vocab"])
+    lib = _lib.load()
+    old = lib.gm_apply_set_blend(0)
+    try:
+        compiled = gm.GrammarCompiler(gm.TokenizerInfo.from_vocabulary(vocab)).compile_grammar(
+            fx["grammars"]["sql"]["text"])
+    finally:
+        lib.gm_apply_set_blend(old)
+    assert compiled._dev.cache.stats["blend_keys"] == 0
+    trajs = fx["grammars"]["sql"]["trajectories"]
+    n = replay_k5([compiled] * len(trajs), trajs, logits=True)
+    assert n == sum(len(t["masks"]) for t in trajs)
+
+
 def test_k5_config5_distinct_schemas_one_batch():
     """Config 5: 16 mutated schemas x 2 trajectories, each request with its
     own compiled grammar, one K5 launch per step."""

@@ -73,15 +73,57 @@ constexpr bool kTimeline = false;
 // is shifts and masks.  (Measured and rejected: K0's warp-tile scheme here,
 // 0.3 us/step slower — the block-contiguous chunk order streams better from
 // one SM.)
+#ifndef GM_LEAN_APPLY
+#define GM_LEAN_APPLY 1
+#endif
 template <int EB, bool BLEND>
 __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint32_t* __restrict__ words,
                                             int64_t tok_lo, int64_t tok_hi, uint32_t neg) {
   // words[] holds the mask from token tok_lo (a multiple of 128) on
   constexpr int vec = 16 / EB;
+  constexpr int cpw = 32 / vec;  // chunks per mask word
   constexpr uint32_t full = (1u << vec) - 1u;
   const int32_t lim = (int32_t)(tok_hi - tok_lo);  // tokens of this span (< 2^31)
-  const int32_t chunks = (lim + vec - 1) / vec;
+  const int32_t whole = lim / vec;                 // chunks entirely inside the span
   char* base = rowp + tok_lo * EB;
+#if GM_LEAN_APPLY
+  // the per-chunk work kept minimal (the per-SM apply rate is partly issue
+  // bound): no tail test, word index and shift from the chunk index, the
+  // chunk pointer advanced by a constant
+  const int32_t stride = (int32_t)blockDim.x;
+  char* p = base + (int64_t)threadIdx.x * 16;
+  const int64_t pstep = (int64_t)stride * 16;
+  for (int32_t c = threadIdx.x; c < whole; c += stride, p += pstep) {
+    const uint32_t keep = (words[c / cpw] >> ((c % cpw) * vec)) & full;
+    if (keep == full) continue;
+    if (keep == 0) {
+      st_cs_v4(p, neg);
+    } else if (BLEND) {
+      blend_chunk<EB>(p, keep, neg);
+    } else {
+      uint32_t m = ~keep & full;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        if (EB == 4) st_cs_u32(p + j * 4, neg);
+        else st_cs_u16(p + j * 2, neg);
+      }
+    }
+  }
+  if (whole * vec < lim && threadIdx.x == (unsigned)(whole % stride)) {  // the ragged last chunk
+    const int32_t t0 = whole * vec;
+    const uint32_t keep = ((words[t0 >> 5] >> (t0 & 31)) & full) | (full & ~((1u << (lim - t0)) - 1u));
+    uint32_t m = ~keep & full;
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      if (EB == 4) st_cs_u32(base + (int64_t)t0 * EB + j * 4, neg);
+      else st_cs_u16(base + (int64_t)t0 * EB + j * 2, neg);
+    }
+  }
+#else
+  const int32_t chunks = (lim + vec - 1) / vec;
+  (void)whole;
   for (int32_t c = threadIdx.x; c < chunks; c += blockDim.x) {
     const int32_t t0 = c * vec;  // relative to tok_lo
     uint32_t keep = (words[t0 >> 5] >> (t0 & 31)) & full;
@@ -103,6 +145,7 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
       }
     }
   }
+#endif
 }
 
 // The blended apply (2-byte logits), out of line: only rows the per-key

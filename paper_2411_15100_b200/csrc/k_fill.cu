@@ -67,29 +67,25 @@ constexpr bool kTimeline = false;
 
 // K3/K5 tail: mask one logits row in place from the finished mask words in
 // shared memory (coalesced 16-byte chunks, -inf only where masked, logits
-// never read; mixed chunks store just their masked elements, or — `blend`,
-// decided per row from its mask statistics — are loaded, blended and stored
-// whole).  EB = bytes per logit as a template parameter: the chunk arithmetic
-// is shifts and masks.  (Measured and rejected: K0's warp-tile scheme here,
+// never read; mixed chunks store just their masked elements, or — rows of
+// keys the per-key policy flagged, apply_row_blend2 — are loaded, blended and
+// stored whole).  EB = bytes per logit as a template parameter: the chunk
+// arithmetic is shifts and masks.  (Measured and rejected: K0's warp-tile scheme here,
 // 0.3 us/step slower — the block-contiguous chunk order streams better from
 // one SM.)
-#ifndef GM_LEAN_APPLY
-#define GM_LEAN_APPLY 1
-#endif
-template <int EB, bool BLEND>
+template <int EB>
 __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint32_t* __restrict__ words,
                                             int64_t tok_lo, int64_t tok_hi, uint32_t neg) {
-  // words[] holds the mask from token tok_lo (a multiple of 128) on
+  // words[] holds the mask from token tok_lo (a multiple of 128) on.  The
+  // per-chunk work is kept minimal: no tail test (the ragged last chunk is
+  // handled apart), word index and shift from the chunk index, the chunk
+  // pointer advanced by a constant (XML K5 16.94 -> 16.81 us/step).
   constexpr int vec = 16 / EB;
   constexpr int cpw = 32 / vec;  // chunks per mask word
   constexpr uint32_t full = (1u << vec) - 1u;
   const int32_t lim = (int32_t)(tok_hi - tok_lo);  // tokens of this span (< 2^31)
   const int32_t whole = lim / vec;                 // chunks entirely inside the span
   char* base = rowp + tok_lo * EB;
-#if GM_LEAN_APPLY
-  // the per-chunk work kept minimal (the per-SM apply rate is partly issue
-  // bound): no tail test, word index and shift from the chunk index, the
-  // chunk pointer advanced by a constant
   const int32_t stride = (int32_t)blockDim.x;
   char* p = base + (int64_t)threadIdx.x * 16;
   const int64_t pstep = (int64_t)stride * 16;
@@ -98,9 +94,7 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
     if (keep == full) continue;
     if (keep == 0) {
       st_cs_v4(p, neg);
-    } else if (BLEND) {
-      blend_chunk<EB>(p, keep, neg);
-    } else {
+    } else {  // mixed: only the masked elements
       uint32_t m = ~keep & full;
       while (m) {
         const int j = __ffs(m) - 1;
@@ -121,31 +115,6 @@ __device__ __forceinline__ void apply_row_t(char* __restrict__ rowp, const uint3
       else st_cs_u16(base + (int64_t)t0 * EB + j * 2, neg);
     }
   }
-#else
-  const int32_t chunks = (lim + vec - 1) / vec;
-  (void)whole;
-  for (int32_t c = threadIdx.x; c < chunks; c += blockDim.x) {
-    const int32_t t0 = c * vec;  // relative to tok_lo
-    uint32_t keep = (words[t0 >> 5] >> (t0 & 31)) & full;
-    const bool tail = t0 + vec > lim;
-    if (tail) keep |= full & ~((1u << (lim - t0)) - 1u);
-    if (keep == full) continue;
-    char* p = base + t0 * EB;
-    if (keep == 0) {
-      st_cs_v4(p, neg);
-    } else if (BLEND && !tail) {  // dense, heavily masked mixed chunks: load, blend, one full store
-      blend_chunk<EB>(p, keep, neg);
-    } else {  // element stores, nothing past the span's end
-      uint32_t m = ~keep & full;
-      while (m) {
-        const int j = __ffs(m) - 1;
-        m &= m - 1;
-        if (EB == 4) st_cs_u32(p + j * 4, neg);
-        else st_cs_u16(p + j * 2, neg);
-      }
-    }
-  }
-#endif
 }
 
 // The blended apply (2-byte logits), out of line: only rows the per-key
@@ -216,11 +185,11 @@ __device__ __noinline__ void apply_row_blend2(char* rowp, const uint32_t* words,
 
 __device__ __forceinline__ void apply_row(char* __restrict__ rowp, const uint32_t* __restrict__ words, int64_t tok_lo,
                                           int64_t tok_hi, int eb, uint32_t neg, bool blend = false) {
-  // one instantiation per policy: the element-store loop stays as tight as
-  // without the blend path (measured +0.3 us/step on JSON with a runtime flag)
-  if (eb == 4) apply_row_t<4, false>(rowp, words, tok_lo, tok_hi, neg);
+  // the blend path out of line: the element-store loop stays as tight as
+  // without it (measured +0.3 us/step on JSON with a runtime flag in the loop)
+  if (eb == 4) apply_row_t<4>(rowp, words, tok_lo, tok_hi, neg);
   else if (blend) apply_row_blend2(rowp, words, tok_lo, tok_hi, neg);
-  else apply_row_t<2, false>(rowp, words, tok_lo, tok_hi, neg);
+  else apply_row_t<2>(rowp, words, tok_lo, tok_hi, neg);
 }
 
 // Caller index of a top's parent frame within the callers of the top's
